@@ -1,0 +1,177 @@
+/* pf_b200.h — C ABI of the B200-native pose-parsing hot path.
+ *
+ * The reference (poseflow, /root/reference/pkg/src/poseflow) is pure
+ * Python; it has no FFI of its own.  This ABI replaces, one-for-one, the
+ * functions on its hot path:
+ *
+ *   pf_parse_device / pf_parse_host  <- paf.parse                (paf.py:292-305)
+ *                                        incl. nms_peaks           (paf.py:74-109)
+ *                                        connect_limbs/score_limb  (paf.py:112-199)
+ *                                        assemble_humans           (paf.py:210-289)
+ *                                        cell_to_pixel             (types.py:233-235)
+ *   pf_params                        <- ParserParams               (paf.py:34-54)
+ *   pf_set_topology                  <- SkeletonTopology           (types.py:81-166)
+ *   pf_preprocess_device             <- make_preprocess.fn         (operators.py:114-131)
+ *                                        + read_ppm u8/255         (formats.py:116-117)
+ *                                        + bilinear_resize 3-D     (operators.py:79-107)
+ *   pf_resize_device                 <- bilinear_resize 2-D, per channel (operators.py:79-107)
+ *
+ * Plain pointers and sizes only; no torch types.  The Python host layer
+ * (paper_2108_11826_b200.parser / .pipeline_ops) binds this with ctypes and
+ * mirrors the reference API; INTEGRATION.md shows the binding a poseflow
+ * maintainer would add.
+ *
+ * Status codes map onto the reference exception hierarchy (errors.py):
+ *   PF_ERR_CONFIG   -> ConfigError   (raised before any work, like paf.py:295)
+ *   PF_ERR_CONTRACT -> ContractError (types.py:185-205, operators.py:83, :121)
+ *   PF_ERR_CAPACITY -> a frame exceeded a capacity; never silently truncated
+ *   PF_ERR_CUDA     -> CUDA runtime failure
+ * pf_last_error() returns the message of the last failing call.
+ *
+ * Threading: one pf_ctx per (device, stream).  Distinct contexts may be
+ * used concurrently from different threads; one context is not reentrant.
+ * Device entry points are asynchronous on the context stream; results are
+ * valid after pf_sync()/pf_get_results().
+ */
+#ifndef PF_B200_H
+#define PF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_ERR_CONFIG 1
+#define PF_ERR_CONTRACT 2
+#define PF_ERR_CAPACITY 3
+#define PF_ERR_CUDA 4
+
+#define PF_MAX_KEYPOINTS 32
+#define PF_MAX_LIMBS 64
+#define PF_ABI_VERSION 1
+
+typedef struct pf_ctx pf_ctx;
+
+/* ParserParams (paf.py:34-42) plus two B200-path knobs:
+ *   upsample   — 1: parse on the feature grid (the reference as-is);
+ *                u>1: every map is bilinear-resized x u (operators.py:79-107)
+ *                before parsing, coordinates in grid*u space (stride/u).
+ *   blur_sigma — 0: off (identity).  >0: separable Gaussian on the part
+ *                confidence maps after upsampling (no reference). */
+typedef struct pf_params {
+    double conf_threshold;        /* [0,1], compared in fp32 (numpy NEP 50) */
+    int32_t nms_window;           /* odd, >= 3 */
+    int32_t n_samples;            /* >= 2 */
+    double sample_dot_threshold;  /* [0,1] */
+    double good_fraction_min;     /* [0,1] */
+    int32_t min_parts;            /* >= 1 */
+    double min_human_score;
+    int32_t upsample;             /* >= 1, stride % upsample == 0 */
+    double blur_sigma;            /* >= 0 */
+} pf_params;
+
+/* Capacities of the context workspaces (0 = default).  Exceeding one sets
+ * PF_ERR_CAPACITY for the call with the offending frame index. */
+typedef struct pf_caps {
+    int32_t max_peaks_per_part;    /* default 128 */
+    int32_t max_peaks_per_frame;   /* default 1024 */
+    int32_t max_candidates;        /* gated candidate pairs per frame, default 4096 */
+    int32_t max_humans_per_frame;  /* builders per frame before filtering, default 256 */
+    int32_t chunk_frames;          /* frames per internal launch chunk, default 1024 */
+    int32_t max_humans_total;      /* output pool per call, default 64 * batch */
+} pf_caps;
+
+/* Results of the last parse call, in context-owned pinned host memory,
+ * valid until the next parse on the same context.  Humans of frame f are
+ * entries frame_first[f] .. frame_first[f] + frame_count[f] - 1, already in
+ * the reference output order (score descending, stable, paf.py:288). */
+typedef struct pf_results {
+    int32_t n_frames;
+    int32_t n_keypoints;
+    int32_t total_humans;
+    const int32_t *frame_first;    /* [n_frames] */
+    const int32_t *frame_count;    /* [n_frames] */
+    const double *human_score;     /* [total] */
+    const int32_t *human_n_parts;  /* [total] */
+    const double *kp_x;            /* [total * K]  cell_to_pixel x */
+    const double *kp_y;            /* [total * K] */
+    const float *kp_score;         /* [total * K]  peak value (fp32) */
+    const int32_t *kp_peak;        /* [total * K]  per-frame peak id, -1 = absent */
+} pf_results;
+
+int pf_abi_version(void);
+
+int pf_create(pf_ctx **out, int device, const pf_caps *caps);
+void pf_destroy(pf_ctx *ctx);
+const char *pf_last_error(const pf_ctx *ctx);
+
+/* Bind the context to a CUDA stream (cudaStream_t passed as void*);
+ * NULL = the context's own non-blocking stream. */
+int pf_set_stream(pf_ctx *ctx, void *cuda_stream);
+
+/* SkeletonTopology (types.py:81-166): limbs and paf_channels are [L][2]. */
+int pf_set_topology(pf_ctx *ctx, int n_keypoints, int n_limbs,
+                    const int32_t *limbs, const int32_t *paf_channels);
+
+/* ParserParams.validate (paf.py:44-54) + the two extension knobs. */
+int pf_validate_params(const pf_params *p);
+
+/* Parse `batch` frames whose maps are resident on the device:
+ * conf [batch][K+1][grid_h][grid_w], paf [batch][2L][grid_h][grid_w],
+ * contiguous f32 (FeatureMaps layout, types.py:169-205).  Asynchronous. */
+int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch,
+                    int grid_h, int grid_w, int stride, const pf_params *p);
+
+/* Same, from HOST buffers (pinned for full overlap): H2D copies are
+ * chunked and overlapped with the kernels; returns after results are on
+ * the host (implies pf_get_results). */
+int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch,
+                  int grid_h, int grid_w, int stride, const pf_params *p,
+                  pf_results *out);
+
+/* Wait for the last parse and expose its results (D2H of the compact pool). */
+int pf_get_results(pf_ctx *ctx, pf_results *out);
+
+/* Wait for all work on the context stream. */
+int pf_sync(pf_ctx *ctx);
+
+/* Stage intermediates of the last parse for per-stage parity checks
+ * (requires pf_set_debug(ctx, 1) before the parse).  Peaks in id order:
+ * part, row, col, score; connections in connect_limbs order: limb, id_a,
+ * id_b, score, good_fraction.  Returns counts through n_*; pass NULL
+ * arrays to query counts only. */
+int pf_set_debug(pf_ctx *ctx, int enable);
+int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,
+                 int32_t *col, float *score);
+int pf_get_connections(pf_ctx *ctx, int frame, int *n_conns, int32_t *limb,
+                       int32_t *id_a, int32_t *id_b, double *score, double *good);
+
+/* Pre-processing (operators.py:114-131): u8 HWC [batch][h][w][3] (device)
+ * -> f32 CHW [batch][3][out_h][out_w] (device).  Same size = layout only. */
+int pf_preprocess_device(pf_ctx *ctx, const uint8_t *src, int batch, int h, int w,
+                         float *dst, int out_h, int out_w);
+
+/* Same, for already-normalised f32 HWC frames (a reference Frame image,
+ * types.py:57-72): layout permutation or fp64 bilinear resize only. */
+int pf_preprocess_f32_device(pf_ctx *ctx, const float *src, int batch, int h, int w,
+                             float *dst, int out_h, int out_w);
+
+/* bilinear_resize 2-D branch per channel: [n_planes][in_h][in_w] ->
+ * [n_planes][out_h][out_w] (device). */
+int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int in_w,
+                     float *dst, int out_h, int out_w);
+
+/* Pinned host allocation helpers for callers without their own allocator. */
+void *pf_host_alloc(size_t bytes);
+void pf_host_free(void *p);
+
+/* Kernel launches issued by this context since creation (evidence counter). */
+int64_t pf_launch_count(const pf_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,912 @@
+// pf_capi.cu — the C ABI (include/pf_b200.h): context, workspaces, the
+// chunked launch sequence and the host<->device result path.
+//
+// Launch sequence per chunk of frames (device-resident maps):
+//   Mode R (upsample 1, no blur)   k_nms_plane  -> k_parse_frames
+//   Mode U (upsample u, no blur)   k_nms_up     -> k_parse_frames   (fused, default)
+//   blur or NMS window > 33        k_resize_planes -> k_blur_rows/cols
+//                                  -> k_nms_plane -> k_parse_frames
+// k_parse_frames resets the per-slab peak counters it consumed, so the
+// steady state needs no memset between chunks; one 32-byte memset clears
+// the status/pool counter per call.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pf_launch.h"
+
+using namespace pf;
+
+namespace {
+
+struct AxisCache {
+    int in_n = 0, out_n = 0;
+    std::vector<int32_t> i0, i1;
+    std::vector<double> t, omt;
+    int32_t *d_i0 = nullptr, *d_i1 = nullptr;
+    double *d_t = nullptr, *d_omt = nullptr;
+    AxisTab dev() const { return AxisTab{d_i0, d_i1, d_t, d_omt}; }
+};
+
+// operators.py:86-96, evaluated on the host in fp64 with the reference op
+// order (built with -ffp-contract=off: no FMA on the host side either).
+void fill_axis(AxisCache &a, int in_n, int out_n)
+{
+    a.in_n = in_n;
+    a.out_n = out_n;
+    a.i0.resize(out_n); a.i1.resize(out_n); a.t.resize(out_n); a.omt.resize(out_n);
+    const volatile double ratio = (double)in_n / (double)out_n;
+    for (int o = 0; o < out_n; ++o) {
+        const volatile double prod = ((double)o + 0.5) * ratio;
+        const double s = prod - 0.5;
+        const long long f = (long long)std::floor(s);
+        const double t = s - (double)f;
+        a.t[o] = t;
+        a.omt[o] = 1.0 - t;
+        a.i0[o] = (int32_t)(f < 0 ? 0 : (f > in_n - 1 ? in_n - 1 : f));
+        a.i1[o] = (int32_t)(f + 1 < 0 ? 0 : (f + 1 > in_n - 1 ? in_n - 1 : f + 1));
+    }
+}
+
+template <typename T>
+cudaError_t dev_alloc(T **p, size_t n)
+{
+    return cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T) + 16);
+}
+
+template <typename T>
+cudaError_t host_alloc(T **p, size_t n)
+{
+    return cudaHostAlloc(reinterpret_cast<void **>(p), n * sizeof(T) + 16, cudaHostAllocDefault);
+}
+
+}  // namespace
+
+struct pf_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    Topo topo{};
+    bool has_topo = false;
+    pf_caps caps{};
+    std::string err;
+    int debug = 0;
+    int64_t launches = 0;
+
+    // NMS workspace (chunk-sized)
+    int *d_counts = nullptr;
+    uint2 *d_peaks = nullptr;
+    size_t ws_frames = 0;
+    int ws_K = 0;
+
+    // resize tables, keyed by (in, out)
+    std::map<std::pair<int, int>, AxisCache> axes;
+
+    // outputs
+    int *d_frame_first = nullptr, *d_frame_count = nullptr;
+    int *h_frame_first = nullptr, *h_frame_count = nullptr;
+    size_t frames_cap = 0;
+    double *d_hscore = nullptr, *h_hscore = nullptr;
+    int *d_hnparts = nullptr, *h_hnparts = nullptr;
+    double *d_kpx = nullptr, *d_kpy = nullptr, *h_kpx = nullptr, *h_kpy = nullptr;
+    float *d_kps = nullptr, *h_kps = nullptr;
+    int *d_kpp = nullptr, *h_kpp = nullptr;
+    size_t pool_cap = 0;
+    int pool_K = 0;
+    Status *d_status = nullptr, *h_status = nullptr;
+
+    // materialised full-resolution workspace (blur / wide NMS window)
+    float *d_full = nullptr, *d_tmp = nullptr;
+    size_t full_elems = 0;
+
+    // host-path staging (double buffered)
+    float *d_in[2] = {nullptr, nullptr};
+    size_t in_elems = 0;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+
+    // debug slabs
+    int *d_dbg_np = nullptr, *d_dbg_nc = nullptr, *d_dbg_ci = nullptr;
+    int4 *d_dbg_peaks = nullptr;
+    double *d_dbg_cd = nullptr;
+    size_t dbg_frames = 0;
+
+    int last_batch = 0;
+    int last_K = 0;
+    bool results_ready = false;
+};
+
+namespace {
+
+thread_local std::string g_create_err;   // pf_create failures (no context yet)
+
+int fail(pf_ctx *c, int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    else g_create_err = buf;
+    return code;
+}
+
+#define CU(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(ctx, PF_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                              \
+    } while (0)
+
+int set_device(pf_ctx *ctx)
+{
+    CU(cudaSetDevice(ctx->device));
+    return PF_OK;
+}
+
+int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
+{
+    auto key = std::make_pair(in_n, out_n);
+    auto it = ctx->axes.find(key);
+    if (it == ctx->axes.end()) {
+        AxisCache a;
+        fill_axis(a, in_n, out_n);
+        CU(dev_alloc(&a.d_i0, out_n));
+        CU(dev_alloc(&a.d_i1, out_n));
+        CU(dev_alloc(&a.d_t, out_n));
+        CU(dev_alloc(&a.d_omt, out_n));
+        CU(cudaMemcpy(a.d_i0, a.i0.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(a.d_i1, a.i1.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(a.d_t, a.t.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(a.d_omt, a.omt.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
+        it = ctx->axes.emplace(key, std::move(a)).first;
+    }
+    *out = &it->second;
+    return PF_OK;
+}
+
+int ensure_nms_ws(pf_ctx *ctx, size_t frames, int K)
+{
+    if (frames <= ctx->ws_frames && K <= ctx->ws_K) return PF_OK;
+    cudaFree(ctx->d_counts);
+    cudaFree(ctx->d_peaks);
+    ctx->d_counts = nullptr;
+    ctx->d_peaks = nullptr;
+    const size_t f = frames > ctx->ws_frames ? frames : ctx->ws_frames;
+    const int k = K > ctx->ws_K ? K : ctx->ws_K;
+    CU(dev_alloc(&ctx->d_counts, f * k));
+    CU(cudaMemset(ctx->d_counts, 0, f * k * sizeof(int)));
+    CU(dev_alloc(&ctx->d_peaks, f * k * (size_t)ctx->caps.max_peaks_per_part));
+    ctx->ws_frames = f;
+    ctx->ws_K = k;
+    return PF_OK;
+}
+
+int ensure_frames(pf_ctx *ctx, size_t frames)
+{
+    if (frames <= ctx->frames_cap) return PF_OK;
+    cudaFree(ctx->d_frame_first); cudaFree(ctx->d_frame_count);
+    cudaFreeHost(ctx->h_frame_first); cudaFreeHost(ctx->h_frame_count);
+    CU(dev_alloc(&ctx->d_frame_first, frames));
+    CU(dev_alloc(&ctx->d_frame_count, frames));
+    CU(host_alloc(&ctx->h_frame_first, frames));
+    CU(host_alloc(&ctx->h_frame_count, frames));
+    ctx->frames_cap = frames;
+    return PF_OK;
+}
+
+int ensure_pool(pf_ctx *ctx, size_t humans, int K)
+{
+    if (humans <= ctx->pool_cap && K <= ctx->pool_K) return PF_OK;
+    const size_t n = humans > ctx->pool_cap ? humans : ctx->pool_cap;
+    const int k = K > ctx->pool_K ? K : ctx->pool_K;
+    cudaFree(ctx->d_hscore); cudaFree(ctx->d_hnparts); cudaFree(ctx->d_kpx);
+    cudaFree(ctx->d_kpy); cudaFree(ctx->d_kps); cudaFree(ctx->d_kpp);
+    cudaFreeHost(ctx->h_hscore); cudaFreeHost(ctx->h_hnparts); cudaFreeHost(ctx->h_kpx);
+    cudaFreeHost(ctx->h_kpy); cudaFreeHost(ctx->h_kps); cudaFreeHost(ctx->h_kpp);
+    CU(dev_alloc(&ctx->d_hscore, n));
+    CU(dev_alloc(&ctx->d_hnparts, n));
+    CU(dev_alloc(&ctx->d_kpx, n * k));
+    CU(dev_alloc(&ctx->d_kpy, n * k));
+    CU(dev_alloc(&ctx->d_kps, n * k));
+    CU(dev_alloc(&ctx->d_kpp, n * k));
+    CU(host_alloc(&ctx->h_hscore, n));
+    CU(host_alloc(&ctx->h_hnparts, n));
+    CU(host_alloc(&ctx->h_kpx, n * k));
+    CU(host_alloc(&ctx->h_kpy, n * k));
+    CU(host_alloc(&ctx->h_kps, n * k));
+    CU(host_alloc(&ctx->h_kpp, n * k));
+    ctx->pool_cap = n;
+    ctx->pool_K = k;
+    return PF_OK;
+}
+
+int ensure_debug(pf_ctx *ctx, size_t frames)
+{
+    if (!ctx->debug || frames <= ctx->dbg_frames) return PF_OK;
+    cudaFree(ctx->d_dbg_np); cudaFree(ctx->d_dbg_nc); cudaFree(ctx->d_dbg_ci);
+    cudaFree(ctx->d_dbg_peaks); cudaFree(ctx->d_dbg_cd);
+    CU(dev_alloc(&ctx->d_dbg_np, frames));
+    CU(dev_alloc(&ctx->d_dbg_nc, frames));
+    CU(dev_alloc(&ctx->d_dbg_peaks, frames * (size_t)ctx->caps.max_peaks_per_frame));
+    CU(dev_alloc(&ctx->d_dbg_ci, frames * (size_t)ctx->caps.max_candidates * 3));
+    CU(dev_alloc(&ctx->d_dbg_cd, frames * (size_t)ctx->caps.max_candidates * 2));
+    ctx->dbg_frames = frames;
+    return PF_OK;
+}
+
+int ensure_full(pf_ctx *ctx, size_t elems)
+{
+    if (elems <= ctx->full_elems) return PF_OK;
+    cudaFree(ctx->d_full);
+    cudaFree(ctx->d_tmp);
+    CU(dev_alloc(&ctx->d_full, elems));
+    CU(dev_alloc(&ctx->d_tmp, elems));
+    ctx->full_elems = elems;
+    return PF_OK;
+}
+
+int validate_params_impl(pf_ctx *ctx, const pf_params *p)
+{
+    if (!p) return fail(ctx, PF_ERR_CONFIG, "params is NULL");
+    // paf.py:44-54
+    if (p->nms_window < 3 || p->nms_window % 2 == 0)
+        return fail(ctx, PF_ERR_CONFIG, "nms_window must be odd and >= 3");
+    if (p->n_samples < 2) return fail(ctx, PF_ERR_CONFIG, "n_samples must be >= 2");
+    const double v[3] = {p->conf_threshold, p->sample_dot_threshold, p->good_fraction_min};
+    const char *names[3] = {"conf_threshold", "sample_dot_threshold", "good_fraction_min"};
+    for (int k = 0; k < 3; ++k)
+        if (!(0.0 <= v[k] && v[k] <= 1.0))
+            return fail(ctx, PF_ERR_CONFIG, "%s must be in [0, 1], got %g", names[k], v[k]);
+    if (p->min_parts < 1) return fail(ctx, PF_ERR_CONFIG, "min_parts must be >= 1");
+    // extension knobs
+    if (p->upsample < 1) return fail(ctx, PF_ERR_CONFIG, "upsample must be >= 1");
+    if (!(p->blur_sigma >= 0.0) || !std::isfinite(p->blur_sigma))
+        return fail(ctx, PF_ERR_CONFIG, "blur_sigma must be finite and >= 0");
+    if (p->blur_sigma > 0.0 && (int)std::ceil(3.0 * p->blur_sigma) > kMaxBlurRadius)
+        return fail(ctx, PF_ERR_CONFIG, "blur_sigma too large (radius > %d)", kMaxBlurRadius);
+    if (p->n_samples > (1 << 24) - 1) return fail(ctx, PF_ERR_CONFIG, "n_samples too large for the GPU path");
+    return PF_OK;
+}
+
+// radius ceil(3 sigma), taps exp(-k^2 / (2 sigma^2)) normalised
+// by their sum accumulated in ascending k.
+void make_taps(double sigma, BlurTaps &t)
+{
+    const int r = (int)std::ceil(3.0 * sigma);
+    t.r = r;
+    double sum = 0.0;
+    for (int k = -r; k <= r; ++k) {
+        t.w[k + r] = std::exp(-(double)(k * k) / (2.0 * sigma * sigma));
+        sum += t.w[k + r];
+    }
+    for (int k = 0; k <= 2 * r; ++k) t.w[k] /= sum;
+}
+
+int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame_base,
+              int h, int w, int stride, const pf_params *p, AxisCache *rows, AxisCache *cols,
+              int pool_cap)
+{
+    const int K = ctx->topo.K, L = ctx->topo.L;
+    const int C = K + 1;
+    const int up = p->upsample;
+    const int H = h * up, W = w * up;
+    const int half = p->nms_window / 2;
+    const float thr = (float)p->conf_threshold;   // numpy NEP 50: fp32 compare
+    const bool blur = p->blur_sigma > 0.0;
+    cudaStream_t s = ctx->stream;
+
+    if (!blur && up == 1) {
+        CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
+                            ctx->d_counts, ctx->d_peaks, s));
+        ctx->launches += 1;
+    } else if (!blur && half <= kMaxFusedHalf) {
+        UpArgs a{};
+        a.conf = conf; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
+        a.rows = rows->dev(); a.cols = cols->dev();
+        a.thr = thr; a.half = half; a.cap = ctx->caps.max_peaks_per_part;
+        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+        // band height: keep the fp64 staging of the source rows <= 48 KB
+        int band = H;
+        auto src_rows = [&](int b0, int b1) {
+            const int lo = b0 - half < 0 ? 0 : b0 - half;
+            const int hi = b1 + half > H ? H : b1 + half;
+            return rows->i1[hi - 1] - rows->i0[lo] + 1;
+        };
+        while (band > 8 && (size_t)src_rows(0, band) * w * sizeof(double) > 48 * 1024) band = (band + 1) / 2;
+        band = ((band + 7) / 8) * 8;
+        if (band > H) band = H;
+        a.band_rows = band;
+        a.n_bands = (H + band - 1) / band;
+        int max_src = 0;
+        for (int bi = 0; bi < a.n_bands; ++bi) {
+            const int b0 = bi * band, b1 = b0 + band < H ? b0 + band : H;
+            const int ns = src_rows(b0, b1);
+            if (ns > max_src) max_src = ns;
+        }
+        const size_t smem = nms_up_smem(max_src, w, half, band, W);
+        CU(launch_nms_up(a, n, smem, s));
+        ctx->launches += 1;
+    } else {
+        // materialised: resize (if up > 1) -> blur (if sigma > 0) -> NMS
+        const size_t frame_full = (size_t)C * H * W;
+        int rc = ensure_full(ctx, (size_t)n * frame_full);
+        if (rc) return rc;
+        const float *nms_src = conf;
+        long long src_frame = (long long)C * h * w;
+        if (up > 1) {
+            CU(launch_resize_planes(conf, (long long)n * C, h, w, ctx->d_full, H, W, rows->dev(),
+                                    cols->dev(), ctx->sms, s));
+            ctx->launches += 1;
+            nms_src = ctx->d_full;
+            src_frame = (long long)frame_full;
+        }
+        if (blur) {
+            BlurTaps taps;
+            make_taps(p->blur_sigma, taps);
+            CU(launch_blur(nms_src, src_frame, ctx->d_tmp, ctx->d_full, (long long)frame_full, n, K,
+                           H, W, taps, ctx->sms, s));
+            ctx->launches += 2;
+            nms_src = ctx->d_full;
+        }
+        CU(launch_nms_plane(nms_src, n, C, K, H, W, thr, half, ctx->caps.max_peaks_per_part,
+                            ctx->d_counts, ctx->d_peaks, s));
+        ctx->launches += 1;
+    }
+
+    ParseArgs a{};
+    a.topo = ctx->topo;
+    a.paf = paf; a.h = h; a.w = w; a.up = up;
+    if (up > 1) { a.rows = rows->dev(); a.cols = cols->dev(); }
+    a.stride_eff = stride / up;
+    a.n_samples = p->n_samples;
+    a.dot_thr = p->sample_dot_threshold;
+    a.good_min = p->good_fraction_min;
+    a.min_score = p->min_human_score;
+    a.min_parts = p->min_parts;
+    a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+    a.cap_part = ctx->caps.max_peaks_per_part;
+    a.cap_frame = ctx->caps.max_peaks_per_frame;
+    a.cap_cands = ctx->caps.max_candidates;
+    a.cap_humans = ctx->caps.max_humans_per_frame;
+    a.frame_base = frame_base;
+    a.frame_first = ctx->d_frame_first; a.frame_count = ctx->d_frame_count;
+    a.h_score = ctx->d_hscore; a.h_nparts = ctx->d_hnparts;
+    a.kp_x = ctx->d_kpx; a.kp_y = ctx->d_kpy; a.kp_score = ctx->d_kps; a.kp_peak = ctx->d_kpp;
+    a.pool_cap = pool_cap;
+    a.st = ctx->d_status;
+    a.debug = ctx->debug;
+    a.dbg_npeaks = ctx->d_dbg_np; a.dbg_peaks = ctx->d_dbg_peaks;
+    a.dbg_nconns = ctx->d_dbg_nc; a.dbg_conn_i = ctx->d_dbg_ci; a.dbg_conn_d = ctx->d_dbg_cd;
+    const int threads = 256;
+    const size_t smem = parse_smem_bytes(a.cap_frame, a.cap_cands, a.cap_humans, K, threads / 32);
+    CU(launch_parse_frames(a, n, threads, smem, s));
+    ctx->launches += 1;
+    return PF_OK;
+}
+
+int check_call(pf_ctx *ctx, int batch, int grid_h, int grid_w, int stride, const pf_params *p)
+{
+    int rc = validate_params_impl(ctx, p);          // ConfigError first (paf.py:295)
+    if (rc) return rc;
+    if (!ctx->has_topo) return fail(ctx, PF_ERR_CONTRACT, "topology not set");
+    if (batch < 0) return fail(ctx, PF_ERR_CONTRACT, "batch must be >= 0");
+    if (grid_h < 0 || grid_w < 0) return fail(ctx, PF_ERR_CONTRACT, "grid extents must be >= 0");
+    if (stride < 1) return fail(ctx, PF_ERR_CONTRACT, "stride must be >= 1");   // types.py:194-195
+    if (stride % p->upsample != 0)
+        return fail(ctx, PF_ERR_CONTRACT, "stride %d not divisible by upsample %d", stride, p->upsample);
+    if ((long long)grid_h * p->upsample > 65535 || (long long)grid_w * p->upsample > 65535)
+        return fail(ctx, PF_ERR_CONTRACT, "parse grid exceeds 65535 cells per axis");
+    return PF_OK;
+}
+
+int begin_call(pf_ctx *ctx, int batch, int pool_cap)
+{
+    int rc = ensure_frames(ctx, batch > 0 ? batch : 1);
+    if (rc) return rc;
+    rc = ensure_pool(ctx, pool_cap > 0 ? pool_cap : 1, ctx->topo.K);
+    if (rc) return rc;
+    rc = ensure_debug(ctx, batch > 0 ? batch : 1);
+    if (rc) return rc;
+    // status: code 0, frame INT_MAX, pool_used 0
+    Status init{};
+    init.frame = 0x7fffffff;
+    *ctx->h_status = init;
+    CU(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->results_ready = false;
+    return PF_OK;
+}
+
+int pool_cap_for(pf_ctx *ctx, int batch)
+{
+    if (ctx->caps.max_humans_total > 0) return ctx->caps.max_humans_total;
+    long long v = 64LL * (batch > 0 ? batch : 1);
+    return (int)(v > (1LL << 30) ? (1LL << 30) : v);
+}
+
+int prepare_axes(pf_ctx *ctx, int h, int w, const pf_params *p, AxisCache **rows, AxisCache **cols)
+{
+    *rows = *cols = nullptr;
+    if (p->upsample > 1 && h > 0 && w > 0) {
+        int rc = get_axis(ctx, h, h * p->upsample, rows);
+        if (rc) return rc;
+        rc = get_axis(ctx, w, w * p->upsample, cols);
+        if (rc) return rc;
+    }
+    return PF_OK;
+}
+
+int chunk_for(pf_ctx *ctx, const pf_params *p, int h, int w)
+{
+    int chunk = ctx->caps.chunk_frames;
+    const bool materialise = p->blur_sigma > 0.0 ||
+                             (p->upsample > 1 && p->nms_window / 2 > kMaxFusedHalf);
+    if (materialise) {
+        // bound the full-resolution workspace to ~2 GiB
+        const size_t per = (size_t)(ctx->topo.K + 1) * h * w * p->upsample * p->upsample * sizeof(float);
+        size_t lim = per ? ((size_t)2 << 30) / per : chunk;
+        if (lim < 1) lim = 1;
+        if ((size_t)chunk > lim) chunk = (int)lim;
+    }
+    return chunk;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_abi_version(void) { return PF_ABI_VERSION; }
+
+int pf_create(pf_ctx **out, int device, const pf_caps *caps)
+{
+    if (!out) return fail(nullptr, PF_ERR_CONTRACT, "out is NULL");
+    *out = nullptr;
+    pf_caps c{};
+    if (caps) c = *caps;
+    if (c.max_peaks_per_part <= 0) c.max_peaks_per_part = 128;
+    if (c.max_peaks_per_frame <= 0) c.max_peaks_per_frame = 1024;
+    if (c.max_candidates <= 0) c.max_candidates = 4096;
+    if (c.max_humans_per_frame <= 0) c.max_humans_per_frame = 256;
+    if (c.chunk_frames <= 0) c.chunk_frames = 1024;
+    // candidate storage doubles as the peak staging area; bitonic needs 2^k
+    int pc = 1;
+    while (pc < c.max_candidates) pc <<= 1;
+    c.max_candidates = pc;
+    if (c.max_peaks_per_frame > 32767 || c.max_peaks_per_frame > 2 * c.max_candidates)
+        return fail(nullptr, PF_ERR_CONFIG, "max_peaks_per_frame must be <= min(32767, 2*max_candidates)");
+    if (c.max_humans_per_frame > 32767) return fail(nullptr, PF_ERR_CONFIG, "max_humans_per_frame > 32767");
+    pf_ctx *ctx = new pf_ctx();
+    ctx->device = device;
+    ctx->caps = c;
+    auto bail = [&](int code) {
+        g_create_err = ctx->err;
+        pf_destroy(ctx);
+        return code;
+    };
+    if (set_device(ctx)) return bail(PF_ERR_CUDA);
+    cudaDeviceProp prop;
+    {
+        cudaError_t e = cudaGetDeviceProperties(&prop, device);
+        if (e != cudaSuccess) { fail(ctx, PF_ERR_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e)); return bail(PF_ERR_CUDA); }
+    }
+    if (prop.major < 10) {
+        fail(ctx, PF_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a", device, prop.major, prop.minor);
+        return bail(PF_ERR_CUDA);
+    }
+    ctx->sms = prop.multiProcessorCount;
+    auto cu = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess) fail(ctx, PF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+        return e != cudaSuccess;
+    };
+    if (cu(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream") ||
+        cu(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream"))
+        return bail(PF_ERR_CUDA);
+    ctx->stream = ctx->own_stream;
+    for (int k = 0; k < 2; ++k) {
+        if (cu(cudaEventCreateWithFlags(&ctx->ev_copied[k], cudaEventDisableTiming), "event") ||
+            cu(cudaEventCreateWithFlags(&ctx->ev_free[k], cudaEventDisableTiming), "event"))
+            return bail(PF_ERR_CUDA);
+    }
+    if (cu(cudaMalloc(&ctx->d_status, sizeof(Status)), "cudaMalloc status") ||
+        cu(cudaHostAlloc(&ctx->h_status, sizeof(Status), cudaHostAllocDefault), "cudaHostAlloc status"))
+        return bail(PF_ERR_CUDA);
+    const int max_smem = prop.sharedMemPerBlockOptin;
+    if (cu(configure_nms_kernels(max_smem), "configure k_nms_up") ||
+        cu(configure_parse_kernels(max_smem), "configure k_parse_frames"))
+        return bail(PF_ERR_CUDA);
+    const size_t need = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
+                                         PF_MAX_KEYPOINTS, 8) + 2048;
+    if (need > (size_t)max_smem) {
+        fail(ctx, PF_ERR_CONFIG, "caps need %zu B of shared memory per frame CTA (> %d)", need, max_smem);
+        return bail(PF_ERR_CONFIG);
+    }
+    *out = ctx;
+    return PF_OK;
+}
+
+void pf_destroy(pf_ctx *ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    void *dev[] = {ctx->d_counts, ctx->d_peaks, ctx->d_frame_first, ctx->d_frame_count,
+                   ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
+                   ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
+                   ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd};
+    for (void *p : dev) cudaFree(p);
+    void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
+                    ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};
+    for (void *p : host) cudaFreeHost(p);
+    for (auto &kv : ctx->axes) {
+        cudaFree(kv.second.d_i0); cudaFree(kv.second.d_i1);
+        cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (ctx->ev_copied[k]) cudaEventDestroy(ctx->ev_copied[k]);
+        if (ctx->ev_free[k]) cudaEventDestroy(ctx->ev_free[k]);
+    }
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+}
+
+const char *pf_last_error(const pf_ctx *ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int pf_set_stream(pf_ctx *ctx, void *cuda_stream)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    ctx->stream = cuda_stream ? reinterpret_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    return PF_OK;
+}
+
+int pf_set_topology(pf_ctx *ctx, int n_keypoints, int n_limbs, const int32_t *limbs,
+                    const int32_t *paf_channels)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    // SkeletonTopology.validate (types.py:115-143)
+    if (n_keypoints < 1) return fail(ctx, PF_ERR_CONTRACT, "topology needs at least one keypoint");
+    if (n_keypoints > PF_MAX_KEYPOINTS)
+        return fail(ctx, PF_ERR_CONTRACT, "at most %d keypoints supported", PF_MAX_KEYPOINTS);
+    if (n_limbs < 0 || n_limbs > PF_MAX_LIMBS)
+        return fail(ctx, PF_ERR_CONTRACT, "at most %d limbs supported", PF_MAX_LIMBS);
+    if (n_limbs > 0 && (!limbs || !paf_channels)) return fail(ctx, PF_ERR_CONTRACT, "null limb tables");
+    Topo t{};
+    t.K = n_keypoints;
+    t.L = n_limbs;
+    std::vector<int> seen(2 * n_limbs + 1, -1);
+    for (int l = 0; l < n_limbs; ++l) {
+        const int a = limbs[2 * l], b = limbs[2 * l + 1];
+        if (a == b) return fail(ctx, PF_ERR_CONTRACT, "limb %d connects keypoint %d to itself", l, a);
+        if (a < 0 || a >= n_keypoints || b < 0 || b >= n_keypoints)
+            return fail(ctx, PF_ERR_CONTRACT, "limb %d endpoint out of range: (%d, %d)", l, a, b);
+        const int cx = paf_channels[2 * l], cy = paf_channels[2 * l + 1];
+        for (int ch : {cx, cy}) {
+            if (ch < 0 || ch >= 2 * n_limbs)
+                return fail(ctx, PF_ERR_CONTRACT, "paf channel %d of limb %d out of range", ch, l);
+            if (seen[ch] >= 0)
+                return fail(ctx, PF_ERR_CONTRACT, "paf channel %d shared by limbs %d and %d", ch, seen[ch], l);
+            seen[ch] = l;
+        }
+        if (cx == cy) return fail(ctx, PF_ERR_CONTRACT, "limb %d maps both components to channel %d", l, cx);
+        t.la[l] = (int8_t)a;
+        t.lb[l] = (int8_t)b;
+        t.cx[l] = (int16_t)cx;
+        t.cy[l] = (int16_t)cy;
+    }
+    ctx->topo = t;
+    ctx->has_topo = true;
+    return PF_OK;
+}
+
+int pf_validate_params(const pf_params *p) { return validate_params_impl(nullptr, p); }
+
+int pf_set_debug(pf_ctx *ctx, int enable)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    ctx->debug = enable ? 1 : 0;
+    return PF_OK;
+}
+
+int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch, int grid_h,
+                    int grid_w, int stride, const pf_params *p)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    int rc = check_call(ctx, batch, grid_h, grid_w, stride, p);
+    if (rc) return rc;
+    rc = set_device(ctx);
+    if (rc) return rc;
+    const int K = ctx->topo.K, L = ctx->topo.L;
+    const int pool = pool_cap_for(ctx, batch);
+    rc = begin_call(ctx, batch, pool);
+    if (rc) return rc;
+    ctx->last_batch = batch;
+    ctx->last_K = K;
+    if (batch == 0) return PF_OK;
+    if (grid_h == 0 || grid_w == 0) {
+        // no cells, no peaks: every frame parses to [] (nms_peaks on empty maps)
+        CU(cudaMemsetAsync(ctx->d_frame_count, 0, sizeof(int) * batch, ctx->stream));
+        CU(cudaMemsetAsync(ctx->d_frame_first, 0, sizeof(int) * batch, ctx->stream));
+        if (ctx->debug) {
+            CU(cudaMemsetAsync(ctx->d_dbg_np, 0, sizeof(int) * batch, ctx->stream));
+            CU(cudaMemsetAsync(ctx->d_dbg_nc, 0, sizeof(int) * batch, ctx->stream));
+        }
+        return PF_OK;
+    }
+    if (!conf || (L > 0 && !paf)) return fail(ctx, PF_ERR_CONTRACT, "null map pointer");
+    AxisCache *rows, *cols;
+    rc = prepare_axes(ctx, grid_h, grid_w, p, &rows, &cols);
+    if (rc) return rc;
+    const int chunk = chunk_for(ctx, p, grid_h, grid_w);
+    rc = ensure_nms_ws(ctx, chunk, K);
+    if (rc) return rc;
+    const size_t conf_frame = (size_t)(K + 1) * grid_h * grid_w;
+    const size_t paf_frame = (size_t)2 * L * grid_h * grid_w;
+    for (int f0 = 0; f0 < batch; f0 += chunk) {
+        const int n = batch - f0 < chunk ? batch - f0 : chunk;
+        rc = run_chunk(ctx, conf + (size_t)f0 * conf_frame, paf + (size_t)f0 * paf_frame, n, f0,
+                       grid_h, grid_w, stride, p, rows, cols, pool);
+        if (rc) return rc;
+    }
+    return PF_OK;
+}
+
+int pf_get_results(pf_ctx *ctx, pf_results *out)
+{
+    if (!ctx || !out) return PF_ERR_CONTRACT;
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    const int B = ctx->last_batch;
+    const int K = ctx->last_K;
+    if (!ctx->results_ready) {
+        CU(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost, ctx->stream));
+        if (B > 0) {
+            CU(cudaMemcpyAsync(ctx->h_frame_first, ctx->d_frame_first, sizeof(int) * B,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaMemcpyAsync(ctx->h_frame_count, ctx->d_frame_count, sizeof(int) * B,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        CU(cudaStreamSynchronize(ctx->stream));
+        const Status st = *ctx->h_status;
+        if (st.code == PF_ERR_CAPACITY) {
+            static const char *what[] = {"?", "max_peaks_per_part", "max_peaks_per_frame",
+                                         "max_candidates", "max_humans_per_frame", "max_humans_total"};
+            const int wi = st.what >= 1 && st.what <= 5 ? st.what : 0;
+            return fail(ctx, PF_ERR_CAPACITY, "frame %d exceeds capacity %s (needs %d)", st.frame,
+                        what[wi], st.value);
+        }
+        const size_t total = (size_t)st.pool_used;
+        if (total > 0) {
+            CU(cudaMemcpyAsync(ctx->h_hscore, ctx->d_hscore, sizeof(double) * total, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaMemcpyAsync(ctx->h_hnparts, ctx->d_hnparts, sizeof(int) * total, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaMemcpyAsync(ctx->h_kpx, ctx->d_kpx, sizeof(double) * total * K, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaMemcpyAsync(ctx->h_kpy, ctx->d_kpy, sizeof(double) * total * K, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaMemcpyAsync(ctx->h_kps, ctx->d_kps, sizeof(float) * total * K, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaMemcpyAsync(ctx->h_kpp, ctx->d_kpp, sizeof(int) * total * K, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+        }
+        ctx->results_ready = true;
+    }
+    out->n_frames = B;
+    out->n_keypoints = K;
+    out->total_humans = ctx->h_status->pool_used;
+    out->frame_first = ctx->h_frame_first;
+    out->frame_count = ctx->h_frame_count;
+    out->human_score = ctx->h_hscore;
+    out->human_n_parts = ctx->h_hnparts;
+    out->kp_x = ctx->h_kpx;
+    out->kp_y = ctx->h_kpy;
+    out->kp_score = ctx->h_kps;
+    out->kp_peak = ctx->h_kpp;
+    return PF_OK;
+}
+
+int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, int grid_h, int grid_w,
+                  int stride, const pf_params *p, pf_results *out)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    int rc = check_call(ctx, batch, grid_h, grid_w, stride, p);
+    if (rc) return rc;
+    rc = set_device(ctx);
+    if (rc) return rc;
+    const int K = ctx->topo.K, L = ctx->topo.L;
+    if (batch == 0 || grid_h == 0 || grid_w == 0) {
+        rc = pf_parse_device(ctx, nullptr, nullptr, batch, grid_h, grid_w, stride, p);
+        if (rc) return rc;
+        return out ? pf_get_results(ctx, out) : PF_OK;
+    }
+    if (!conf || (L > 0 && !paf)) return fail(ctx, PF_ERR_CONTRACT, "null map pointer");
+    const int pool = pool_cap_for(ctx, batch);
+    rc = begin_call(ctx, batch, pool);
+    if (rc) return rc;
+    ctx->last_batch = batch;
+    ctx->last_K = K;
+    AxisCache *rows, *cols;
+    rc = prepare_axes(ctx, grid_h, grid_w, p, &rows, &cols);
+    if (rc) return rc;
+    int chunk = chunk_for(ctx, p, grid_h, grid_w);
+    if (chunk > 256) chunk = 256;   // copy/compute overlap granularity
+    rc = ensure_nms_ws(ctx, chunk, K);
+    if (rc) return rc;
+    const size_t plane = (size_t)grid_h * grid_w;
+    const size_t conf_frame = (size_t)(K + 1) * plane, paf_frame = (size_t)2 * L * plane;
+    const size_t slot = (size_t)chunk * (conf_frame + paf_frame);
+    if (slot > ctx->in_elems) {
+        cudaFree(ctx->d_in[0]);
+        cudaFree(ctx->d_in[1]);
+        CU(dev_alloc(&ctx->d_in[0], slot));
+        CU(dev_alloc(&ctx->d_in[1], slot));
+        ctx->in_elems = slot;
+    }
+    // slots start free
+    for (int k = 0; k < 2; ++k) CU(cudaEventRecord(ctx->ev_free[k], ctx->stream));
+    int ci = 0;
+    for (int f0 = 0; f0 < batch; f0 += chunk, ++ci) {
+        const int n = batch - f0 < chunk ? batch - f0 : chunk;
+        const int sl = ci & 1;
+        float *dconf = ctx->d_in[sl];
+        float *dpaf = dconf + (size_t)n * conf_frame;
+        CU(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_free[sl], 0));
+        // the background channel (index K) is never read: copy K of K+1 planes per frame
+        CU(cudaMemcpy2DAsync(dconf, conf_frame * sizeof(float), conf + (size_t)f0 * conf_frame,
+                             conf_frame * sizeof(float), (size_t)K * plane * sizeof(float), n,
+                             cudaMemcpyHostToDevice, ctx->copy_stream));
+        if (L > 0)
+            CU(cudaMemcpyAsync(dpaf, paf + (size_t)f0 * paf_frame, (size_t)n * paf_frame * sizeof(float),
+                               cudaMemcpyHostToDevice, ctx->copy_stream));
+        CU(cudaEventRecord(ctx->ev_copied[sl], ctx->copy_stream));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[sl], 0));
+        rc = run_chunk(ctx, dconf, dpaf, n, f0, grid_h, grid_w, stride, p, rows, cols, pool);
+        if (rc) return rc;
+        CU(cudaEventRecord(ctx->ev_free[sl], ctx->stream));
+    }
+    return out ? pf_get_results(ctx, out) : PF_OK;
+}
+
+int pf_sync(pf_ctx *ctx)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return PF_OK;
+}
+
+int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row, int32_t *col,
+                 float *score)
+{
+    if (!ctx || !n_peaks) return PF_ERR_CONTRACT;
+    if (!ctx->debug || !ctx->d_dbg_np) return fail(ctx, PF_ERR_CONTRACT, "debug capture not enabled");
+    if (frame < 0 || frame >= ctx->last_batch) return fail(ctx, PF_ERR_CONTRACT, "frame out of range");
+    CU(cudaStreamSynchronize(ctx->stream));
+    int n = 0;
+    CU(cudaMemcpy(&n, ctx->d_dbg_np + frame, sizeof(int), cudaMemcpyDeviceToHost));
+    *n_peaks = n;
+    if (!part && !row && !col && !score) return PF_OK;
+    std::vector<int4> buf(n > 0 ? n : 1);
+    if (n > 0)
+        CU(cudaMemcpy(buf.data(), ctx->d_dbg_peaks + (size_t)frame * ctx->caps.max_peaks_per_frame,
+                      sizeof(int4) * n, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < n; ++q) {
+        if (part) part[q] = buf[q].x;
+        if (row) row[q] = buf[q].y;
+        if (col) col[q] = buf[q].z;
+        if (score) { int bits = buf[q].w; std::memcpy(&score[q], &bits, sizeof(float)); }
+    }
+    return PF_OK;
+}
+
+int pf_get_connections(pf_ctx *ctx, int frame, int *n_conns, int32_t *limb, int32_t *id_a,
+                       int32_t *id_b, double *score, double *good)
+{
+    if (!ctx || !n_conns) return PF_ERR_CONTRACT;
+    if (!ctx->debug || !ctx->d_dbg_nc) return fail(ctx, PF_ERR_CONTRACT, "debug capture not enabled");
+    if (frame < 0 || frame >= ctx->last_batch) return fail(ctx, PF_ERR_CONTRACT, "frame out of range");
+    CU(cudaStreamSynchronize(ctx->stream));
+    int n = 0;
+    CU(cudaMemcpy(&n, ctx->d_dbg_nc + frame, sizeof(int), cudaMemcpyDeviceToHost));
+    *n_conns = n;
+    if (!limb && !id_a && !id_b && !score && !good) return PF_OK;
+    std::vector<int> ci((size_t)(n > 0 ? n : 1) * 3);
+    std::vector<double> cd((size_t)(n > 0 ? n : 1) * 2);
+    if (n > 0) {
+        const size_t o = (size_t)frame * ctx->caps.max_candidates;
+        CU(cudaMemcpy(ci.data(), ctx->d_dbg_ci + o * 3, sizeof(int) * 3 * n, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(cd.data(), ctx->d_dbg_cd + o * 2, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+    }
+    for (int q = 0; q < n; ++q) {
+        if (limb) limb[q] = ci[q * 3 + 0];
+        if (id_a) id_a[q] = ci[q * 3 + 1];
+        if (id_b) id_b[q] = ci[q * 3 + 2];
+        if (score) score[q] = cd[q * 2 + 0];
+        if (good) good[q] = cd[q * 2 + 1];
+    }
+    return PF_OK;
+}
+
+static int preprocess_impl(pf_ctx *ctx, const void *src, int is_f32, int batch, int h, int w,
+                           float *dst, int out_h, int out_w)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    // operators.py:120-121 zero-area frame; operators.py:83 positive extents
+    if (h < 1 || w < 1) return fail(ctx, PF_ERR_CONTRACT, "zero-area frame");
+    if (out_h < 1 || out_w < 1) return fail(ctx, PF_ERR_CONTRACT, "resize requires positive extents");
+    if (batch < 0) return fail(ctx, PF_ERR_CONTRACT, "batch must be >= 0");
+    if (batch == 0) return PF_OK;
+    if (!src || !dst) return fail(ctx, PF_ERR_CONTRACT, "null image pointer");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    AxisTab rt{}, ct{};
+    if (h != out_h || w != out_w) {
+        AxisCache *r, *c;
+        rc = get_axis(ctx, h, out_h, &r);
+        if (rc) return rc;
+        rc = get_axis(ctx, w, out_w, &c);
+        if (rc) return rc;
+        rt = r->dev();
+        ct = c->dev();
+    }
+    CU(launch_preprocess(src, is_f32, batch, h, w, dst, out_h, out_w, rt, ct, ctx->sms, ctx->stream));
+    ctx->launches += 1;
+    return PF_OK;
+}
+
+int pf_preprocess_device(pf_ctx *ctx, const uint8_t *src, int batch, int h, int w, float *dst,
+                         int out_h, int out_w)
+{
+    return preprocess_impl(ctx, src, 0, batch, h, w, dst, out_h, out_w);
+}
+
+int pf_preprocess_f32_device(pf_ctx *ctx, const float *src, int batch, int h, int w, float *dst,
+                             int out_h, int out_w)
+{
+    return preprocess_impl(ctx, src, 1, batch, h, w, dst, out_h, out_w);
+}
+
+int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int in_w, float *dst,
+                     int out_h, int out_w)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    if (in_h < 1 || in_w < 1 || out_h < 1 || out_w < 1)
+        return fail(ctx, PF_ERR_CONTRACT, "resize requires positive extents");
+    if (n_planes < 0) return fail(ctx, PF_ERR_CONTRACT, "n_planes must be >= 0");
+    if (n_planes == 0) return PF_OK;
+    if (!src || !dst) return fail(ctx, PF_ERR_CONTRACT, "null plane pointer");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    if (in_h == out_h && in_w == out_w) {   // operators.py:84-85 exact copy
+        CU(cudaMemcpyAsync(dst, src, sizeof(float) * (size_t)n_planes * in_h * in_w,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+        return PF_OK;
+    }
+    AxisCache *r, *c;
+    rc = get_axis(ctx, in_h, out_h, &r);
+    if (rc) return rc;
+    rc = get_axis(ctx, in_w, out_w, &c);
+    if (rc) return rc;
+    CU(launch_resize_planes(src, n_planes, in_h, in_w, dst, out_h, out_w, r->dev(), c->dev(), ctx->sms,
+                            ctx->stream));
+    ctx->launches += 1;
+    return PF_OK;
+}
+
+void *pf_host_alloc(size_t bytes)
+{
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void pf_host_free(void *p)
+{
+    if (p) cudaFreeHost(p);
+}
+
+int64_t pf_launch_count(const pf_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

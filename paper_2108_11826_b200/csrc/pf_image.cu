@@ -1,0 +1,195 @@
+// pf_image.cu — dense image/map kernels: pre-processing, materialised
+// bilinear resize of planes, separable Gaussian smoothing.  All three are
+// HBM-streaming kernels (no reuse beyond the 2x2 / (2r+1) stencils, which
+// L1 absorbs); stores are 16-byte vectors where the row width allows.
+#include "pf_launch.h"
+
+namespace pf {
+
+// operators.py:114-131 (+ formats.py:116-117 for u8 input): HWC -> f32 CHW.
+// u8 input: v = float32(u8) / 255.0f (IEEE division, tabulated with the same
+// division); f32 input: the value as-is (an already-normalised Frame image).
+// Unless the size is unchanged (pure layout permutation, operators.py:123-124)
+// the fp64 bilinear formula of operators.py:97-101 (3-D branch) is applied and
+// rounded once to fp32.
+template <typename Tin>
+struct PixelLoad;
+
+template <>
+struct PixelLoad<uint8_t> {
+    const float *lut;
+    __device__ float operator()(const uint8_t *p) const { return lut[*p]; }
+};
+
+template <>
+struct PixelLoad<float> {
+    __device__ float operator()(const float *p) const { return __ldg(p); }
+};
+
+template <typename Tin>
+__global__ void __launch_bounds__(256)
+k_preprocess(const Tin *__restrict__ src, int h, int w, float *__restrict__ dst,
+             int H, int W, AxisTab rows, AxisTab cols, int same, long long total)
+{
+    __shared__ float lut[256];
+    for (int u = threadIdx.x; u < 256; u += blockDim.x) lut[u] = __fdiv_rn((float)u, 255.0f);
+    __syncthreads();
+    PixelLoad<Tin> ld;
+    if constexpr (sizeof(Tin) == 1) ld.lut = lut;
+    const long long HW = (long long)H * W;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long bb = e / HW;
+        const int rem = int(e - bb * HW);
+        const int y = rem / W, x = rem - y * W;
+        const Tin *s = src + bb * (long long)h * w * 3;
+        float *d = dst + bb * 3 * HW + rem;
+        if (same) {
+            const Tin *px = s + ((size_t)y * w + x) * 3;
+            d[0] = ld(px);
+            d[HW] = ld(px + 1);
+            d[2 * HW] = ld(px + 2);
+        } else {
+            const int i0 = __ldg(rows.i0 + y), i1 = __ldg(rows.i1 + y);
+            const int j0 = __ldg(cols.i0 + x), j1 = __ldg(cols.i1 + x);
+            const double ty = __ldg(rows.t + y), omty = __ldg(rows.omt + y);
+            const double tx = __ldg(cols.t + x), omtx = __ldg(cols.omt + x);
+            const Tin *p00 = s + ((size_t)i0 * w + j0) * 3, *p01 = s + ((size_t)i0 * w + j1) * 3;
+            const Tin *p10 = s + ((size_t)i1 * w + j0) * 3, *p11 = s + ((size_t)i1 * w + j1) * 3;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                d[c * HW] = bilerp(ld(p00 + c), ld(p01 + c), ld(p10 + c), ld(p11 + c), tx, omtx, ty, omty);
+        }
+    }
+}
+
+// operators.py:102-107 (2-D branch) applied per plane: [P][h][w] -> [P][H][W].
+// Each thread produces 4 consecutive outputs of one row (float4 store when
+// W % 4 == 0).
+__global__ void __launch_bounds__(256)
+k_resize_planes(const float *__restrict__ src, int h, int w, float *__restrict__ dst,
+                int H, int W, AxisTab rows, AxisTab cols, long long total_quads, int quads_per_row)
+{
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_quads;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long row_id = q / quads_per_row;          // plane * H + y
+        const int x0 = int(q - row_id * quads_per_row) * 4;
+        const long long plane = row_id / H;
+        const int y = int(row_id - plane * H);
+        const float *s = src + plane * (long long)h * w;
+        const int i0 = __ldg(rows.i0 + y), i1 = __ldg(rows.i1 + y);
+        const double ty = __ldg(rows.t + y), omty = __ldg(rows.omt + y);
+        const float *r0 = s + (size_t)i0 * w, *r1 = s + (size_t)i1 * w;
+        float out[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int x = min(x0 + k, W - 1);
+            const int j0 = __ldg(cols.i0 + x), j1 = __ldg(cols.i1 + x);
+            out[k] = bilerp(__ldg(r0 + j0), __ldg(r0 + j1), __ldg(r1 + j0), __ldg(r1 + j1),
+                            __ldg(cols.t + x), __ldg(cols.omt + x), ty, omty);
+        }
+        float *d = dst + row_id * W + x0;
+        if ((W & 3) == 0) {
+            *reinterpret_cast<float4 *>(d) = make_float4(out[0], out[1], out[2], out[3]);
+        } else {
+            for (int k = 0; k < 4 && x0 + k < W; ++k) d[k] = out[k];
+        }
+    }
+}
+
+// Separable Gaussian (no reference): taps k=-r..r, clamped
+// edges, fp64 accumulation in ascending k without FMA, rounded to fp32.
+// Source and destination planes are addressed as (plane / K) * src_frame +
+// (plane % K) * HW so the blur can read part channels out of a [K+1]-channel
+// tensor.
+
+__global__ void __launch_bounds__(256)
+k_blur_rows(const float *__restrict__ src, long long src_frame, float *__restrict__ dst,
+            long long dst_frame, int K, int H, int W, const BlurTaps taps, long long total)
+{
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long HW = (long long)H * W;
+        const long long plane = e / HW;
+        const int rem = int(e - plane * HW);
+        const int y = rem / W, x = rem - y * W;
+        const long long fb = plane / K;
+        const int k = int(plane - fb * K);
+        const float *s = src + fb * src_frame + (long long)k * HW + (long long)y * W;
+        double acc = 0.0;
+        for (int t = -taps.r; t <= taps.r; ++t) {
+            const int xx = min(max(x + t, 0), W - 1);
+            acc = dadd(acc, dmul(taps.w[t + taps.r], (double)__ldg(s + xx)));
+        }
+        dst[fb * dst_frame + (long long)k * HW + rem] = __double2float_rn(acc);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_blur_cols(const float *__restrict__ src, long long src_frame, float *__restrict__ dst,
+            long long dst_frame, int K, int H, int W, const BlurTaps taps, long long total)
+{
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long HW = (long long)H * W;
+        const long long plane = e / HW;
+        const int rem = int(e - plane * HW);
+        const int y = rem / W, x = rem - y * W;
+        const long long fb = plane / K;
+        const int k = int(plane - fb * K);
+        const float *s = src + fb * src_frame + (long long)k * HW + x;
+        double acc = 0.0;
+        for (int t = -taps.r; t <= taps.r; ++t) {
+            const int yy = min(max(y + t, 0), H - 1);
+            acc = dadd(acc, dmul(taps.w[t + taps.r], (double)__ldg(s + (long long)yy * W)));
+        }
+        dst[fb * dst_frame + (long long)k * HW + rem] = __double2float_rn(acc);
+    }
+}
+
+static unsigned grid_for(long long total, int threads, int sms)
+{
+    long long blocks = (total + threads - 1) / threads;
+    const long long cap = (long long)sms * 16;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks < 1 ? 1 : blocks);
+}
+
+cudaError_t launch_preprocess(const void *src, int src_is_f32, int B, int h, int w, float *dst,
+                              int H, int W, AxisTab rows, AxisTab cols, int sms, cudaStream_t s)
+{
+    const long long total = (long long)B * H * W;
+    if (total == 0) return cudaSuccess;
+    const int same = (h == H && w == W);
+    if (src_is_f32)
+        k_preprocess<float><<<grid_for(total, 256, sms), 256, 0, s>>>(
+            static_cast<const float *>(src), h, w, dst, H, W, rows, cols, same, total);
+    else
+        k_preprocess<uint8_t><<<grid_for(total, 256, sms), 256, 0, s>>>(
+            static_cast<const uint8_t *>(src), h, w, dst, H, W, rows, cols, same, total);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_resize_planes(const float *src, long long P, int h, int w, float *dst, int H, int W,
+                                 AxisTab rows, AxisTab cols, int sms, cudaStream_t s)
+{
+    const int qpr = (W + 3) / 4;
+    const long long total = P * H * qpr;
+    if (total == 0) return cudaSuccess;
+    k_resize_planes<<<grid_for(total, 256, sms), 256, 0, s>>>(src, h, w, dst, H, W, rows, cols, total, qpr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blur(const float *src, long long src_frame, float *tmp, float *dst,
+                        long long dst_frame, int B, int K, int H, int W, const BlurTaps &taps,
+                        int sms, cudaStream_t s)
+{
+    const long long total = (long long)B * K * H * W;
+    if (total == 0) return cudaSuccess;
+    const long long tmp_frame = (long long)K * H * W;
+    k_blur_rows<<<grid_for(total, 256, sms), 256, 0, s>>>(src, src_frame, tmp, tmp_frame, K, H, W, taps, total);
+    k_blur_cols<<<grid_for(total, 256, sms), 256, 0, s>>>(tmp, tmp_frame, dst, dst_frame, K, H, W, taps, total);
+    return cudaGetLastError();
+}
+
+}  // namespace pf

@@ -1,0 +1,76 @@
+// pf_launch.h — internal launch interface between the C ABI (pf_capi.cu)
+// and the kernel translation units.
+#pragma once
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+// pf_nms.cu
+struct UpArgs {
+    const float *conf;
+    int C, K, h, w;
+    int H, W;
+    AxisTab rows, cols;
+    float thr;
+    int half;
+    int band_rows;
+    int n_bands;
+    int cap;
+    int *counts;
+    uint2 *peaks;
+};
+constexpr int kMaxFusedHalf = 16;
+cudaError_t launch_nms_plane(const float *conf, int B, int C, int K, int H, int W, float thr,
+                             int half, int cap, int *counts, uint2 *peaks, cudaStream_t s);
+size_t nms_up_smem(int n_src_max, int w, int half, int band_rows, int W);
+cudaError_t launch_nms_up(const UpArgs &a, int B, size_t smem, cudaStream_t s);
+cudaError_t configure_nms_kernels(int max_smem);
+
+// pf_parse.cu
+struct ParseArgs {
+    Topo topo;
+    const float *paf;
+    int h, w;
+    int up;
+    AxisTab rows, cols;
+    int stride_eff;
+    int n_samples;
+    double dot_thr, good_min, min_score;
+    int min_parts;
+    int *counts;
+    const uint2 *peaks;
+    int cap_part, cap_frame, cap_cands, cap_humans;
+    int frame_base;
+    int *frame_first, *frame_count;
+    double *h_score;
+    int *h_nparts;
+    double *kp_x, *kp_y;
+    float *kp_score;
+    int *kp_peak;
+    int pool_cap;
+    Status *st;
+    int debug;
+    int *dbg_npeaks;
+    int4 *dbg_peaks;
+    int *dbg_nconns;
+    int *dbg_conn_i;
+    double *dbg_conn_d;
+};
+enum { kCapPart = 1, kCapFrame = 2, kCapCands = 3, kCapHumans = 4, kCapPool = 5 };
+size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps);
+cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s);
+cudaError_t configure_parse_kernels(int max_smem);
+
+// pf_image.cu
+constexpr int kMaxBlurRadius = 64;
+struct BlurTaps { double w[2 * kMaxBlurRadius + 1]; int r; };
+cudaError_t launch_preprocess(const void *src, int src_is_f32, int B, int h, int w, float *dst,
+                              int H, int W, AxisTab rows, AxisTab cols, int sms, cudaStream_t s);
+cudaError_t launch_resize_planes(const float *src, long long P, int h, int w, float *dst, int H, int W,
+                                 AxisTab rows, AxisTab cols, int sms, cudaStream_t s);
+cudaError_t launch_blur(const float *src, long long src_frame, float *tmp, float *dst,
+                        long long dst_frame, int B, int K, int H, int W, const BlurTaps &taps,
+                        int sms, cudaStream_t s);
+
+}  // namespace pf

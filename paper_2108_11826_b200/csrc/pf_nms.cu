@@ -1,0 +1,213 @@
+// pf_nms.cu — peak extraction (paf.py:74-109 nms_peaks) on sm_100a.
+//
+// Two kernels, both writing unsorted peak records into per-(frame, part)
+// slabs with a per-slab counter; k_parse_frames sorts them into the
+// reference order (score desc, row, col) and assigns ids, so the atomic
+// arrival order never shows in the results.
+//
+//  k_nms_plane — NMS over materialised maps (Mode R: the feature grid as-is;
+//    also the upsampled/blurred maps when those are materialised).  One CTA
+//    per plane streams the plane with 16-byte loads; only cells >= thr look
+//    at their (2h+1)^2-1 neighbours, through L1.  HBM-read bound.
+//
+//  k_nms_up — fused x`up` bilinear upsample + NMS (Mode U).  The low-res
+//    plane (or a row band of it) is staged in shared memory as fp64; the
+//    output band is cut into 8x32 tiles and a tile is evaluated only if the
+//    max of its low-res source rectangle reaches the fp32 threshold — exact,
+//    because every upsampled value is a convex combination of its four
+//    sources and rounds to <= their max.  A hot
+//    tile's values plus an NMS halo are computed in fp64 (reference op
+//    order) into a warp-private shared tile, then tested.  The upsampled
+//    maps never touch HBM.
+#include "pf_launch.h"
+
+namespace pf {
+
+__device__ __forceinline__ bool plane_is_peak(const float *__restrict__ p, int H, int W,
+                                              int i, int j, float v, int half)
+{
+    for (int di = -half; di <= half; ++di) {
+        const int ni = i + di;
+        if (ni < 0 || ni >= H) continue;
+        for (int dj = -half; dj <= half; ++dj) {
+            const int nj = j + dj;
+            if ((di | dj) == 0 || nj < 0 || nj >= W) continue;
+            if (!nms_beats(v, __ldg(p + (size_t)ni * W + nj), di, dj)) return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ void emit_peak(int *counts, uint2 *peaks, int plane, int cap,
+                                          float v, int i, int j)
+{
+    const int slot = atomicAdd(counts + plane, 1);
+    if (slot < cap) peaks[(size_t)plane * cap + slot] = pack_peak(v, i, j);
+}
+
+// conf: [B][C][H][W]; planes are (b, k) for k < K; plane index = b*K + k.
+__global__ void __launch_bounds__(256)
+k_nms_plane(const float *__restrict__ conf, int C, int K, int H, int W, float thr, int half,
+            int cap, int *__restrict__ counts, uint2 *__restrict__ peaks)
+{
+    const int plane = blockIdx.x;
+    const int b = plane / K, k = plane - b * K;
+    const float *p = conf + ((size_t)b * C + k) * (size_t)H * W;
+    const int HW = H * W;
+    if ((HW & 3) == 0 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        const float4 *p4 = reinterpret_cast<const float4 *>(p);
+        for (int e4 = threadIdx.x; e4 < (HW >> 2); e4 += blockDim.x) {
+            const float4 v4 = __ldg(p4 + e4);
+            const float vs[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!(vs[q] >= thr)) continue;
+                const int e = e4 * 4 + q, i = e / W, j = e - i * W;
+                if (plane_is_peak(p, H, W, i, j, vs[q], half)) emit_peak(counts, peaks, plane, cap, vs[q], i, j);
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < HW; e += blockDim.x) {
+            const float v = __ldg(p + e);
+            if (!(v >= thr)) continue;
+            const int i = e / W, j = e - i * W;
+            if (plane_is_peak(p, H, W, i, j, v, half)) emit_peak(counts, peaks, plane, cap, v, i, j);
+        }
+    }
+}
+
+constexpr int kTH = 8;    // tile rows
+constexpr int kTW = 32;   // tile cols (one per lane)
+
+// Shared memory: low-res band as fp64 [n_src][w] | per-warp value tiles
+// [(kTH+2h)][(kTW+2h)] f32 | hot-tile list.
+__global__ void __launch_bounds__(256)
+k_nms_up(const UpArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int plane = blockIdx.x / a.n_bands;
+    const int band = blockIdx.x - plane * a.n_bands;
+    const int b = plane / a.K, k = plane - b * a.K;
+    const float *src = a.conf + ((size_t)b * a.C + k) * (size_t)a.h * a.w;
+
+    const int r0 = band * a.band_rows;
+    const int r1 = min(a.H, r0 + a.band_rows);
+    const int ev_lo = max(0, r0 - a.half), ev_hi = min(a.H, r1 + a.half);  // rows evaluated
+    const int s_lo = __ldg(a.rows.i0 + ev_lo);
+    const int s_hi = __ldg(a.rows.i1 + ev_hi - 1);
+    const int n_src = s_hi - s_lo + 1;
+
+    double *lo = reinterpret_cast<double *>(smem_raw);
+    const int RW = kTW + 2 * a.half, RH = kTH + 2 * a.half;
+    float *tiles = reinterpret_cast<float *>(lo + (size_t)n_src * a.w);
+    const int n_warps = blockDim.x / kWarp;
+    int *hot = reinterpret_cast<int *>(tiles + (size_t)n_warps * RH * RW);
+    __shared__ int n_hot;
+
+    // Stage the low-res rows (coalesced) as fp64.
+    const float *srow = src + (size_t)s_lo * a.w;
+    for (int e = threadIdx.x; e < n_src * a.w; e += blockDim.x) lo[e] = (double)__ldg(srow + e);
+    if (threadIdx.x == 0) n_hot = 0;
+    __syncthreads();
+
+    // Phase 1: hot-tile detection.
+    const int tiles_y = (r1 - r0 + kTH - 1) / kTH;
+    const int tiles_x = (a.W + kTW - 1) / kTW;
+    const double thr_d = (double)a.thr;
+    for (int t = threadIdx.x; t < tiles_y * tiles_x; t += blockDim.x) {
+        const int ty = t / tiles_x, tx = t - ty * tiles_x;
+        const int y0 = r0 + ty * kTH, y1 = min(r1, y0 + kTH);
+        const int x0 = tx * kTW, x1 = min(a.W, x0 + kTW);
+        const int si0 = __ldg(a.rows.i0 + y0) - s_lo, si1 = __ldg(a.rows.i1 + y1 - 1) - s_lo;
+        const int sj0 = __ldg(a.cols.i0 + x0), sj1 = __ldg(a.cols.i1 + x1 - 1);
+        bool is_hot = false;
+        for (int si = si0; si <= si1 && !is_hot; ++si)
+            for (int sj = sj0; sj <= sj1; ++sj)
+                if (lo[si * a.w + sj] >= thr_d) { is_hot = true; break; }
+        if (is_hot) hot[atomicAdd(&n_hot, 1)] = t;
+    }
+    __syncthreads();
+
+    // Phase 2: one warp per hot tile.
+    const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    float *vt = tiles + (size_t)warp * RH * RW;
+    for (int q = warp; q < n_hot; q += n_warps) {
+        const int t = hot[q];
+        const int ty = t / tiles_x, tx = t - ty * tiles_x;
+        const int y0 = r0 + ty * kTH, y1 = min(r1, y0 + kTH);
+        const int x0 = tx * kTW, x1 = min(a.W, x0 + kTW);
+        const int ry0 = max(0, y0 - a.half), ry1 = min(a.H, y1 + a.half);
+        const int rx0 = max(0, x0 - a.half), rx1 = min(a.W, x1 + a.half);
+        for (int c = lane; c < rx1 - rx0; c += kWarp) {
+            const int xo = rx0 + c;
+            const int j0 = __ldg(a.cols.i0 + xo), j1 = __ldg(a.cols.i1 + xo);
+            const double txv = __ldg(a.cols.t + xo), omtx = __ldg(a.cols.omt + xo);
+            for (int r = 0; r < ry1 - ry0; ++r) {
+                const int yo = ry0 + r;
+                const int i0 = __ldg(a.rows.i0 + yo) - s_lo, i1 = __ldg(a.rows.i1 + yo) - s_lo;
+                const double tyv = __ldg(a.rows.t + yo), omty = __ldg(a.rows.omt + yo);
+                vt[r * RW + c] = bilerp(lo[i0 * a.w + j0], lo[i0 * a.w + j1],
+                                        lo[i1 * a.w + j0], lo[i1 * a.w + j1],
+                                        txv, omtx, tyv, omty);
+            }
+        }
+        __syncwarp();
+        const int xo = x0 + lane;
+        if (xo < x1) {
+            const int c = xo - rx0;
+            for (int yo = y0; yo < y1; ++yo) {
+                const int r = yo - ry0;
+                const float v = vt[r * RW + c];
+                if (!(v >= a.thr)) continue;
+                bool peak = true;
+                for (int di = -a.half; di <= a.half && peak; ++di) {
+                    const int ny = yo + di;
+                    if (ny < 0 || ny >= a.H) continue;
+                    for (int dj = -a.half; dj <= a.half; ++dj) {
+                        const int nx = xo + dj;
+                        if ((di | dj) == 0 || nx < 0 || nx >= a.W) continue;
+                        if (!nms_beats(v, vt[(ny - ry0) * RW + (nx - rx0)], di, dj)) { peak = false; break; }
+                    }
+                }
+                if (peak) emit_peak(a.counts, a.peaks, plane, a.cap, v, yo, xo);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Host-side launch helpers (called from pf_capi.cu).
+cudaError_t launch_nms_plane(const float *conf, int B, int C, int K, int H, int W, float thr,
+                             int half, int cap, int *counts, uint2 *peaks, cudaStream_t s)
+{
+    if (B * K == 0) return cudaSuccess;
+    k_nms_plane<<<B * K, 256, 0, s>>>(conf, C, K, H, W, thr, half, cap, counts, peaks);
+    return cudaGetLastError();
+}
+
+size_t nms_up_smem(int n_src_max, int w, int half, int band_rows, int W)
+{
+    const int RW = kTW + 2 * half, RH = kTH + 2 * half;
+    const int tiles = ((band_rows + kTH - 1) / kTH) * ((W + kTW - 1) / kTW);
+    return (size_t)n_src_max * w * sizeof(double) + (size_t)8 * RH * RW * sizeof(float) +
+           (size_t)tiles * sizeof(int);
+}
+
+cudaError_t launch_nms_up(const UpArgs &a, int B, size_t smem, cudaStream_t s)
+{
+    const long long grid = (long long)B * a.K * a.n_bands;
+    if (grid == 0) return cudaSuccess;
+    k_nms_up<<<(unsigned)grid, 256, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t configure_nms_kernels(int max_smem)
+{
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_nms_up);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_nms_up, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                max_smem - (int)fa.sharedSizeBytes);
+}
+
+}  // namespace pf

@@ -1,0 +1,491 @@
+// pf_parse.cu — per-frame limb scoring, greedy matching and human assembly.
+//
+// One CTA per frame (frames are independent; paf.py:292-305 is pure).
+// Everything after peak extraction happens in shared memory:
+//
+//   1. peak ids      — rank-sort each part's peaks by (score desc, row, col)
+//                      (paf.py:104) and prefix the parts (paf.py:298-303)
+//   2. line integral — every (limb, a, b) pair of the frame is one work item
+//                      over all threads: n_samples fp64 samples, nearest cell
+//                      (paf.py:112-146), gate good>=min && score>0
+//                      (paf.py:162); in Mode U the PAF value of a full-res
+//                      cell is re-derived on the fly from the low-res PAF
+//                      with the operators.py:102-107 fp64 formula
+//   3. greedy        — bitonic sort of the gated candidates by
+//                      (limb, -score, id_a, id_b) (paf.py:173), then one warp
+//                      per limb walks its segment with used-bitmaps
+//                      (paf.py:174-181)
+//   4. assembly      — one thread replays assemble_humans' order-dependent
+//                      branches exactly (paf.py:241-271) on shared tables
+//                      (owner per peak, part slots + dict insertion order +
+//                      part bitmask per human)
+//   5. finalise      — per-human Neumaier keypoint sum (CPython 3.12 sum()),
+//                      filters (paf.py:276-281), stable rank by -score
+//                      (paf.py:288), cell_to_pixel (types.py:233-235), and a
+//                      compact write into the output pool.
+#include "pf_launch.h"
+
+namespace pf {
+
+struct Cand {
+    double score;
+    uint32_t ab;     // id_a << 16 | id_b ; bit 31 = accepted
+    uint32_t lg;     // limb << 24 | n_good
+};
+
+constexpr uint32_t kAccepted = 0x80000000u;
+
+__device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y)
+{
+    const uint32_t lx = x.lg >> 24, ly = y.lg >> 24;
+    if (lx != ly) return lx < ly;
+    if (x.score != y.score) return x.score > y.score;
+    return (x.ab & 0x7fffffffu) < (y.ab & 0x7fffffffu);  // (id_a, id_b) lexicographic
+}
+
+__device__ __forceinline__ double sample_paf(const ParseArgs &a, const float *__restrict__ ch,
+                                             int ci, int cj)
+{
+    if (a.up == 1) return (double)__ldg(ch + (size_t)ci * a.w + cj);
+    const int i0 = __ldg(a.rows.i0 + ci), i1 = __ldg(a.rows.i1 + ci);
+    const int j0 = __ldg(a.cols.i0 + cj), j1 = __ldg(a.cols.i1 + cj);
+    const float v = bilerp(__ldg(ch + (size_t)i0 * a.w + j0), __ldg(ch + (size_t)i0 * a.w + j1),
+                           __ldg(ch + (size_t)i1 * a.w + j0), __ldg(ch + (size_t)i1 * a.w + j1),
+                           __ldg(a.cols.t + cj), __ldg(a.cols.omt + cj),
+                           __ldg(a.rows.t + ci), __ldg(a.rows.omt + ci));
+    return (double)v;
+}
+
+// CPython 3.12 builtin sum() over floats starting from int 0 (Neumaier).
+__device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
+{
+    const double t = dadd(f, v);
+    if (fabs(f) >= fabs(v)) c = dadd(c, dadd(__dsub_rn(f, t), v));
+    else c = dadd(c, dadd(__dsub_rn(v, t), f));
+    f = t;
+}
+
+__global__ void __launch_bounds__(256)
+k_parse_frames(const ParseArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int K = a.topo.K, L = a.topo.L;
+    const int b = blockIdx.x;
+    const int gframe = a.frame_base + b;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int warp = tid / kWarp, lane = tid % kWarp, n_warps = nthr / kWarp;
+
+    __shared__ int s_base[PF_MAX_KEYPOINTS + 1];
+    __shared__ int s_pp[PF_MAX_LIMBS + 1];      // pair prefix per limb
+    __shared__ int s_seg[PF_MAX_LIMBS + 1];     // candidate segment start per limb
+    __shared__ int s_err, s_errval, s_ncand, s_nh, s_nkeep, s_pool_base;
+    __shared__ int8_t s_la[PF_MAX_LIMBS], s_lb[PF_MAX_LIMBS];
+    __shared__ int16_t s_cx[PF_MAX_LIMBS], s_cy[PF_MAX_LIMBS];
+    for (int l = tid; l < L; l += nthr) {
+        s_la[l] = a.topo.la[l]; s_lb[l] = a.topo.lb[l];
+        s_cx[l] = a.topo.cx[l]; s_cy[l] = a.topo.cy[l];
+    }
+
+    // ---- shared layout (sizes from the caps; see parse_smem_bytes) ----
+    Cand *cand = reinterpret_cast<Cand *>(smem_raw);                         // cap_cands
+    double *h_conn = reinterpret_cast<double *>(cand + a.cap_cands);         // cap_humans
+    double *h_final = h_conn + a.cap_humans;                                  // cap_humans
+    uint32_t *p_cell = reinterpret_cast<uint32_t *>(h_final + a.cap_humans); // cap_frame
+    float *p_score = reinterpret_cast<float *>(p_cell + a.cap_frame);        // cap_frame
+    uint32_t *h_mask = reinterpret_cast<uint32_t *>(p_score + a.cap_frame);  // cap_humans
+    int *h_pos = reinterpret_cast<int *>(h_mask + a.cap_humans);             // cap_humans
+    const int bm_words = (a.cap_frame + 31) / 32;
+    uint32_t *used = reinterpret_cast<uint32_t *>(h_pos + a.cap_humans);     // n_warps*2*bm_words
+    int16_t *owner = reinterpret_cast<int16_t *>(used + n_warps * 2 * bm_words);  // cap_frame
+    int16_t *h_parts = owner + a.cap_frame;                                   // cap_humans*K
+    int8_t *h_order = reinterpret_cast<int8_t *>(h_parts + a.cap_humans * K); // cap_humans*K
+    int8_t *h_n = h_order + a.cap_humans * K;                                 // cap_humans
+    int8_t *h_alive = h_n + a.cap_humans;                                     // cap_humans
+
+    // ---- 1. peak counts, prefix, capacity checks; reset counters ----
+    if (tid == 0) { s_err = 0; s_ncand = 0; }
+    int my_cnt = 0;
+    if (tid < K) {
+        my_cnt = a.counts[(size_t)b * K + tid];
+        a.counts[(size_t)b * K + tid] = 0;   // ready for the next launch
+        s_base[tid + 1] = my_cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        s_base[0] = 0;
+        int err = 0, val = 0;
+        for (int k = 0; k < K; ++k) {
+            const int c = s_base[k + 1];
+            if (c > a.cap_part && !err) { err = kCapPart; val = c; }
+            s_base[k + 1] = s_base[k] + c;
+        }
+        if (!err && s_base[K] > a.cap_frame) { err = kCapFrame; val = s_base[K]; }
+        s_err = err; s_errval = val;
+    }
+    __syncthreads();
+    if (s_err) {
+        if (tid == 0) {
+            report_capacity(a.st, gframe, s_err, s_errval);
+            a.frame_first[gframe] = 0;
+            a.frame_count[gframe] = 0;
+            if (a.debug) { a.dbg_npeaks[gframe] = 0; a.dbg_nconns[gframe] = 0; }
+        }
+        return;
+    }
+    const int P = s_base[K];
+
+    // ---- 2. stage raw peaks, rank-sort within each part ----
+    uint2 *stage = reinterpret_cast<uint2 *>(cand);   // P <= cap_frame <= 2*cap_cands
+    for (int e = tid; e < P; e += nthr) {
+        int part = 0;
+        while (e >= s_base[part + 1]) ++part;
+        stage[e] = __ldg(a.peaks + ((size_t)b * K + part) * a.cap_part + (e - s_base[part]));
+    }
+    __syncthreads();
+    for (int e = tid; e < P; e += nthr) {
+        int part = 0;
+        while (e >= s_base[part + 1]) ++part;
+        const uint2 v = stage[e];
+        const float vs = __uint_as_float(v.x);
+        int rank = 0;
+        for (int q = s_base[part]; q < s_base[part + 1]; ++q) {
+            const uint2 u = stage[q];
+            const float us = __uint_as_float(u.x);
+            rank += (us > vs) || (us == vs && u.y < v.y);
+        }
+        p_cell[s_base[part] + rank] = v.y;
+        p_score[s_base[part] + rank] = vs;
+    }
+    for (int e = tid; e < P; e += nthr) owner[e] = -1;
+    if (tid == 0) {
+        int acc = 0;
+        for (int l = 0; l < L; ++l) {
+            s_pp[l] = acc;
+            const int na = s_base[s_la[l] + 1] - s_base[s_la[l]];
+            const int nb = s_base[s_lb[l] + 1] - s_base[s_lb[l]];
+            acc += na * nb;
+        }
+        s_pp[L] = acc;
+    }
+    for (int l = tid; l <= L; l += nthr) s_seg[l] = 0x7fffffff;
+    __syncthreads();
+    if (a.debug) {
+        for (int e = tid; e < P; e += nthr) {
+            int part = 0;
+            while (e >= s_base[part + 1]) ++part;
+            a.dbg_peaks[(size_t)gframe * a.cap_frame + e] =
+                make_int4(part, int(p_cell[e] >> 16), int(p_cell[e] & 0xffff), __float_as_int(p_score[e]));
+        }
+        if (tid == 0) a.dbg_npeaks[gframe] = P;
+    }
+
+    // ---- 3. line integral over every candidate pair ----
+    const float *paf_f = a.paf + (size_t)b * (2 * L) * a.h * a.w;
+    const int n_pairs = s_pp[L];
+    const int n = a.n_samples;
+    const double inv_den = (double)(n - 1);
+    for (int p = tid; p < n_pairs; p += nthr) {
+        int l = 0;
+        while (p >= s_pp[l + 1]) ++l;
+        const int pa_part = s_la[l], pb_part = s_lb[l];
+        const int nb = s_base[pb_part + 1] - s_base[pb_part];
+        const int local = p - s_pp[l];
+        const int ia = s_base[pa_part] + local / nb, ib = s_base[pb_part] + local % nb;
+        const int ai = int(p_cell[ia] >> 16), aj = int(p_cell[ia] & 0xffff);
+        const int bi = int(p_cell[ib] >> 16), bj = int(p_cell[ib] & 0xffff);
+        if (ai == bi && aj == bj) continue;          // (0, 0) never passes the gate
+        const int di = bi - ai, dj = bj - aj;
+        const double norm = __dsqrt_rn((double)(di * di + dj * dj));
+        const double vx = __ddiv_rn((double)dj, norm), vy = __ddiv_rn((double)di, norm);
+        const float *chx = paf_f + (size_t)s_cx[l] * a.h * a.w;
+        const float *chy = paf_f + (size_t)s_cy[l] * a.h * a.w;
+        double total = 0.0;
+        int ngood = 0;
+        for (int u = 0; u < n; ++u) {
+            const double t = __ddiv_rn((double)u, inv_den);
+            const int ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
+            const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
+            const double d = dadd(dmul(sample_paf(a, chx, ci, cj), vx),
+                                  dmul(sample_paf(a, chy, ci, cj), vy));
+            total = dadd(total, d);
+            ngood += (d >= a.dot_thr);
+        }
+        const double score = __ddiv_rn(total, (double)n);
+        const double good = __ddiv_rn((double)ngood, (double)n);
+        if (good >= a.good_min && score > 0.0) {
+            const int slot = atomicAdd(&s_ncand, 1);
+            if (slot < a.cap_cands) {
+                Cand c;
+                c.score = score;
+                c.ab = (uint32_t(ia) << 16) | uint32_t(ib);
+                c.lg = (uint32_t(l) << 24) | uint32_t(ngood);
+                cand[slot] = c;
+            }
+        }
+    }
+    __syncthreads();
+    const int nc = s_ncand;
+    if (nc > a.cap_cands) {
+        if (tid == 0) {
+            report_capacity(a.st, gframe, kCapCands, nc);
+            a.frame_first[gframe] = 0;
+            a.frame_count[gframe] = 0;
+            if (a.debug) a.dbg_nconns[gframe] = 0;
+        }
+        return;
+    }
+
+    // ---- 4. sort candidates by (limb, -score, id_a, id_b), bitonic ----
+    int n2 = 1;
+    while (n2 < nc) n2 <<= 1;
+    if (nc > 1) {
+        for (int e = nc + tid; e < n2; e += nthr) {
+            Cand pad;
+            pad.score = 0.0; pad.ab = 0x7fffffffu; pad.lg = 0xff000000u;
+            cand[e] = pad;
+        }
+        __syncthreads();
+        for (int kk = 2; kk <= n2; kk <<= 1) {
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (int i = tid; i < n2; i += nthr) {
+                    const int ixj = i ^ jj;
+                    if (ixj > i) {
+                        const Cand x = cand[i], y = cand[ixj];
+                        const bool asc = (i & kk) == 0;
+                        if (asc ? cand_less(y, x) : cand_less(x, y)) { cand[i] = y; cand[ixj] = x; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    // segment starts: first index of each limb
+    for (int e = tid; e < nc; e += nthr) {
+        const int l = int(cand[e].lg >> 24);
+        const int prev = e ? int(cand[e - 1].lg >> 24) : -1;
+        for (int q = prev + 1; q <= l; ++q) s_seg[q] = e;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // limbs after the last candidate start at nc; fill gaps backwards
+        int next = nc;
+        for (int l = L; l >= 0; --l) {
+            if (s_seg[l] == 0x7fffffff) s_seg[l] = next;
+            next = s_seg[l];
+        }
+    }
+    __syncthreads();
+
+    // ---- 5. greedy per limb (one warp per limb) ----
+    uint32_t *used_a = used + warp * 2 * bm_words;
+    uint32_t *used_b = used_a + bm_words;
+    for (int l = warp; l < L; l += n_warps) {
+        for (int q = lane; q < bm_words; q += kWarp) { used_a[q] = 0u; used_b[q] = 0u; }
+        __syncwarp();
+        if (lane == 0) {
+            for (int e = s_seg[l]; e < s_seg[l + 1]; ++e) {
+                const uint32_t ab = cand[e].ab;
+                const int ia = int((ab >> 16) & 0x7fff), ib = int(ab & 0xffff);
+                if ((used_a[ia >> 5] >> (ia & 31)) & 1u) continue;
+                if ((used_b[ib >> 5] >> (ib & 31)) & 1u) continue;
+                used_a[ia >> 5] |= 1u << (ia & 31);
+                used_b[ib >> 5] |= 1u << (ib & 31);
+                cand[e].ab = ab | kAccepted;
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (a.debug && tid == 0) {
+        int q = 0;
+        for (int e = 0; e < nc; ++e) {
+            if (!(cand[e].ab & kAccepted)) continue;
+            const size_t o = (size_t)gframe * a.cap_cands + q;
+            a.dbg_conn_i[o * 3 + 0] = int(cand[e].lg >> 24);
+            a.dbg_conn_i[o * 3 + 1] = int((cand[e].ab >> 16) & 0x7fff);
+            a.dbg_conn_i[o * 3 + 2] = int(cand[e].ab & 0xffff);
+            a.dbg_conn_d[o * 2 + 0] = cand[e].score;
+            a.dbg_conn_d[o * 2 + 1] = __ddiv_rn((double)(cand[e].lg & 0xffffffu), (double)n);
+            ++q;
+        }
+        a.dbg_nconns[gframe] = q;
+    }
+
+    // ---- 6. assembly: exact sequential replay (paf.py:241-271) ----
+    if (tid == 0) {
+        int nh = 0, err = 0;
+        for (int e = 0; e < nc && !err; ++e) {
+            const Cand c = cand[e];
+            if (!(c.ab & kAccepted)) continue;
+            const int l = int(c.lg >> 24);
+            const int a_part = s_la[l], b_part = s_lb[l];
+            const int pa = int((c.ab >> 16) & 0x7fff), pb = int(c.ab & 0xffff);
+            const int ha = owner[pa], hb = owner[pb];
+            if (ha < 0 && hb < 0) {
+                if (nh >= a.cap_humans) { err = 1; break; }
+                int16_t *parts = h_parts + nh * K;
+                for (int k = 0; k < K; ++k) parts[k] = -1;
+                parts[a_part] = int16_t(pa);
+                parts[b_part] = int16_t(pb);
+                h_order[nh * K + 0] = int8_t(a_part);
+                h_order[nh * K + 1] = int8_t(b_part);
+                h_n[nh] = 2;
+                h_mask[nh] = (1u << a_part) | (1u << b_part);
+                h_conn[nh] = c.score;
+                h_alive[nh] = 1;
+                owner[pa] = int16_t(nh);
+                owner[pb] = int16_t(nh);
+                ++nh;
+            } else if (ha >= 0 && hb >= 0) {
+                if (ha == hb) {
+                    h_conn[ha] = dadd(h_conn[ha], c.score);
+                } else if ((h_mask[ha] & h_mask[hb]) == 0u) {
+                    const int nB = h_n[hb];
+                    int nA = h_n[ha];
+                    for (int q = 0; q < nB; ++q) {
+                        const int part = h_order[hb * K + q];
+                        const int pid = h_parts[hb * K + part];
+                        h_parts[ha * K + part] = int16_t(pid);
+                        h_order[ha * K + nA++] = int8_t(part);
+                        owner[pid] = int16_t(ha);
+                    }
+                    h_n[ha] = int8_t(nA);
+                    h_mask[ha] |= h_mask[hb];
+                    h_conn[ha] = dadd(h_conn[ha], dadd(h_conn[hb], c.score));
+                    h_alive[hb] = 0;
+                }
+            } else {
+                const int hidx = ha >= 0 ? ha : hb;
+                const int part = ha >= 0 ? b_part : a_part;
+                const int pid = ha >= 0 ? pb : pa;
+                if (!((h_mask[hidx] >> part) & 1u)) {
+                    h_parts[hidx * K + part] = int16_t(pid);
+                    h_order[hidx * K + h_n[hidx]] = int8_t(part);
+                    h_n[hidx] = int8_t(h_n[hidx] + 1);
+                    h_mask[hidx] |= 1u << part;
+                    h_conn[hidx] = dadd(h_conn[hidx], c.score);
+                    owner[pid] = int16_t(hidx);
+                }
+            }
+        }
+        s_nh = nh;
+        s_err = err;
+    }
+    __syncthreads();
+    if (s_err) {
+        if (tid == 0) {
+            report_capacity(a.st, gframe, kCapHumans, a.cap_humans + 1);
+            a.frame_first[gframe] = 0;
+            a.frame_count[gframe] = 0;
+        }
+        return;
+    }
+    const int nh = s_nh;
+
+    // ---- 7. filters and scores (paf.py:273-287) ----
+    for (int hh = tid; hh < nh; hh += nthr) {
+        bool keep = h_alive[hh] && h_n[hh] >= a.min_parts;
+        double score = 0.0;
+        if (keep) {
+            const int np = h_n[hh];
+            double f = 0.0, c = 0.0;
+            for (int q = 0; q < np; ++q) {
+                const double v = (double)p_score[h_parts[hh * K + h_order[hh * K + q]]];
+                if (q == 0) f = dadd(0.0, v);
+                else neumaier_add(f, c, v);
+            }
+            if (c != 0.0 && isfinite(c)) f = dadd(f, c);
+            score = __ddiv_rn(dadd(f, h_conn[hh]), (double)np);
+            keep = !(score < a.min_score);
+        }
+        h_final[hh] = score;
+        h_pos[hh] = keep ? 1 : 0;
+    }
+    __syncthreads();
+    // stable rank by -score among kept humans (paf.py:288)
+    for (int hh = tid; hh < nh; hh += nthr) {
+        if (!h_pos[hh]) continue;
+        const double s = h_final[hh];
+        int pos = 0;
+        for (int g = 0; g < nh; ++g) {
+            if (!h_pos[g]) continue;
+            const double sg = h_final[g];
+            pos += (sg > s) || (sg == s && g < hh);
+        }
+        h_mask[hh] = uint32_t(pos);   // mask no longer needed; reuse as rank
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int nk = 0;
+        for (int hh = 0; hh < nh; ++hh) nk += h_pos[hh];
+        s_nkeep = nk;
+        const int base = nk ? atomicAdd(&a.st->pool_used, nk) : 0;
+        if (base + nk > a.pool_cap) {
+            report_capacity(a.st, gframe, kCapPool, base + nk);
+            s_pool_base = -1;
+            a.frame_first[gframe] = 0;
+            a.frame_count[gframe] = 0;
+        } else {
+            s_pool_base = base;
+            a.frame_first[gframe] = base;
+            a.frame_count[gframe] = nk;
+        }
+    }
+    __syncthreads();
+    if (s_pool_base < 0) return;
+    const int base = s_pool_base;
+    const double sd = (double)a.stride_eff;
+    for (int x = tid; x < nh * K; x += nthr) {
+        const int hh = x / K, k = x - hh * K;
+        if (!h_pos[hh]) continue;
+        const size_t o = (size_t)(base + int(h_mask[hh]));
+        if (k == 0) {
+            a.h_score[o] = h_final[hh];
+            a.h_nparts[o] = h_n[hh];
+        }
+        const int pid = h_parts[hh * K + k];
+        const size_t ok = o * K + k;
+        if (pid < 0) {
+            a.kp_x[ok] = 0.0; a.kp_y[ok] = 0.0; a.kp_score[ok] = 0.0f; a.kp_peak[ok] = -1;
+        } else {
+            const uint32_t cell = p_cell[pid];
+            const double i = (double)(cell >> 16), j = (double)(cell & 0xffff);
+            a.kp_x[ok] = dadd(dmul(dadd(j, 0.5), sd), -0.5);
+            a.kp_y[ok] = dadd(dmul(dadd(i, 0.5), sd), -0.5);
+            a.kp_score[ok] = p_score[pid];
+            a.kp_peak[ok] = pid;
+        }
+    }
+}
+
+size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps)
+{
+    const int bm_words = (cap_frame + 31) / 32;
+    size_t s = (size_t)cap_cands * sizeof(Cand);
+    s += (size_t)cap_humans * 2 * sizeof(double);
+    s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
+    s += (size_t)cap_humans * (sizeof(uint32_t) + sizeof(int));
+    s += (size_t)n_warps * 2 * bm_words * sizeof(uint32_t);
+    s += (size_t)cap_frame * sizeof(int16_t);
+    s += (size_t)cap_humans * K * (sizeof(int16_t) + sizeof(int8_t));
+    s += (size_t)cap_humans * 2;
+    return (s + 15) & ~size_t(15);
+}
+
+cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s)
+{
+    if (B == 0) return cudaSuccess;
+    k_parse_frames<<<B, threads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t configure_parse_kernels(int max_smem)
+{
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_parse_frames);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_parse_frames, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                max_smem - (int)fa.sharedSizeBytes);
+}
+
+}  // namespace pf

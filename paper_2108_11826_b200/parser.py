@@ -1,0 +1,296 @@
+"""PAF pose parsing on B200 — drop-in for ``poseflow.paf`` (``paf.py``).
+
+Public surface (reference lines in brackets):
+
+* ``ParserParams``  [paf.py:34-54] — same seven fields, defaults and
+  ``validate()`` errors, plus ``upsample`` (1 = parse the feature grid as
+  the reference does; 8 = HyperPose-style x8 bilinear upsample first) and
+  ``blur_sigma`` (0 = off).
+* ``parse(maps, topo, params)`` [paf.py:292-305] — one frame, returns a new
+  ``List[HumanPose]``; raises ``ConfigError``/``ContractError`` before any
+  device work.  Pure and deterministic: the GPU result equals the reference's
+  bit for bit (peaks, connections, assignment, scores).
+* ``parse_batch`` / ``parse_arrays`` / ``PafParser.parse_device`` — the
+  batched forms the GPU is built for (SoA results, lazy ``HumanPose``).
+
+Every call goes through ``libpf_b200.so``; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native
+from .core import FeatureMaps, HumanPose, Keypoint, SkeletonTopology
+from .errors import ConfigError, ContractError
+
+
+@dataclass
+class ParserParams:
+    conf_threshold: float = 0.10
+    nms_window: int = 3
+    n_samples: int = 10
+    sample_dot_threshold: float = 0.05
+    good_fraction_min: float = 0.8
+    min_parts: int = 4
+    min_human_score: float = 0.2
+    # B200-path extensions (not in the reference; defaults = reference behaviour)
+    upsample: int = 1
+    blur_sigma: float = 0.0
+
+    def validate(self) -> None:
+        # paf.py:44-54, same order and messages
+        if self.nms_window < 3 or self.nms_window % 2 == 0:
+            raise ConfigError("nms_window must be odd and >= 3")
+        if self.n_samples < 2:
+            raise ConfigError("n_samples must be >= 2")
+        for name in ("conf_threshold", "sample_dot_threshold", "good_fraction_min"):
+            value = getattr(self, name)
+            if not (0.0 <= value <= 1.0):
+                raise ConfigError(f"{name} must be in [0, 1], got {value}")
+        if self.min_parts < 1:
+            raise ConfigError("min_parts must be >= 1")
+        if int(self.upsample) != self.upsample or self.upsample < 1:
+            raise ConfigError("upsample must be an integer >= 1")
+        if not (self.blur_sigma >= 0.0) or self.blur_sigma == float("inf"):
+            raise ConfigError("blur_sigma must be finite and >= 0")
+
+    def to_native(self) -> _native.PfParams:
+        return _native.PfParams(float(self.conf_threshold), int(self.nms_window),
+                                int(self.n_samples), float(self.sample_dot_threshold),
+                                float(self.good_fraction_min), int(self.min_parts),
+                                float(self.min_human_score), int(self.upsample),
+                                float(self.blur_sigma))
+
+
+def _params_of(params) -> ParserParams:
+    """Accept our ParserParams or any object with the reference's fields."""
+    if isinstance(params, ParserParams):
+        return params
+    return ParserParams(**{f: getattr(params, f) for f in (
+        "conf_threshold", "nms_window", "n_samples", "sample_dot_threshold",
+        "good_fraction_min", "min_parts", "min_human_score")},
+        upsample=getattr(params, "upsample", 1), blur_sigma=getattr(params, "blur_sigma", 0.0))
+
+
+class BatchResult:
+    """Humans of a batch as structure-of-arrays (a copy of the C ABI's
+    ``pf_results``); ``poses(f)`` materialises ``HumanPose`` objects lazily."""
+
+    def __init__(self, res: _native.PfResults):
+        n, total, k = res.n_frames, res.total_humans, res.n_keypoints
+        self.n_frames, self.total_humans, self.n_keypoints = n, total, k
+
+        def arr(ptr, count, dtype):
+            if count <= 0:
+                return np.zeros(0, dtype)
+            return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
+
+        self.frame_first = arr(res.frame_first, n, np.int32)
+        self.frame_count = arr(res.frame_count, n, np.int32)
+        self.human_score = arr(res.human_score, total, np.float64)
+        self.human_n_parts = arr(res.human_n_parts, total, np.int32)
+        self.kp_x = arr(res.kp_x, total * k, np.float64).reshape(total, k)
+        self.kp_y = arr(res.kp_y, total * k, np.float64).reshape(total, k)
+        self.kp_score = arr(res.kp_score, total * k, np.float32).reshape(total, k)
+        self.kp_peak = arr(res.kp_peak, total * k, np.int32).reshape(total, k)
+
+    def poses(self, frame: int) -> List[HumanPose]:
+        first, count = int(self.frame_first[frame]), int(self.frame_count[frame])
+        out = []
+        for h in range(first, first + count):
+            kps = []
+            for k in range(self.n_keypoints):
+                if self.kp_peak[h, k] < 0:
+                    kps.append(None)
+                else:
+                    kps.append(Keypoint(x=float(self.kp_x[h, k]), y=float(self.kp_y[h, k]),
+                                        score=float(self.kp_score[h, k])))
+            out.append(HumanPose(keypoints=tuple(kps), score=float(self.human_score[h]),
+                                 n_parts=int(self.human_n_parts[h])))
+        return out
+
+    def all_poses(self) -> List[List[HumanPose]]:
+        return [self.poses(f) for f in range(self.n_frames)]
+
+
+class PafParser:
+    """A GPU parsing engine bound to one device (one ``pf_ctx``).
+
+    Not reentrant; use one per thread (``parse()`` keeps a thread-local one).
+    """
+
+    def __init__(self, topo: SkeletonTopology, device: int = 0,
+                 caps: Optional[dict] = None, debug: bool = False):
+        c = _native.PfCaps(**(caps or {}))
+        self.ctx = _native.Context(device, c)
+        self.topo = topo
+        self.ctx.set_topology(topo)
+        self.device = device
+        if debug:
+            self.set_debug(True)
+
+    def set_debug(self, enable: bool) -> None:
+        self.ctx.check(self.ctx.lib.pf_set_debug(self.ctx.handle, 1 if enable else 0))
+
+    def set_stream(self, stream_handle: int) -> None:
+        self.ctx.check(self.ctx.lib.pf_set_stream(self.ctx.handle, ctypes.c_void_p(stream_handle)))
+
+    def launch_count(self) -> int:
+        return self.ctx.launch_count()
+
+    def _check_arrays(self, conf_shape, paf_shape, stride):
+        k, n_l = self.topo.n_keypoints, self.topo.n_limbs
+        if len(conf_shape) != 4 or conf_shape[1] != k + 1:
+            raise ContractError(f"conf dims {tuple(conf_shape)} inconsistent with {k} keypoints")
+        if len(paf_shape) != 4 or paf_shape[1] != 2 * n_l:
+            raise ContractError(f"paf dims {tuple(paf_shape)} inconsistent with {n_l} limbs")
+        if conf_shape[0] != paf_shape[0]:
+            raise ContractError("conf and paf batch sizes differ")
+        if tuple(conf_shape[2:]) != tuple(paf_shape[2:]):
+            raise ContractError(f"conf grid {tuple(conf_shape[2:])} != paf grid {tuple(paf_shape[2:])}")
+        if stride < 1:
+            raise ContractError("stride must be >= 1")
+
+    def parse_arrays(self, conf: np.ndarray, paf: np.ndarray, stride: int,
+                     params: ParserParams) -> BatchResult:
+        """Host arrays conf [B,K+1,H,W], paf [B,2L,H,W] (f32) -> BatchResult."""
+        params = _params_of(params)
+        params.validate()
+        conf = np.ascontiguousarray(conf, dtype=np.float32)
+        paf = np.ascontiguousarray(paf, dtype=np.float32)
+        self._check_arrays(conf.shape, paf.shape, stride)
+        res = _native.PfResults()
+        p = params.to_native()
+        b, _, h, w = conf.shape
+        self.ctx.check(self.ctx.lib.pf_parse_host(
+            self.ctx.handle, conf.ctypes.data if conf.size else None,
+            paf.ctypes.data if paf.size else None, b, h, w, int(stride),
+            ctypes.byref(p), ctypes.byref(res)))
+        return BatchResult(res)
+
+    def parse_device(self, conf_ptr: int, paf_ptr: int, batch: int, grid_h: int, grid_w: int,
+                     stride: int, params: ParserParams) -> None:
+        """Asynchronous parse of device-resident maps (raw CUDA pointers, the
+        FeatureMaps layout batched); collect with ``results()``."""
+        p = _params_of(params).to_native()
+        self.ctx.check(self.ctx.lib.pf_parse_device(
+            self.ctx.handle, ctypes.c_void_p(conf_ptr), ctypes.c_void_p(paf_ptr), int(batch),
+            int(grid_h), int(grid_w), int(stride), ctypes.byref(p)))
+
+    def parse_tensors(self, conf, paf, stride: int, params: ParserParams) -> None:
+        """torch CUDA tensors [B,K+1,H,W] / [B,2L,H,W] on this engine's device;
+        enqueued on torch's current stream."""
+        import torch
+
+        params = _params_of(params)
+        params.validate()
+        self._check_arrays(tuple(conf.shape), tuple(paf.shape), stride)
+        if conf.dtype != torch.float32 or paf.dtype != torch.float32:
+            raise ContractError("maps must be float32")
+        if not (conf.is_cuda and paf.is_cuda):
+            raise ContractError("parse_tensors needs CUDA tensors")
+        conf = conf.contiguous()
+        paf = paf.contiguous()
+        self.set_stream(torch.cuda.current_stream(conf.device).cuda_stream)
+        b, _, h, w = conf.shape
+        self.parse_device(conf.data_ptr(), paf.data_ptr(), b, h, w, stride, params)
+
+    def results(self) -> BatchResult:
+        res = _native.PfResults()
+        self.ctx.check(self.ctx.lib.pf_get_results(self.ctx.handle, ctypes.byref(res)))
+        return BatchResult(res)
+
+    def peaks(self, frame: int):
+        """Debug capture: [(part, row, col, score, id)] in id order."""
+        lib, h = self.ctx.lib, self.ctx.handle
+        n = ctypes.c_int()
+        self.ctx.check(lib.pf_get_peaks(h, frame, ctypes.byref(n), None, None, None, None))
+        cnt = max(n.value, 1)
+        part, row, col = (np.zeros(cnt, np.int32) for _ in range(3))
+        score = np.zeros(cnt, np.float32)
+        self.ctx.check(lib.pf_get_peaks(h, frame, ctypes.byref(n), part.ctypes.data,
+                                        row.ctypes.data, col.ctypes.data, score.ctypes.data))
+        return [(int(part[q]), int(row[q]), int(col[q]), float(score[q]), q)
+                for q in range(n.value)]
+
+    def connections(self, frame: int):
+        """Debug capture: [(limb, id_a, id_b, score, good_fraction)]."""
+        lib, h = self.ctx.lib, self.ctx.handle
+        n = ctypes.c_int()
+        self.ctx.check(lib.pf_get_connections(h, frame, ctypes.byref(n), None, None, None, None, None))
+        cnt = max(n.value, 1)
+        limb, ia, ib = (np.zeros(cnt, np.int32) for _ in range(3))
+        sc, gd = np.zeros(cnt, np.float64), np.zeros(cnt, np.float64)
+        self.ctx.check(lib.pf_get_connections(h, frame, ctypes.byref(n), limb.ctypes.data,
+                                              ia.ctypes.data, ib.ctypes.data, sc.ctypes.data,
+                                              gd.ctypes.data))
+        return [(int(limb[q]), int(ia[q]), int(ib[q]), float(sc[q]), float(gd[q]))
+                for q in range(n.value)]
+
+    def close(self) -> None:
+        self.ctx.close()
+
+
+_tls = threading.local()
+DEFAULT_DEVICE = 0
+
+
+def default_parser(topo: SkeletonTopology, device: Optional[int] = None) -> PafParser:
+    """Thread-local engine per device (contexts are not reentrant)."""
+    dev = DEFAULT_DEVICE if device is None else int(device)
+    cache = getattr(_tls, "parsers", None)
+    if cache is None:
+        cache = _tls.parsers = {}
+    eng = cache.get(dev)
+    if eng is None:
+        eng = cache[dev] = PafParser(topo, device=dev)
+    else:
+        eng.topo = topo
+        eng.ctx.set_topology(topo)
+    return eng
+
+
+def _stack_maps(maps_list: Sequence[FeatureMaps], topo: SkeletonTopology):
+    strides = {m.stride for m in maps_list}
+    grids = {m.grid_shape() for m in maps_list}
+    if len(strides) != 1 or len(grids) != 1:
+        raise ContractError("parse_batch needs frames with one grid shape and stride")
+    conf = np.stack([m.conf.array for m in maps_list])
+    paf = np.stack([m.paf.array for m in maps_list])
+    return conf, paf, strides.pop()
+
+
+def parse(maps: FeatureMaps, topo: SkeletonTopology, params) -> List[HumanPose]:
+    """Drop-in for ``poseflow.paf.parse`` (paf.py:292-305), on the GPU."""
+    params = _params_of(params)
+    params.validate()          # ConfigError before any work (paf.py:295)
+    maps.validate(topo)        # ContractError (paf.py:296)
+    eng = default_parser(topo)
+    conf = maps.conf.array[None]
+    paf = maps.paf.array[None]
+    return eng.parse_arrays(conf, paf, maps.stride, params).poses(0)
+
+
+def parse_batch(maps_list: Sequence[FeatureMaps], topo: SkeletonTopology, params,
+                device: Optional[int] = None) -> List[List[HumanPose]]:
+    """``[parse(m, topo, params) for m in maps_list]`` in one GPU call."""
+    params = _params_of(params)
+    params.validate()
+    for m in maps_list:
+        m.validate(topo)
+    if not maps_list:
+        return []
+    conf, paf, stride = _stack_maps(maps_list, topo)
+    return default_parser(topo, device).parse_arrays(conf, paf, stride, params).all_poses()
+
+
+def parse_arrays(conf: np.ndarray, paf: np.ndarray, stride: int, topo: SkeletonTopology,
+                 params, device: Optional[int] = None) -> BatchResult:
+    """Batched host arrays -> SoA ``BatchResult`` (no per-human objects)."""
+    return default_parser(topo, device).parse_arrays(conf, paf, stride, params)
