@@ -108,9 +108,11 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps);
 void pf_destroy(pf_ctx *ctx);
 const char *pf_last_error(const pf_ctx *ctx);
 
-/* Bind the context to a CUDA stream (cudaStream_t passed as void*);
- * NULL = the context's own non-blocking stream. */
+/* Bind the context to a CUDA stream (cudaStream_t passed as void*; NULL is
+ * the legacy default stream, e.g. torch's default stream).  A new context
+ * uses its own non-blocking stream; pf_use_own_stream() returns to it. */
 int pf_set_stream(pf_ctx *ctx, void *cuda_stream);
+int pf_use_own_stream(pf_ctx *ctx);
 
 /* SkeletonTopology (types.py:81-166): limbs and paf_channels are [L][2]. */
 int pf_set_topology(pf_ctx *ctx, int n_keypoints, int n_limbs,
@@ -144,6 +146,21 @@ int pf_sync(pf_ctx *ctx);
  * id_b, score, good_fraction.  Returns counts through n_*; pass NULL
  * arrays to query counts only. */
 int pf_set_debug(pf_ctx *ctx, int enable);
+
+/* Options: PF_OPT_DEBUG (= pf_set_debug), PF_OPT_TIMING (CUDA events around
+ * every kernel launch, read with pf_get_kernel_times), PF_OPT_MATERIALISE
+ * (force the unfused Mode U path: resize -> [blur] -> NMS over HBM maps). */
+#define PF_OPT_DEBUG 1
+#define PF_OPT_TIMING 2
+#define PF_OPT_MATERIALISE 3
+#define PF_OPT_GENERIC_FUSED 4   /* use the shared-memory tile kernel for Mode U */
+int pf_set_option(pf_ctx *ctx, int option, int value);
+
+/* Per-kernel device time (ms, CUDA events on the launching stream) and launch
+ * counts accumulated since the last reset; ids index pf_kernel_name(). */
+#define PF_N_KERNELS 8
+const char *pf_kernel_name(int id);
+int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset);
 int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,
                  int32_t *col, float *score);
 int pf_get_connections(pf_ctx *ctx, int frame, int *n_conns, int32_t *limb,

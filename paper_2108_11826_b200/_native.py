@@ -20,12 +20,16 @@ LIB_PATH = os.path.join(_HERE, "libpf_b200.so")
 
 PF_OK, PF_ERR_CONFIG, PF_ERR_CONTRACT, PF_ERR_CAPACITY, PF_ERR_CUDA = 0, 1, 2, 3, 4
 PF_MAX_KEYPOINTS, PF_MAX_LIMBS = 32, 64
+PF_OPT_DEBUG, PF_OPT_TIMING, PF_OPT_MATERIALISE, PF_OPT_GENERIC_FUSED = 1, 2, 3, 4
+PF_N_KERNELS = 8
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (
     "pf_abi_version", "pf_create", "pf_destroy", "pf_last_error", "pf_set_stream",
+    "pf_use_own_stream",
     "pf_set_topology", "pf_validate_params", "pf_parse_device", "pf_parse_host",
-    "pf_get_results", "pf_sync", "pf_set_debug", "pf_get_peaks", "pf_get_connections",
+    "pf_get_results", "pf_sync", "pf_set_debug", "pf_set_option", "pf_kernel_name",
+    "pf_get_kernel_times", "pf_get_peaks", "pf_get_connections",
     "pf_preprocess_device", "pf_preprocess_f32_device", "pf_resize_device", "pf_host_alloc", "pf_host_free",
     "pf_launch_count",
 )
@@ -95,6 +99,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pf_last_error.argtypes = [vp]
         lib.pf_last_error.restype = ctypes.c_char_p
         lib.pf_set_stream.argtypes = [vp, vp]
+        lib.pf_use_own_stream.argtypes = [vp]
         lib.pf_set_topology.argtypes = [vp, c_int, c_int, vp, vp]
         lib.pf_validate_params.argtypes = [ctypes.POINTER(PfParams)]
         lib.pf_parse_device.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int,
@@ -104,6 +109,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pf_get_results.argtypes = [vp, ctypes.POINTER(PfResults)]
         lib.pf_sync.argtypes = [vp]
         lib.pf_set_debug.argtypes = [vp, c_int]
+        lib.pf_set_option.argtypes = [vp, c_int, c_int]
+        lib.pf_kernel_name.argtypes = [c_int]
+        lib.pf_kernel_name.restype = ctypes.c_char_p
+        lib.pf_get_kernel_times.argtypes = [vp, vp, vp, c_int]
         lib.pf_get_peaks.argtypes = [vp, c_int, ctypes.POINTER(c_int), vp, vp, vp, vp]
         lib.pf_get_connections.argtypes = [vp, c_int, ctypes.POINTER(c_int), vp, vp, vp, vp, vp]
         lib.pf_preprocess_device.argtypes = [vp, vp, c_int, c_int, c_int, vp, c_int, c_int]
@@ -165,6 +174,18 @@ class Context:
 
     def launch_count(self) -> int:
         return int(self.lib.pf_launch_count(self.handle))
+
+    def set_option(self, option: int, value: int) -> None:
+        self.check(self.lib.pf_set_option(self.handle, int(option), int(value)))
+
+    def kernel_times(self, reset: bool = False) -> dict:
+        """{kernel name: (total ms, launches)} since the last reset (PF_OPT_TIMING)."""
+        ms = np.zeros(PF_N_KERNELS, np.float64)
+        n = np.zeros(PF_N_KERNELS, np.int64)
+        self.check(self.lib.pf_get_kernel_times(self.handle, ms.ctypes.data, n.ctypes.data,
+                                                1 if reset else 0))
+        return {self.lib.pf_kernel_name(k).decode(): (float(ms[k]), int(n[k]))
+                for k in range(PF_N_KERNELS) if n[k]}
 
     def close(self) -> None:
         if getattr(self, "handle", None):

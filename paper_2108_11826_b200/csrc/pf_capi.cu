@@ -28,7 +28,8 @@ struct AxisCache {
     int in_n = 0, out_n = 0;
     std::vector<int32_t> i0, i1;
     std::vector<double> t, omt;
-    int32_t *d_i0 = nullptr, *d_i1 = nullptr;
+    std::vector<int32_t> first_out, last_out;   // inverse map: outputs reading input row r
+    int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr;
     double *d_t = nullptr, *d_omt = nullptr;
     AxisTab dev() const { return AxisTab{d_i0, d_i1, d_t, d_omt}; }
 };
@@ -50,6 +51,14 @@ void fill_axis(AxisCache &a, int in_n, int out_n)
         a.omt[o] = 1.0 - t;
         a.i0[o] = (int32_t)(f < 0 ? 0 : (f > in_n - 1 ? in_n - 1 : f));
         a.i1[o] = (int32_t)(f + 1 < 0 ? 0 : (f + 1 > in_n - 1 ? in_n - 1 : f + 1));
+    }
+    a.first_out.assign(in_n, 0x3fffffff);
+    a.last_out.assign(in_n, -1);
+    for (int o = 0; o < out_n; ++o) {
+        for (int r : {a.i0[o], a.i1[o]}) {
+            if (o < a.first_out[r]) a.first_out[r] = o;
+            if (o > a.last_out[r]) a.last_out[r] = o;
+        }
     }
 }
 
@@ -117,6 +126,15 @@ struct pf_ctx {
     double *d_dbg_cd = nullptr;
     size_t dbg_frames = 0;
 
+    // per-kernel timing (PF_OPT_TIMING)
+    int timing = 0;
+    int materialise = 0;
+    int generic_fused = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    double kernel_ms[PF_N_KERNELS] = {0};
+    int64_t kernel_launches[PF_N_KERNELS] = {0};
+
     int last_batch = 0;
     int last_K = 0;
     bool results_ready = false;
@@ -146,6 +164,49 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
                         __FILE__, __LINE__);                                              \
     } while (0)
 
+enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
+                kNmsUpWin };
+const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
+                                          "k_resize_planes", "k_blur_rows", "k_blur_cols",
+                                          "k_preprocess", "k_nms_up_win"};
+
+cudaEvent_t take_event(pf_ctx *ctx)
+{
+    if (!ctx->ev_pool.empty()) {
+        cudaEvent_t e = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one kernel launch with timing events when PF_OPT_TIMING is on.
+struct KernelTimer {
+    pf_ctx *ctx;
+    int id;
+    int n;
+    cudaEvent_t a = nullptr;
+    KernelTimer(pf_ctx *c, int kid, int launches = 1) : ctx(c), id(kid), n(launches)
+    {
+        if (ctx->timing) {
+            a = take_event(ctx);
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    ~KernelTimer()
+    {
+        ctx->launches += n;
+        ctx->kernel_launches[id] += n;
+        if (a) {
+            cudaEvent_t b = take_event(ctx);
+            cudaEventRecord(b, ctx->stream);
+            ctx->pending.push_back({id, {a, b}});
+        }
+    }
+};
+
 int set_device(pf_ctx *ctx)
 {
     CU(cudaSetDevice(ctx->device));
@@ -167,6 +228,10 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
         CU(cudaMemcpy(a.d_i1, a.i1.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(a.d_t, a.t.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(a.d_omt, a.omt.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
+        CU(dev_alloc(&a.d_first, in_n));
+        CU(dev_alloc(&a.d_last, in_n));
+        CU(cudaMemcpy(a.d_first, a.first_out.data(), in_n * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(a.d_last, a.last_out.data(), in_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         it = ctx->axes.emplace(key, std::move(a)).first;
     }
     *out = &it->second;
@@ -305,10 +370,20 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     cudaStream_t s = ctx->stream;
 
     if (!blur && up == 1) {
+        KernelTimer kt(ctx, kNmsPlane);
         CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
-        ctx->launches += 1;
-    } else if (!blur && half <= kMaxFusedHalf) {
+    } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused) {
+        UpWinArgs a{};
+        a.conf = conf; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
+        a.ry = (double)h / (double)H;
+        a.rx = (double)w / (double)W;
+        a.thr = thr; a.half = half; a.cap = ctx->caps.max_peaks_per_part;
+        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+        a.first_out = rows->d_first; a.last_out = rows->d_last;
+        KernelTimer kt(ctx, kNmsUpWin);
+        CU(launch_nms_up_win(a, n, s));
+    } else if (!blur && half <= kMaxFusedHalf && !ctx->materialise) {
         UpArgs a{};
         a.conf = conf; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
         a.rows = rows->dev(); a.cols = cols->dev();
@@ -333,8 +408,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             if (ns > max_src) max_src = ns;
         }
         const size_t smem = nms_up_smem(max_src, w, half, band, W);
+        KernelTimer kt(ctx, kNmsUp);
         CU(launch_nms_up(a, n, smem, s));
-        ctx->launches += 1;
     } else {
         // materialised: resize (if up > 1) -> blur (if sigma > 0) -> NMS
         const size_t frame_full = (size_t)C * H * W;
@@ -343,23 +418,23 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         const float *nms_src = conf;
         long long src_frame = (long long)C * h * w;
         if (up > 1) {
+            KernelTimer kt(ctx, kResize);
             CU(launch_resize_planes(conf, (long long)n * C, h, w, ctx->d_full, H, W, rows->dev(),
                                     cols->dev(), ctx->sms, s));
-            ctx->launches += 1;
             nms_src = ctx->d_full;
             src_frame = (long long)frame_full;
         }
         if (blur) {
             BlurTaps taps;
             make_taps(p->blur_sigma, taps);
+            KernelTimer kt(ctx, kBlurRows, 2);   // rows + cols pass, timed together
             CU(launch_blur(nms_src, src_frame, ctx->d_tmp, ctx->d_full, (long long)frame_full, n, K,
                            H, W, taps, ctx->sms, s));
-            ctx->launches += 2;
             nms_src = ctx->d_full;
         }
+        KernelTimer kt(ctx, kNmsPlane);
         CU(launch_nms_plane(nms_src, n, C, K, H, W, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
-        ctx->launches += 1;
     }
 
     ParseArgs a{};
@@ -388,8 +463,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     a.dbg_nconns = ctx->d_dbg_nc; a.dbg_conn_i = ctx->d_dbg_ci; a.dbg_conn_d = ctx->d_dbg_cd;
     const int threads = 256;
     const size_t smem = parse_smem_bytes(a.cap_frame, a.cap_cands, a.cap_humans, K, threads / 32);
+    KernelTimer kt(ctx, kParseFrames);
     CU(launch_parse_frames(a, n, threads, smem, s));
-    ctx->launches += 1;
     return PF_OK;
 }
 
@@ -448,7 +523,7 @@ int chunk_for(pf_ctx *ctx, const pf_params *p, int h, int w)
 {
     int chunk = ctx->caps.chunk_frames;
     const bool materialise = p->blur_sigma > 0.0 ||
-                             (p->upsample > 1 && p->nms_window / 2 > kMaxFusedHalf);
+                             (p->upsample > 1 && (p->nms_window / 2 > kMaxFusedHalf || ctx->materialise));
     if (materialise) {
         // bound the full-resolution workspace to ~2 GiB
         const size_t per = (size_t)(ctx->topo.K + 1) * h * w * p->upsample * p->upsample * sizeof(float);
@@ -548,7 +623,10 @@ void pf_destroy(pf_ctx *ctx)
     for (auto &kv : ctx->axes) {
         cudaFree(kv.second.d_i0); cudaFree(kv.second.d_i1);
         cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
+        cudaFree(kv.second.d_first); cudaFree(kv.second.d_last);
     }
+    for (auto &p : ctx->pending) { ctx->ev_pool.push_back(p.second.first); ctx->ev_pool.push_back(p.second.second); }
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k) {
         if (ctx->ev_copied[k]) cudaEventDestroy(ctx->ev_copied[k]);
         if (ctx->ev_free[k]) cudaEventDestroy(ctx->ev_free[k]);
@@ -563,7 +641,14 @@ const char *pf_last_error(const pf_ctx *ctx) { return ctx ? ctx->err.c_str() : g
 int pf_set_stream(pf_ctx *ctx, void *cuda_stream)
 {
     if (!ctx) return PF_ERR_CONTRACT;
-    ctx->stream = cuda_stream ? reinterpret_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    return PF_OK;
+}
+
+int pf_use_own_stream(pf_ctx *ctx)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    ctx->stream = ctx->own_stream;
     return PF_OK;
 }
 
@@ -612,6 +697,42 @@ int pf_set_debug(pf_ctx *ctx, int enable)
 {
     if (!ctx) return PF_ERR_CONTRACT;
     ctx->debug = enable ? 1 : 0;
+    return PF_OK;
+}
+
+int pf_set_option(pf_ctx *ctx, int option, int value)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    switch (option) {
+    case PF_OPT_DEBUG: ctx->debug = value ? 1 : 0; return PF_OK;
+    case PF_OPT_TIMING: ctx->timing = value ? 1 : 0; return PF_OK;
+    case PF_OPT_MATERIALISE: ctx->materialise = value ? 1 : 0; return PF_OK;
+    case PF_OPT_GENERIC_FUSED: ctx->generic_fused = value ? 1 : 0; return PF_OK;
+    default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
+    }
+}
+
+const char *pf_kernel_name(int id) { return id >= 0 && id < PF_N_KERNELS ? kKernelNames[id] : ""; }
+
+int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    if (!ctx->pending.empty()) {
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (auto &p : ctx->pending) {
+            float t = 0.f;
+            CU(cudaEventElapsedTime(&t, p.second.first, p.second.second));
+            ctx->kernel_ms[p.first] += t;
+            ctx->ev_pool.push_back(p.second.first);
+            ctx->ev_pool.push_back(p.second.second);
+        }
+        ctx->pending.clear();
+    }
+    for (int k = 0; k < PF_N_KERNELS; ++k) {
+        if (ms) ms[k] = ctx->kernel_ms[k];
+        if (launches) launches[k] = ctx->kernel_launches[k];
+        if (reset) { ctx->kernel_ms[k] = 0.0; ctx->kernel_launches[k] = 0; }
+    }
     return PF_OK;
 }
 
@@ -851,8 +972,8 @@ static int preprocess_impl(pf_ctx *ctx, const void *src, int is_f32, int batch, 
         rt = r->dev();
         ct = c->dev();
     }
+    KernelTimer kt(ctx, kPreprocess);
     CU(launch_preprocess(src, is_f32, batch, h, w, dst, out_h, out_w, rt, ct, ctx->sms, ctx->stream));
-    ctx->launches += 1;
     return PF_OK;
 }
 
@@ -889,9 +1010,9 @@ int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int 
     if (rc) return rc;
     rc = get_axis(ctx, in_w, out_w, &c);
     if (rc) return rc;
+    KernelTimer kt(ctx, kResize);
     CU(launch_resize_planes(src, n_planes, in_h, in_w, dst, out_h, out_w, r->dev(), c->dev(), ctx->sms,
                             ctx->stream));
-    ctx->launches += 1;
     return PF_OK;
 }
 

@@ -21,6 +21,20 @@ struct UpArgs {
     uint2 *peaks;
 };
 constexpr int kMaxFusedHalf = 16;
+struct UpWinArgs {
+    const float *conf;   // low-res [B][C][h][w]
+    int C, K, h, w;
+    int H, W;            // parse grid
+    double ry, rx;       // h/H, w/W (operators.py:88-89 ratios)
+    float thr;
+    int half;            // 1 or 2
+    int cap;
+    int *counts;
+    uint2 *peaks;
+    const int32_t *first_out, *last_out;   // [h]: output rows reading source row r
+};
+size_t nms_up_win_smem(int h, int w, int threads);
+cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s);
 cudaError_t launch_nms_plane(const float *conf, int B, int C, int K, int H, int W, float thr,
                              int half, int cap, int *counts, uint2 *peaks, cudaStream_t s);
 size_t nms_up_smem(int n_src_max, int w, int half, int band_rows, int W);

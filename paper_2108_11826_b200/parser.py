@@ -144,6 +144,16 @@ class PafParser:
     def launch_count(self) -> int:
         return self.ctx.launch_count()
 
+    def set_timing(self, enable: bool) -> None:
+        self.ctx.set_option(_native.PF_OPT_TIMING, 1 if enable else 0)
+
+    def set_materialise(self, enable: bool) -> None:
+        """Force the unfused Mode U path (resize -> NMS through HBM)."""
+        self.ctx.set_option(_native.PF_OPT_MATERIALISE, 1 if enable else 0)
+
+    def kernel_times(self, reset: bool = False) -> dict:
+        return self.ctx.kernel_times(reset)
+
     def _check_arrays(self, conf_shape, paf_shape, stride):
         k, n_l = self.topo.n_keypoints, self.topo.n_limbs
         if len(conf_shape) != 4 or conf_shape[1] != k + 1:

@@ -50,3 +50,7 @@ total += check("procedural-U", [pf.procedural_scene(7, s, 656, 368, sp) for s in
 total += check("crowd-R", [pf.crowd_scene(3, s) for s in range(2)], 1)
 total += check("crowd-U", [pf.crowd_scene(3, s) for s in range(1)], 8)
 print("TOTAL mismatching", total)
+total += check("procedural-U-w5", [pf.procedural_scene(9, s, 656, 368, sp) for s in range(4)], 8, pf.ParserParams(nms_window=5))
+total += check("procedural-U-w7", [pf.procedural_scene(9, s, 656, 368, sp) for s in range(2)], 8, pf.ParserParams(nms_window=7))
+total += check("procedural-U-x4", [pf.procedural_scene(9, s, 656, 368, sp) for s in range(2)], 4)
+print("TOTAL2 mismatching", total)
