@@ -92,6 +92,7 @@ struct pf_ctx {
     // NMS workspace (chunk-sized)
     int *d_counts = nullptr;
     uint2 *d_peaks = nullptr;
+    void *d_spill = nullptr;     // candidate spill slab for crowded frames
     size_t ws_frames = 0;
     int ws_K = 0;
 
@@ -243,13 +244,17 @@ int ensure_nms_ws(pf_ctx *ctx, size_t frames, int K)
     if (frames <= ctx->ws_frames && K <= ctx->ws_K) return PF_OK;
     cudaFree(ctx->d_counts);
     cudaFree(ctx->d_peaks);
+    cudaFree(ctx->d_spill);
     ctx->d_counts = nullptr;
     ctx->d_peaks = nullptr;
+    ctx->d_spill = nullptr;
     const size_t f = frames > ctx->ws_frames ? frames : ctx->ws_frames;
     const int k = K > ctx->ws_K ? K : ctx->ws_K;
     CU(dev_alloc(&ctx->d_counts, f * k));
     CU(cudaMemset(ctx->d_counts, 0, f * k * sizeof(int)));
     CU(dev_alloc(&ctx->d_peaks, f * k * (size_t)ctx->caps.max_peaks_per_part));
+    CU(dev_alloc(reinterpret_cast<char **>(&ctx->d_spill),
+                 f * cand_spill_bytes_per_frame(ctx->caps.max_candidates)));
     ctx->ws_frames = f;
     ctx->ws_K = k;
     return PF_OK;
@@ -373,7 +378,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         KernelTimer kt(ctx, kNmsPlane);
         CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
-    } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused) {
+    } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
+               nms_up_win_smem(h, w, H, 128) <= 96 * 1024) {
         UpWinArgs a{};
         a.conf = conf; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
         a.ry = (double)h / (double)H;
@@ -461,7 +467,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     a.debug = ctx->debug;
     a.dbg_npeaks = ctx->d_dbg_np; a.dbg_peaks = ctx->d_dbg_peaks;
     a.dbg_nconns = ctx->d_dbg_nc; a.dbg_conn_i = ctx->d_dbg_ci; a.dbg_conn_d = ctx->d_dbg_cd;
-    const int threads = 256;
+    a.cand_spill = ctx->d_spill;
+    const int threads = kParseThreads;
     const size_t smem = parse_smem_bytes(a.cap_frame, a.cap_cands, a.cap_humans, K, threads / 32);
     KernelTimer kt(ctx, kParseFrames);
     CU(launch_parse_frames(a, n, threads, smem, s));
@@ -550,7 +557,7 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
     if (c.max_peaks_per_frame <= 0) c.max_peaks_per_frame = 1024;
     if (c.max_candidates <= 0) c.max_candidates = 4096;
     if (c.max_humans_per_frame <= 0) c.max_humans_per_frame = 256;
-    if (c.chunk_frames <= 0) c.chunk_frames = 1024;
+    if (c.chunk_frames <= 0) c.chunk_frames = 8192;
     // candidate storage doubles as the peak staging area; bitonic needs 2^k
     int pc = 1;
     while (pc < c.max_candidates) pc <<= 1;
@@ -598,7 +605,7 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
         cu(configure_parse_kernels(max_smem), "configure k_parse_frames"))
         return bail(PF_ERR_CUDA);
     const size_t need = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
-                                         PF_MAX_KEYPOINTS, 8) + 2048;
+                                         PF_MAX_KEYPOINTS, kParseThreads / 32) + 2048;
     if (need > (size_t)max_smem) {
         fail(ctx, PF_ERR_CONFIG, "caps need %zu B of shared memory per frame CTA (> %d)", need, max_smem);
         return bail(PF_ERR_CONFIG);
@@ -612,7 +619,7 @@ void pf_destroy(pf_ctx *ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    void *dev[] = {ctx->d_counts, ctx->d_peaks, ctx->d_frame_first, ctx->d_frame_count,
+    void *dev[] = {ctx->d_counts, ctx->d_peaks, ctx->d_spill, ctx->d_frame_first, ctx->d_frame_count,
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd};

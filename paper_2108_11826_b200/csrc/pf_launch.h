@@ -33,7 +33,7 @@ struct UpWinArgs {
     uint2 *peaks;
     const int32_t *first_out, *last_out;   // [h]: output rows reading source row r
 };
-size_t nms_up_win_smem(int h, int w, int threads);
+size_t nms_up_win_smem(int h, int w, int H, int threads);
 cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s);
 cudaError_t launch_nms_plane(const float *conf, int B, int C, int K, int H, int W, float thr,
                              int half, int cap, int *counts, uint2 *peaks, cudaStream_t s);
@@ -70,7 +70,11 @@ struct ParseArgs {
     int *dbg_nconns;
     int *dbg_conn_i;
     double *dbg_conn_d;
+    void *cand_spill;    // [frames][cap_cands - kCandSmem] candidate records (crowded frames)
 };
+constexpr int kCandSmem = 256;       // gated candidates kept in shared memory per frame
+constexpr int kParseThreads = 128;   // k_parse_frames CTA size
+size_t cand_spill_bytes_per_frame(int cap_cands);
 enum { kCapPart = 1, kCapFrame = 2, kCapCands = 3, kCapHumans = 4, kCapPool = 5 };
 size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps);
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s);

@@ -207,7 +207,8 @@ cudaError_t launch_nms_up(const UpArgs &a, int B, size_t smem, cudaStream_t s)
 // One CTA (4 warps) per (frame, part) plane.
 //  phase 1: the low-res plane is streamed once (16-byte loads) and turned into
 //           per-row "cell >= thr" bitmasks in shared memory (the compulsory
-//           HBM read of the path; later reads hit L1).
+//           HBM read of the path; later reads hit L1).  The output-row
+//           interpolation parameters (operators.py:87-96) go to a shared table.
 //  phase 2: a warp owns a strip of 32 - 2*HALF output columns (one lane per
 //           column, HALF halo lanes each side).  From the bitmasks it derives
 //           the strip's hot source rows and walks only the output rows whose
@@ -215,10 +216,13 @@ cudaError_t launch_nms_up(const UpArgs &a, int B, size_t smem, cudaStream_t s)
 //           lane keeps the horizontal interpolant of its two current source
 //           rows (the reference's `top`/`bot`, operators.py:104-105 — they
 //           depend on the source row only, so reuse is bit-exact) and spends
-//           2 DMUL + 1 DADD + 1 F2F per output.  The last 2*HALF+1 rows and
-//           their left/right neighbours (warp shuffles) sit in registers, so
-//           the NMS test (paf.py:87-99) never touches memory.  Out-of-grid
-//           neighbours are -inf, exactly the reference's padding.
+//           2 DMUL + 1 DADD + 1 F2F per output.
+//  NMS (paf.py:87-99) as two maxima: the centre must beat max(earlier
+//           neighbours) strictly and max(later neighbours) non-strictly.  The
+//           maxima propagate NaN (max.NaN.f32), so a NaN neighbour suppresses
+//           the centre exactly as numpy's compares do; out-of-grid neighbours
+//           are -inf, the reference's padding.  Row maxima are formed once per
+//           row from warp shuffles and kept in a register window.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void axis_at(int o, double ratio, int n_in, int &i0, int &i1, double &t,
                                         double &omt)
@@ -233,6 +237,13 @@ __device__ __forceinline__ void axis_at(int o, double ratio, int n_in, int &i0, 
     i1 = min(max(fi + 1, 0), n_in - 1);
 }
 
+__device__ __forceinline__ float max_nan(float a, float b)
+{
+    float d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+
 template <int HALF>
 __global__ void __launch_bounds__(128)
 k_nms_up_win(const UpWinArgs a)
@@ -243,16 +254,20 @@ k_nms_up_win(const UpWinArgs a)
     const int plane = blockIdx.x;
     const int b = plane / a.K, k = plane - b * a.K;
     const float *p = a.conf + ((size_t)b * a.C + k) * (size_t)a.h * a.w;
-    const int h = a.h, w = a.w;
+    const int h = a.h, w = a.w, H = a.H;
     const int n_cw = (w + 31) >> 5;          // column words per low-res row
     const int n_rw = (h + 31) >> 5;          // row words per strip mask
-    uint8_t *hot = reinterpret_cast<uint8_t *>(sm);                       // [h*w] bytes
-    uint32_t *rowmask = sm + ((h * w + 3) >> 2);                          // [h][n_cw]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_warps = blockDim.x >> 5;
-    uint32_t *srcmask = rowmask + h * n_cw + warp * n_rw;                  // per warp [n_rw]
+    // shared layout: row weights (ty, 1-ty) [H] | row source indices [H] |
+    //                hot bytes [h*w] | row masks [h][n_cw] | strip masks [warps][n_rw]
+    double2 *rt_w = reinterpret_cast<double2 *>(sm);
+    uint32_t *rt_idx = reinterpret_cast<uint32_t *>(rt_w + H);
+    uint8_t *hot = reinterpret_cast<uint8_t *>(rt_idx + H);
+    uint32_t *rowmask = reinterpret_cast<uint32_t *>(hot + ((h * w + 15) & ~15));
+    uint32_t *srcmask = rowmask + h * n_cw + warp * n_rw;
 
-    // ---- phase 1: stream the plane, hot bytes -> row bitmasks ----
+    // ---- phase 1: stream the plane -> hot bytes; row table ----
     const int hw = h * w;
     if ((hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
         const float4 *p4 = reinterpret_cast<const float4 *>(p);
@@ -264,12 +279,20 @@ k_nms_up_win(const UpWinArgs a)
     } else {
         for (int e = threadIdx.x; e < hw; e += blockDim.x) hot[e] = __ldg(p + e) >= a.thr;
     }
+    for (int y = threadIdx.x; y < H; y += blockDim.x) {
+        int i0, i1;
+        double t, omt;
+        axis_at(y, a.ry, h, i0, i1, t, omt);
+        rt_w[y] = make_double2(t, omt);
+        rt_idx[y] = uint32_t(i0) | (uint32_t(i1) << 16);
+    }
     __syncthreads();
-    for (int rq = warp; rq < h * n_cw; rq += n_warps) {
-        const int r = rq / n_cw, q = rq - r * n_cw;
-        const int col = (q << 5) + lane;
-        const uint32_t m = __ballot_sync(0xffffffffu, col < w && hot[r * w + col]);
-        if (lane == 0) rowmask[rq] = m;
+    for (int r = warp; r < h; r += n_warps) {
+        for (int q = 0; q < n_cw; ++q) {
+            const int col = (q << 5) + lane;
+            const uint32_t m = __ballot_sync(0xffffffffu, col < w && hot[r * w + col]);
+            if (lane == 0) rowmask[r * n_cw + q] = m;
+        }
     }
     __syncthreads();
 
@@ -283,18 +306,17 @@ k_nms_up_win(const UpWinArgs a)
         int j0, j1;
         double tx, omtx;
         axis_at(min(max(x, 0), a.W - 1), a.rx, w, j0, j1, tx, omtx);
-        // source-column span of the strip's useful columns
-        int cj0, cj1, dummy;
-        double dt, domt;
-        axis_at(x0, a.rx, w, cj0, dummy, dt, domt);
-        axis_at(min(x0 + SW, a.W) - 1, a.rx, w, dummy, cj1, dt, domt);
+        // source-column span of the strip's useful columns (lanes HALF and last useful)
+        const int last_useful = min(x0 + SW, a.W) - 1 - (x0 - HALF);
+        const int cj0 = __shfl_sync(0xffffffffu, j0, HALF);
+        const int cj1 = __shfl_sync(0xffffffffu, j1, last_useful);
         // hot source rows of this strip -> srcmask
         for (int r0 = 0; r0 < h; r0 += 32) {
             const int r = r0 + lane;
             bool any = false;
             if (r < h) {
                 for (int q = cj0 >> 5; q <= (cj1 >> 5) && !any; ++q) {
-                    uint32_t m = rowmask[r * n_cw + q];
+                    const uint32_t m = rowmask[r * n_cw + q];
                     const int lo = max(cj0 - (q << 5), 0), hi = min(cj1 - (q << 5), 31);
                     const uint32_t span = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
                     any = (m & span) != 0u;
@@ -305,20 +327,18 @@ k_nms_up_win(const UpWinArgs a)
         }
         __syncwarp();
 
-        // walk runs of needed output rows
+        // walk runs of needed output rows (warp-uniform control flow)
         int run_lo = -1, run_hi = -2;
         for (int q = 0; q <= n_rw; ++q) {
             uint32_t m = q < n_rw ? srcmask[q] : 0u;
             bool flush_final = q == n_rw;
             while (m || flush_final) {
-                int lo = 0, hi = 0;
-                bool have = false;
+                int lo = 0, hi = -1;
                 if (m) {
                     const int r = (q << 5) + __ffs(m) - 1;
                     m &= m - 1u;
                     lo = max(__ldg(a.first_out + r) - HALF, 0);
-                    hi = min(__ldg(a.last_out + r) + HALF, a.H - 1);
-                    have = true;
+                    hi = min(__ldg(a.last_out + r) + HALF, H - 1);
                     if (run_hi >= run_lo && lo <= run_hi + 1) {   // extend current run
                         run_hi = max(run_hi, hi);
                         continue;
@@ -328,24 +348,21 @@ k_nms_up_win(const UpWinArgs a)
                 }
                 if (run_hi >= run_lo) {
                     // ---- evaluate rows [run_lo, run_hi] ----
-                    float wv[WIN], wn[WIN][2 * HALF];
+                    // window index 0 = oldest row; HALF = centre; 2*HALF = newest
+                    float full[WIN], cv[WIN], lm[WIN], rm[WIN];
 #pragma unroll
-                    for (int t = 0; t < WIN; ++t) {
-                        wv[t] = -INFINITY;
-#pragma unroll
-                        for (int d = 0; d < 2 * HALF; ++d) wn[t][d] = -INFINITY;
-                    }
+                    for (int t = 0; t < WIN; ++t) { full[t] = cv[t] = lm[t] = rm[t] = -INFINITY; }
                     int ci0 = -1, ci1 = -1;
                     double hA = 0.0, hB = 0.0;
                     const int test_lo = run_lo == 0 ? 0 : run_lo + HALF;
-                    const int test_hi = run_hi == a.H - 1 ? a.H - 1 : run_hi - HALF;
-                    const int last_eval = run_hi == a.H - 1 ? run_hi + HALF : run_hi;
+                    const int test_hi = run_hi == H - 1 ? H - 1 : run_hi - HALF;
+                    const int last_eval = run_hi == H - 1 ? run_hi + HALF : run_hi;
                     for (int y = run_lo; y <= last_eval; ++y) {
                         float v = -INFINITY;
-                        if (y < a.H) {
-                            int i0, i1;
-                            double ty, omty;
-                            axis_at(y, a.ry, h, i0, i1, ty, omty);
+                        if (y < H) {
+                            const uint32_t idx = rt_idx[y];
+                            const double2 wy = rt_w[y];
+                            const int i0 = int(idx & 0xffffu), i1 = int(idx >> 16);
                             if (i0 != ci0) {
                                 hA = (i0 == ci1) ? hB
                                                  : dadd(dmul((double)__ldg(p + i0 * w + j0), omtx),
@@ -358,40 +375,38 @@ k_nms_up_win(const UpWinArgs a)
                                                         dmul((double)__ldg(p + i1 * w + j1), tx));
                                 ci1 = i1;
                             }
-                            v = in_grid ? __double2float_rn(dadd(dmul(hA, omty), dmul(hB, ty))) : -INFINITY;
+                            const float val = __double2float_rn(dadd(dmul(hA, wy.y), dmul(hB, wy.x)));
+                            v = in_grid ? val : -INFINITY;
                         }
-                        // shift window, add the new row with its neighbour columns
-#pragma unroll
-                        for (int t = 0; t < WIN - 1; ++t) {
-                            wv[t] = wv[t + 1];
-#pragma unroll
-                            for (int d = 0; d < 2 * HALF; ++d) wn[t][d] = wn[t + 1][d];
-                        }
-                        wv[WIN - 1] = v;
+                        // row maxima from the neighbouring lanes
+                        float lmax = -INFINITY, rmax = -INFINITY;
 #pragma unroll
                         for (int d = 1; d <= HALF; ++d) {
-                            wn[WIN - 1][HALF - d] = __shfl_up_sync(0xffffffffu, v, d);     // column x-d
-                            wn[WIN - 1][HALF + d - 1] = __shfl_down_sync(0xffffffffu, v, d); // column x+d
+                            lmax = max_nan(lmax, __shfl_up_sync(0xffffffffu, v, d));
+                            rmax = max_nan(rmax, __shfl_down_sync(0xffffffffu, v, d));
                         }
-                        const int yc = y - HALF;                    // centre row of the window
-                        const float c = wv[HALF];
-                        if (useful && yc >= test_lo && yc <= test_hi && c >= a.thr) {
-                            bool peak = true;
 #pragma unroll
-                            for (int di = -HALF; di <= HALF; ++di) {
-#pragma unroll
-                                for (int dj = -HALF; dj <= HALF; ++dj) {
-                                    if (di == 0 && dj == 0) continue;
-                                    const float nv = dj == 0 ? wv[HALF + di]
-                                                   : (dj < 0 ? wn[HALF + di][HALF + dj] : wn[HALF + di][HALF + dj - 1]);
-                                    peak &= nms_beats(c, nv, di, dj);
-                                }
-                            }
-                            if (peak) emit_peak(a.counts, a.peaks, plane, a.cap, c, yc, x);
+                        for (int t = 0; t < WIN - 1; ++t) {
+                            full[t] = full[t + 1]; cv[t] = cv[t + 1];
+                            lm[t] = lm[t + 1]; rm[t] = rm[t + 1];
                         }
+                        full[WIN - 1] = max_nan(max_nan(lmax, v), rmax);
+                        cv[WIN - 1] = v; lm[WIN - 1] = lmax; rm[WIN - 1] = rmax;
+                        // test the centre row
+                        float earlier = lm[HALF], later = rm[HALF];
+#pragma unroll
+                        for (int t = 0; t < HALF; ++t) {
+                            earlier = max_nan(earlier, full[t]);
+                            later = max_nan(later, full[HALF + 1 + t]);
+                        }
+                        const float c = cv[HALF];
+                        const int yc = y - HALF;
+                        const bool peak = useful && yc >= test_lo && yc <= test_hi && c >= a.thr &&
+                                          c > earlier && c >= later;
+                        if (peak) emit_peak(a.counts, a.peaks, plane, a.cap, c, yc, x);
                     }
                 }
-                if (have) { run_lo = lo; run_hi = hi; }
+                if (hi >= lo) { run_lo = lo; run_hi = hi; }
                 else { run_lo = -1; run_hi = -2; }
             }
         }
@@ -399,17 +414,18 @@ k_nms_up_win(const UpWinArgs a)
     }
 }
 
-size_t nms_up_win_smem(int h, int w, int threads)
+size_t nms_up_win_smem(int h, int w, int H, int threads)
 {
     const int n_cw = (w + 31) >> 5, n_rw = (h + 31) >> 5;
-    return (size_t)((h * w + 3) & ~3) + (size_t)h * n_cw * 4 + (size_t)(threads / 32) * n_rw * 4;
+    return (size_t)H * (16 + 4) + (size_t)((h * w + 15) & ~15) + (size_t)h * n_cw * 4 +
+           (size_t)(threads / 32) * n_rw * 4 + 16;
 }
 
 cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s)
 {
     const long long grid = (long long)B * a.K;
     if (grid == 0) return cudaSuccess;
-    const size_t smem = nms_up_win_smem(a.h, a.w, 128);
+    const size_t smem = nms_up_win_smem(a.h, a.w, a.H, 128);
     if (a.half == 1) k_nms_up_win<1><<<(unsigned)grid, 128, smem, s>>>(a);
     else if (a.half == 2) k_nms_up_win<2><<<(unsigned)grid, 128, smem, s>>>(a);
     else return cudaErrorInvalidValue;

@@ -1,20 +1,25 @@
 // pf_parse.cu — per-frame limb scoring, greedy matching and human assembly.
 //
-// One CTA per frame (frames are independent; paf.py:292-305 is pure).
-// Everything after peak extraction happens in shared memory:
+// One CTA (4 warps) per frame (frames are independent; paf.py:292-305 is
+// pure).  Everything after peak extraction happens on chip:
 //
 //   1. peak ids      — rank-sort each part's peaks by (score desc, row, col)
-//                      (paf.py:104) and prefix the parts (paf.py:298-303)
-//   2. line integral — every (limb, a, b) pair of the frame is one work item
-//                      over all threads: n_samples fp64 samples, nearest cell
-//                      (paf.py:112-146), gate good>=min && score>0
-//                      (paf.py:162); in Mode U the PAF value of a full-res
-//                      cell is re-derived on the fly from the low-res PAF
-//                      with the operators.py:102-107 fp64 formula
+//                      (paf.py:104) straight from the NMS slab and prefix the
+//                      parts (paf.py:298-303)
+//   2. line integral — a 16-lane group scores one (limb, a, b) pair: lane u
+//                      takes sample u (nearest cell, paf.py:138-145), so all
+//                      PAF reads of a pair are in flight together; the fp64
+//                      mean is then summed in sample order through shuffles
+//                      (paf.py:144 `total += d`, the reference's rounding
+//                      order) and the good count is a ballot.  Gate
+//                      good >= min && score > 0 (paf.py:162).  In Mode U the
+//                      PAF value of a full-res cell is re-derived from the
+//                      low-res PAF with the operators.py:102-107 fp64 formula.
 //   3. greedy        — bitonic sort of the gated candidates by
-//                      (limb, -score, id_a, id_b) (paf.py:173), then one warp
-//                      per limb walks its segment with used-bitmaps
-//                      (paf.py:174-181)
+//                      (limb, -score, id_a, id_b) (paf.py:173) in shared
+//                      memory (crowded frames spill past kCandSmem entries to
+//                      a per-frame global slab), then one warp per limb walks
+//                      its segment with used-bitmaps (paf.py:174-181)
 //   4. assembly      — one thread replays assemble_humans' order-dependent
 //                      branches exactly (paf.py:241-271) on shared tables
 //                      (owner per peak, part slots + dict insertion order +
@@ -43,6 +48,14 @@ __device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y)
     return (x.ab & 0x7fffffffu) < (y.ab & 0x7fffffffu);  // (id_a, id_b) lexicographic
 }
 
+// Candidate storage: the first kCandSmem entries in shared memory, the rest
+// (crowded frames only) in this frame's global spill slab.
+struct CandStore {
+    Cand *s;
+    Cand *g;
+    __device__ __forceinline__ Cand &operator[](int i) const { return i < kCandSmem ? s[i] : g[i - kCandSmem]; }
+};
+
 __device__ __forceinline__ double sample_paf(const ParseArgs &a, const float *__restrict__ ch,
                                              int ci, int cj)
 {
@@ -56,6 +69,18 @@ __device__ __forceinline__ double sample_paf(const ParseArgs &a, const float *__
     return (double)v;
 }
 
+// One sample of score_limb (paf.py:138-143): nearest cell at t = u/(n-1),
+// dot of the PAF vector with the unit limb direction.
+__device__ __forceinline__ double limb_sample(const ParseArgs &a, const float *chx, const float *chy,
+                                              int ai, int aj, int di, int dj, double vx, double vy,
+                                              int u, double den)
+{
+    const double t = __ddiv_rn((double)u, den);
+    const int ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
+    const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
+    return dadd(dmul(sample_paf(a, chx, ci, cj), vx), dmul(sample_paf(a, chy, ci, cj), vy));
+}
+
 // CPython 3.12 builtin sum() over floats starting from int 0 (Neumaier).
 __device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
 {
@@ -65,7 +90,7 @@ __device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
     f = t;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kParseThreads)
 k_parse_frames(const ParseArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -78,7 +103,7 @@ k_parse_frames(const ParseArgs a)
     __shared__ int s_base[PF_MAX_KEYPOINTS + 1];
     __shared__ int s_pp[PF_MAX_LIMBS + 1];      // pair prefix per limb
     __shared__ int s_seg[PF_MAX_LIMBS + 1];     // candidate segment start per limb
-    __shared__ int s_err, s_errval, s_ncand, s_nh, s_nkeep, s_pool_base;
+    __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base;
     __shared__ int8_t s_la[PF_MAX_LIMBS], s_lb[PF_MAX_LIMBS];
     __shared__ int16_t s_cx[PF_MAX_LIMBS], s_cy[PF_MAX_LIMBS];
     for (int l = tid; l < L; l += nthr) {
@@ -87,10 +112,9 @@ k_parse_frames(const ParseArgs a)
     }
 
     // ---- shared layout (sizes from the caps; see parse_smem_bytes) ----
-    Cand *cand = reinterpret_cast<Cand *>(smem_raw);                         // cap_cands
-    double *h_conn = reinterpret_cast<double *>(cand + a.cap_cands);         // cap_humans
-    double *h_final = h_conn + a.cap_humans;                                  // cap_humans
-    uint32_t *p_cell = reinterpret_cast<uint32_t *>(h_final + a.cap_humans); // cap_frame
+    Cand *cand_s = reinterpret_cast<Cand *>(smem_raw);                       // kCandSmem
+    double *h_score = reinterpret_cast<double *>(cand_s + kCandSmem);        // cap_humans (conn, then final)
+    uint32_t *p_cell = reinterpret_cast<uint32_t *>(h_score + a.cap_humans); // cap_frame
     float *p_score = reinterpret_cast<float *>(p_cell + a.cap_frame);        // cap_frame
     uint32_t *h_mask = reinterpret_cast<uint32_t *>(p_score + a.cap_frame);  // cap_humans
     int *h_pos = reinterpret_cast<int *>(h_mask + a.cap_humans);             // cap_humans
@@ -101,14 +125,15 @@ k_parse_frames(const ParseArgs a)
     int8_t *h_order = reinterpret_cast<int8_t *>(h_parts + a.cap_humans * K); // cap_humans*K
     int8_t *h_n = h_order + a.cap_humans * K;                                 // cap_humans
     int8_t *h_alive = h_n + a.cap_humans;                                     // cap_humans
+    const CandStore cand{cand_s, reinterpret_cast<Cand *>(a.cand_spill) +
+                                     (size_t)b * (a.cap_cands - kCandSmem)};
 
     // ---- 1. peak counts, prefix, capacity checks; reset counters ----
     if (tid == 0) { s_err = 0; s_ncand = 0; }
-    int my_cnt = 0;
     if (tid < K) {
-        my_cnt = a.counts[(size_t)b * K + tid];
+        const int c = a.counts[(size_t)b * K + tid];
         a.counts[(size_t)b * K + tid] = 0;   // ready for the next launch
-        s_base[tid + 1] = my_cnt;
+        s_base[tid + 1] = c;
     }
     __syncthreads();
     if (tid == 0) {
@@ -134,29 +159,24 @@ k_parse_frames(const ParseArgs a)
     }
     const int P = s_base[K];
 
-    // ---- 2. stage raw peaks, rank-sort within each part ----
-    uint2 *stage = reinterpret_cast<uint2 *>(cand);   // P <= cap_frame <= 2*cap_cands
+    // ---- 2. rank-sort each part's peaks (read straight from the NMS slab) ----
     for (int e = tid; e < P; e += nthr) {
         int part = 0;
         while (e >= s_base[part + 1]) ++part;
-        stage[e] = __ldg(a.peaks + ((size_t)b * K + part) * a.cap_part + (e - s_base[part]));
-    }
-    __syncthreads();
-    for (int e = tid; e < P; e += nthr) {
-        int part = 0;
-        while (e >= s_base[part + 1]) ++part;
-        const uint2 v = stage[e];
+        const uint2 *slab = a.peaks + ((size_t)b * K + part) * a.cap_part;
+        const int np = s_base[part + 1] - s_base[part];
+        const uint2 v = __ldg(slab + (e - s_base[part]));
         const float vs = __uint_as_float(v.x);
         int rank = 0;
-        for (int q = s_base[part]; q < s_base[part + 1]; ++q) {
-            const uint2 u = stage[q];
+        for (int q = 0; q < np; ++q) {
+            const uint2 u = __ldg(slab + q);
             const float us = __uint_as_float(u.x);
             rank += (us > vs) || (us == vs && u.y < v.y);
         }
         p_cell[s_base[part] + rank] = v.y;
         p_score[s_base[part] + rank] = vs;
+        owner[e] = -1;
     }
-    for (int e = tid; e < P; e += nthr) owner[e] = -1;
     if (tid == 0) {
         int acc = 0;
         for (int l = 0; l < L; ++l) {
@@ -179,47 +199,68 @@ k_parse_frames(const ParseArgs a)
         if (tid == 0) a.dbg_npeaks[gframe] = P;
     }
 
-    // ---- 3. line integral over every candidate pair ----
+    // ---- 3. line integral: a lane group per pair, a lane per sample ----
     const float *paf_f = a.paf + (size_t)b * (2 * L) * a.h * a.w;
     const int n_pairs = s_pp[L];
     const int n = a.n_samples;
-    const double inv_den = (double)(n - 1);
-    for (int p = tid; p < n_pairs; p += nthr) {
-        int l = 0;
-        while (p >= s_pp[l + 1]) ++l;
-        const int pa_part = s_la[l], pb_part = s_lb[l];
-        const int nb = s_base[pb_part + 1] - s_base[pb_part];
-        const int local = p - s_pp[l];
-        const int ia = s_base[pa_part] + local / nb, ib = s_base[pb_part] + local % nb;
-        const int ai = int(p_cell[ia] >> 16), aj = int(p_cell[ia] & 0xffff);
-        const int bi = int(p_cell[ib] >> 16), bj = int(p_cell[ib] & 0xffff);
-        if (ai == bi && aj == bj) continue;          // (0, 0) never passes the gate
-        const int di = bi - ai, dj = bj - aj;
-        const double norm = __dsqrt_rn((double)(di * di + dj * dj));
-        const double vx = __ddiv_rn((double)dj, norm), vy = __ddiv_rn((double)di, norm);
+    const double den = (double)(n - 1);
+    const int G = n <= 32 ? n : 32;                       // lanes per pair (one per sample)
+    const int gpw = kWarp / G;                            // pairs per warp pass
+    const int grp = min(lane / G, gpw - 1), gl = lane - grp * G;
+    const bool in_group = lane < gpw * G;
+    const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
+    int l_cur = 0;                                        // limb search resumes (p grows)
+    for (int p0 = warp * gpw; p0 < n_pairs; p0 += n_warps * gpw) {
+        const int p = p0 + grp;
+        bool live = in_group && p < n_pairs;
+        int l = l_cur, ia = 0, ib = 0, ai = 0, aj = 0, di = 0, dj = 0;
+        double vx = 0.0, vy = 0.0;
+        if (live) {
+            while (p >= s_pp[l + 1]) ++l;
+            l_cur = l;
+            const int pa_part = s_la[l], pb_part = s_lb[l];
+            const int nb = s_base[pb_part + 1] - s_base[pb_part];
+            const int local = p - s_pp[l];
+            ia = s_base[pa_part] + local / nb;
+            ib = s_base[pb_part] + local % nb;
+            ai = int(p_cell[ia] >> 16); aj = int(p_cell[ia] & 0xffff);
+            const int bi = int(p_cell[ib] >> 16), bj = int(p_cell[ib] & 0xffff);
+            di = bi - ai; dj = bj - aj;
+            live = (di | dj) != 0;          // coincident cells score (0, 0): never gated
+            if (live) {
+                const double norm = __dsqrt_rn((double)(di * di + dj * dj));
+                vx = __ddiv_rn((double)dj, norm);
+                vy = __ddiv_rn((double)di, norm);
+            }
+        }
         const float *chx = paf_f + (size_t)s_cx[l] * a.h * a.w;
         const float *chy = paf_f + (size_t)s_cy[l] * a.h * a.w;
         double total = 0.0;
         int ngood = 0;
-        for (int u = 0; u < n; ++u) {
-            const double t = __ddiv_rn((double)u, inv_den);
-            const int ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
-            const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
-            const double d = dadd(dmul(sample_paf(a, chx, ci, cj), vx),
-                                  dmul(sample_paf(a, chy, ci, cj), vy));
-            total = dadd(total, d);
-            ngood += (d >= a.dot_thr);
+        if (n <= 32) {
+            double d = 0.0;
+            if (live && gl < n) d = limb_sample(a, chx, chy, ai, aj, di, dj, vx, vy, gl, den);
+            ngood = __popc(__ballot_sync(0xffffffffu, live && gl < n && d >= a.dot_thr) & gmask);
+            for (int u = 0; u < n; ++u) total = dadd(total, __shfl_sync(0xffffffffu, d, grp * G + u));
+        } else if (live && gl == 0) {       // long line integrals: one lane, sequential
+            for (int u = 0; u < n; ++u) {
+                const double d = limb_sample(a, chx, chy, ai, aj, di, dj, vx, vy, u, den);
+                total = dadd(total, d);
+                ngood += (d >= a.dot_thr);
+            }
         }
-        const double score = __ddiv_rn(total, (double)n);
-        const double good = __ddiv_rn((double)ngood, (double)n);
-        if (good >= a.good_min && score > 0.0) {
-            const int slot = atomicAdd(&s_ncand, 1);
-            if (slot < a.cap_cands) {
-                Cand c;
-                c.score = score;
-                c.ab = (uint32_t(ia) << 16) | uint32_t(ib);
-                c.lg = (uint32_t(l) << 24) | uint32_t(ngood);
-                cand[slot] = c;
+        if (live && gl == 0) {
+            const double score = __ddiv_rn(total, (double)n);
+            const double good = __ddiv_rn((double)ngood, (double)n);
+            if (good >= a.good_min && score > 0.0) {
+                const int slot = atomicAdd(&s_ncand, 1);
+                if (slot < a.cap_cands) {
+                    Cand c;
+                    c.score = score;
+                    c.ab = (uint32_t(ia) << 16) | uint32_t(ib);
+                    c.lg = (uint32_t(l) << 24) | uint32_t(ngood);
+                    cand[slot] = c;
+                }
             }
         }
     }
@@ -280,6 +321,7 @@ k_parse_frames(const ParseArgs a)
     uint32_t *used_a = used + warp * 2 * bm_words;
     uint32_t *used_b = used_a + bm_words;
     for (int l = warp; l < L; l += n_warps) {
+        if (s_seg[l] == s_seg[l + 1]) continue;           // warp-uniform
         for (int q = lane; q < bm_words; q += kWarp) { used_a[q] = 0u; used_b[q] = 0u; }
         __syncwarp();
         if (lane == 0) {
@@ -321,7 +363,7 @@ k_parse_frames(const ParseArgs a)
             const int a_part = s_la[l], b_part = s_lb[l];
             const int pa = int((c.ab >> 16) & 0x7fff), pb = int(c.ab & 0xffff);
             const int ha = owner[pa], hb = owner[pb];
-            if (ha < 0 && hb < 0) {
+            if (ha < 0 && hb < 0) {                                  // paf.py:246-253
                 if (nh >= a.cap_humans) { err = 1; break; }
                 int16_t *parts = h_parts + nh * K;
                 for (int k = 0; k < K; ++k) parts[k] = -1;
@@ -331,15 +373,15 @@ k_parse_frames(const ParseArgs a)
                 h_order[nh * K + 1] = int8_t(b_part);
                 h_n[nh] = 2;
                 h_mask[nh] = (1u << a_part) | (1u << b_part);
-                h_conn[nh] = c.score;
+                h_score[nh] = c.score;
                 h_alive[nh] = 1;
                 owner[pa] = int16_t(nh);
                 owner[pb] = int16_t(nh);
                 ++nh;
             } else if (ha >= 0 && hb >= 0) {
-                if (ha == hb) {
-                    h_conn[ha] = dadd(h_conn[ha], c.score);
-                } else if ((h_mask[ha] & h_mask[hb]) == 0u) {
+                if (ha == hb) {                                      // paf.py:255-256
+                    h_score[ha] = dadd(h_score[ha], c.score);
+                } else if ((h_mask[ha] & h_mask[hb]) == 0u) {        // paf.py:257-262
                     const int nB = h_n[hb];
                     int nA = h_n[ha];
                     for (int q = 0; q < nB; ++q) {
@@ -351,10 +393,10 @@ k_parse_frames(const ParseArgs a)
                     }
                     h_n[ha] = int8_t(nA);
                     h_mask[ha] |= h_mask[hb];
-                    h_conn[ha] = dadd(h_conn[ha], dadd(h_conn[hb], c.score));
+                    h_score[ha] = dadd(h_score[ha], dadd(h_score[hb], c.score));
                     h_alive[hb] = 0;
-                }
-            } else {
+                }                                                    // else paf.py:263
+            } else {                                                 // paf.py:264-271
                 const int hidx = ha >= 0 ? ha : hb;
                 const int part = ha >= 0 ? b_part : a_part;
                 const int pid = ha >= 0 ? pb : pa;
@@ -363,7 +405,7 @@ k_parse_frames(const ParseArgs a)
                     h_order[hidx * K + h_n[hidx]] = int8_t(part);
                     h_n[hidx] = int8_t(h_n[hidx] + 1);
                     h_mask[hidx] |= 1u << part;
-                    h_conn[hidx] = dadd(h_conn[hidx], c.score);
+                    h_score[hidx] = dadd(h_score[hidx], c.score);
                     owner[pid] = int16_t(hidx);
                 }
             }
@@ -395,30 +437,29 @@ k_parse_frames(const ParseArgs a)
                 else neumaier_add(f, c, v);
             }
             if (c != 0.0 && isfinite(c)) f = dadd(f, c);
-            score = __ddiv_rn(dadd(f, h_conn[hh]), (double)np);
+            score = __ddiv_rn(dadd(f, h_score[hh]), (double)np);
             keep = !(score < a.min_score);
         }
-        h_final[hh] = score;
+        h_score[hh] = score;          // connection sum no longer needed
         h_pos[hh] = keep ? 1 : 0;
     }
     __syncthreads();
     // stable rank by -score among kept humans (paf.py:288)
     for (int hh = tid; hh < nh; hh += nthr) {
         if (!h_pos[hh]) continue;
-        const double s = h_final[hh];
+        const double s = h_score[hh];
         int pos = 0;
         for (int g = 0; g < nh; ++g) {
             if (!h_pos[g]) continue;
-            const double sg = h_final[g];
+            const double sg = h_score[g];
             pos += (sg > s) || (sg == s && g < hh);
         }
-        h_mask[hh] = uint32_t(pos);   // mask no longer needed; reuse as rank
+        h_mask[hh] = uint32_t(pos);   // part mask no longer needed; reuse as rank
     }
     __syncthreads();
     if (tid == 0) {
         int nk = 0;
         for (int hh = 0; hh < nh; ++hh) nk += h_pos[hh];
-        s_nkeep = nk;
         const int base = nk ? atomicAdd(&a.st->pool_used, nk) : 0;
         if (base + nk > a.pool_cap) {
             report_capacity(a.st, gframe, kCapPool, base + nk);
@@ -440,7 +481,7 @@ k_parse_frames(const ParseArgs a)
         if (!h_pos[hh]) continue;
         const size_t o = (size_t)(base + int(h_mask[hh]));
         if (k == 0) {
-            a.h_score[o] = h_final[hh];
+            a.h_score[o] = h_score[hh];
             a.h_nparts[o] = h_n[hh];
         }
         const int pid = h_parts[hh * K + k];
@@ -460,9 +501,10 @@ k_parse_frames(const ParseArgs a)
 
 size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps)
 {
+    (void)cap_cands;
     const int bm_words = (cap_frame + 31) / 32;
-    size_t s = (size_t)cap_cands * sizeof(Cand);
-    s += (size_t)cap_humans * 2 * sizeof(double);
+    size_t s = (size_t)kCandSmem * sizeof(Cand);
+    s += (size_t)cap_humans * sizeof(double);
     s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
     s += (size_t)cap_humans * (sizeof(uint32_t) + sizeof(int));
     s += (size_t)n_warps * 2 * bm_words * sizeof(uint32_t);
@@ -470,6 +512,11 @@ size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int
     s += (size_t)cap_humans * K * (sizeof(int16_t) + sizeof(int8_t));
     s += (size_t)cap_humans * 2;
     return (s + 15) & ~size_t(15);
+}
+
+size_t cand_spill_bytes_per_frame(int cap_cands)
+{
+    return cap_cands > kCandSmem ? (size_t)(cap_cands - kCandSmem) * sizeof(Cand) : 0;
 }
 
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s)
