@@ -87,7 +87,9 @@ typedef struct pf_caps {
 /* Results of the last parse call, in context-owned pinned host memory,
  * valid until the next parse on the same context.  Humans of frame f are
  * entries frame_first[f] .. frame_first[f] + frame_count[f] - 1, already in
- * the reference output order (score descending, stable, paf.py:288). */
+ * the reference output order (score descending, stable, paf.py:288).  The
+ * placement of whole frames inside the pool is unspecified (frames reserve
+ * their slots concurrently); always address a frame through frame_first. */
 typedef struct pf_results {
     int32_t n_frames;
     int32_t n_keypoints;
@@ -123,7 +125,10 @@ int pf_validate_params(const pf_params *p);
 
 /* Parse `batch` frames whose maps are resident on the device:
  * conf [batch][K+1][grid_h][grid_w], paf [batch][2L][grid_h][grid_w],
- * contiguous f32 (FeatureMaps layout, types.py:169-205).  Asynchronous. */
+ * contiguous f32 (FeatureMaps layout, types.py:169-205).  Asynchronous.
+ * The maps must stay valid until pf_get_results() returns: when the
+ * auto-sized output pool (max_humans_total = 0) overflows, the call is
+ * replayed once with a pool of the exact size instead of failing. */
 int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch,
                     int grid_h, int grid_w, int stride, const pf_params *p);
 
@@ -180,6 +185,11 @@ int pf_preprocess_f32_device(pf_ctx *ctx, const float *src, int batch, int h, in
  * [n_planes][out_h][out_w] (device). */
 int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int in_w,
                      float *dst, int out_h, int out_w);
+
+/* The smoothing taps used for blur_sigma > 0: radius
+ * r = ceil(3 sigma), w_k = exp(-k^2 / (2 sigma^2)) / sum, k = -r..r.  Writes
+ * 2r+1 taps (if cap allows) and returns r, or -1 for an invalid sigma. */
+int pf_gaussian_taps(double sigma, double *taps, int cap);
 
 /* Pinned host allocation helpers for callers without their own allocator. */
 void *pf_host_alloc(size_t bytes);

@@ -66,6 +66,7 @@ def _load():
                                    c_int, c_double, ctypes.POINTER(c_double),
                                    ctypes.POINTER(c_double)]
     lib.orc_score_limb.restype = None
+    lib.orc_greedy_select.argtypes = [f64p, i32p, i32p, c_int, i32p]
     lib.orc_py_sum.argtypes = [f64p, c_int]
     lib.orc_py_sum.restype = c_double
     lib.orc_parse.argtypes = [f32p, f32p, c_int, c_int, i32p, i32p, c_int, c_int, c_int,
@@ -229,6 +230,19 @@ def score_limb(paf: np.ndarray, topo, limb: int, cell_a, cell_b, n_samples: int,
                        int(cell_b[0]), int(cell_b[1]), int(n_samples),
                        float(sample_dot_threshold), ctypes.byref(s), ctypes.byref(g))
     return s.value, g.value
+
+
+def greedy_select(candidates):
+    """``paf._greedy_select`` (paf.py:168-182): candidates are
+    ``(id_a, id_b, score)``; returns the accepted ones in acceptance order."""
+    lib = _load()
+    n = len(candidates)
+    sc = np.ascontiguousarray([c[2] for c in candidates] or [0.0], dtype=np.float64)
+    ia = np.ascontiguousarray([c[0] for c in candidates] or [0], dtype=np.int32)
+    ib = np.ascontiguousarray([c[1] for c in candidates] or [0], dtype=np.int32)
+    out = np.zeros(max(n, 1), np.int32)
+    m = lib.orc_greedy_select(sc, ia, ib, n, out)
+    return [candidates[int(out[q])] for q in range(m)]
 
 
 def py_sum(values: Sequence[float]) -> float:

@@ -279,6 +279,37 @@ static int cand_cmp(const void *pa, const void *pb)
     return 0;
 }
 
+static int cand_cmp_stable(const void *pa, const void *pb)
+{
+    int c = cand_cmp(pa, pb);
+    if (c) return c;
+    const cand *x = pa, *y = pb;          /* `good` carries the input position */
+    return (x->good > y->good) - (x->good < y->good);
+}
+
+int orc_greedy_select(const double *score, const int32_t *id_a, const int32_t *id_b,
+                      int n, int32_t *accepted)
+{
+    cand *cs = malloc(sizeof(cand) * ((size_t)n + 1));
+    int32_t max_id = 0;
+    for (int q = 0; q < n; ++q) {
+        cs[q].score = score[q]; cs[q].good = (double)q; cs[q].a = id_a[q]; cs[q].b = id_b[q];
+        if (id_a[q] > max_id) max_id = id_a[q];
+        if (id_b[q] > max_id) max_id = id_b[q];
+    }
+    qsort(cs, (size_t)n, sizeof(cand), cand_cmp_stable);   /* paf.py:173, sorted() is stable */
+    uint8_t *ua = calloc((size_t)max_id + 1, 1), *ub = calloc((size_t)max_id + 1, 1);
+    int m = 0;
+    for (int q = 0; q < n; ++q) {                        /* paf.py:176-181 */
+        if (ua[cs[q].a] || ub[cs[q].b]) continue;
+        ua[cs[q].a] = 1;
+        ub[cs[q].b] = 1;
+        accepted[m++] = (int32_t)cs[q].good;
+    }
+    free(ua); free(ub); free(cs);
+    return m;
+}
+
 typedef struct builder {             /* paf.py:202-207 _Builder */
     int32_t *parts;                  /* [K] peak id or -1 */
     int32_t *order;                  /* dict insertion order of part keys */

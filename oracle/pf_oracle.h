@@ -86,6 +86,12 @@ void orc_score_limb(const float *paf_x, const float *paf_y, int h, int w,
                     int ai, int aj, int bi, int bj, int n_samples,
                     double sample_dot_threshold, double *score, double *good);
 
+/* paf.py:168-182 _greedy_select on one limb's candidates (score, id_a,
+ * id_b); writes the accepted candidate indices in acceptance order and
+ * returns their count. */
+int orc_greedy_select(const double *score, const int32_t *id_a, const int32_t *id_b,
+                      int n, int32_t *accepted);
+
 /* CPython >= 3.12 builtin sum() of a float sequence starting from int 0. */
 double orc_py_sum(const double *x, int n);
 

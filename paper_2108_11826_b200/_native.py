@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "pf_get_results", "pf_sync", "pf_set_debug", "pf_set_option", "pf_kernel_name",
     "pf_get_kernel_times", "pf_get_peaks", "pf_get_connections",
     "pf_preprocess_device", "pf_preprocess_f32_device", "pf_resize_device", "pf_host_alloc", "pf_host_free",
-    "pf_launch_count",
+    "pf_launch_count", "pf_gaussian_taps",
 )
 
 
@@ -124,9 +124,20 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pf_host_free.restype = None
         lib.pf_launch_count.argtypes = [vp]
         lib.pf_launch_count.restype = ctypes.c_int64
+        lib.pf_gaussian_taps.argtypes = [ctypes.c_double, vp, c_int]
         del i32
         _lib = lib
         return lib
+
+
+def gaussian_taps(sigma: float) -> np.ndarray:
+    """The exact smoothing taps the library applies for ``blur_sigma``."""
+    lib = load_library()
+    buf = np.zeros(2 * 64 + 1, np.float64)
+    r = lib.pf_gaussian_taps(float(sigma), buf.ctypes.data, buf.size)
+    if r < 0:
+        raise ConfigError(f"invalid blur_sigma {sigma}")
+    return buf[: 2 * r + 1].copy()
 
 
 def raise_for(code: int, message: str) -> None:

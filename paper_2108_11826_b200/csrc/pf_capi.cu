@@ -95,6 +95,9 @@ struct pf_ctx {
     void *d_spill = nullptr;     // candidate spill slab for crowded frames
     size_t ws_frames = 0;
     int ws_K = 0;
+    int ws_cap_part = 0, ws_cap_cands = 0;
+    int auto_caps = 0;           // bit kCap* set: that capacity grows on demand
+    int max_smem = 0;
 
     // resize tables, keyed by (in, out)
     std::map<std::pair<int, int>, AxisCache> axes;
@@ -126,6 +129,7 @@ struct pf_ctx {
     int4 *d_dbg_peaks = nullptr;
     double *d_dbg_cd = nullptr;
     size_t dbg_frames = 0;
+    int dbg_cap_frame = 0, dbg_cap_cands = 0;
 
     // per-kernel timing (PF_OPT_TIMING)
     int timing = 0;
@@ -139,6 +143,16 @@ struct pf_ctx {
     int last_batch = 0;
     int last_K = 0;
     bool results_ready = false;
+
+    // the last parse call, replayed once with a larger output pool when the
+    // default pool (64 humans/frame) overflows and no fixed cap was requested
+    struct {
+        int kind = 0;                 // 0 none, 1 device, 2 host
+        const float *conf = nullptr, *paf = nullptr;
+        int batch = 0, h = 0, w = 0, stride = 1;
+        pf_params p{};
+    } last;
+    long long pool_need = 0;
 };
 
 namespace {
@@ -241,7 +255,11 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
 
 int ensure_nms_ws(pf_ctx *ctx, size_t frames, int K)
 {
-    if (frames <= ctx->ws_frames && K <= ctx->ws_K) return PF_OK;
+    if (frames <= ctx->ws_frames && K <= ctx->ws_K && ctx->ws_cap_part == ctx->caps.max_peaks_per_part &&
+        ctx->ws_cap_cands == ctx->caps.max_candidates)
+        return PF_OK;
+    ctx->ws_cap_part = ctx->caps.max_peaks_per_part;
+    ctx->ws_cap_cands = ctx->caps.max_candidates;
     cudaFree(ctx->d_counts);
     cudaFree(ctx->d_peaks);
     cudaFree(ctx->d_spill);
@@ -301,7 +319,12 @@ int ensure_pool(pf_ctx *ctx, size_t humans, int K)
 
 int ensure_debug(pf_ctx *ctx, size_t frames)
 {
-    if (!ctx->debug || frames <= ctx->dbg_frames) return PF_OK;
+    if (!ctx->debug || (frames <= ctx->dbg_frames && ctx->dbg_cap_frame == ctx->caps.max_peaks_per_frame &&
+                        ctx->dbg_cap_cands == ctx->caps.max_candidates))
+        return PF_OK;
+    if (frames < ctx->dbg_frames) frames = ctx->dbg_frames;
+    ctx->dbg_cap_frame = ctx->caps.max_peaks_per_frame;
+    ctx->dbg_cap_cands = ctx->caps.max_candidates;
     cudaFree(ctx->d_dbg_np); cudaFree(ctx->d_dbg_nc); cudaFree(ctx->d_dbg_ci);
     cudaFree(ctx->d_dbg_peaks); cudaFree(ctx->d_dbg_cd);
     CU(dev_alloc(&ctx->d_dbg_np, frames));
@@ -507,11 +530,70 @@ int begin_call(pf_ctx *ctx, int batch, int pool_cap)
     return PF_OK;
 }
 
+// Output pool size for a call: the fixed cap if the caller set one, else
+// 64 humans per frame, grown (never shrunk) to whatever a previous call needed.
 int pool_cap_for(pf_ctx *ctx, int batch)
 {
     if (ctx->caps.max_humans_total > 0) return ctx->caps.max_humans_total;
     long long v = 64LL * (batch > 0 ? batch : 1);
+    if (v < (long long)ctx->pool_cap) v = (long long)ctx->pool_cap;
+    if (v < ctx->pool_need) v = ctx->pool_need;
     return (int)(v > (1LL << 30) ? (1LL << 30) : v);
+}
+
+// Grow the automatic capacity a failed call ran out of; false if that
+// capacity is fixed by the caller or cannot grow (shared-memory bound).
+bool grow_cap(pf_ctx *ctx, const Status &st)
+{
+    if (!((ctx->auto_caps >> st.what) & 1)) return false;
+    pf_caps c = ctx->caps;
+    const long long need = st.value > 0 ? st.value : 1;
+    switch (st.what) {
+    case kCapPool:
+        if ((long long)st.pool_used <= ctx->pool_need) return false;
+        ctx->pool_need = st.pool_used;
+        return true;
+    case kCapPart: {
+        long long v = c.max_peaks_per_part;
+        while (v < need) v *= 2;
+        c.max_peaks_per_part = (int)(v > (1 << 20) ? (1 << 20) : v);
+        if (c.max_peaks_per_part > c.max_peaks_per_frame && ((ctx->auto_caps >> kCapFrame) & 1))
+            c.max_peaks_per_frame = c.max_peaks_per_part < 32767 ? c.max_peaks_per_part : 32767;
+        break;
+    }
+    case kCapCands: {
+        long long v = c.max_candidates;
+        while (v < need) v *= 2;
+        if (v > (1 << 24)) return false;
+        c.max_candidates = (int)v;
+        break;
+    }
+    case kCapFrame: {
+        long long v = c.max_peaks_per_frame;
+        while (v < need) v *= 2;
+        if (v > 32767) v = 32767;
+        if (v < need) return false;
+        c.max_peaks_per_frame = (int)v;
+        break;
+    }
+    case kCapHumans: {
+        long long v = c.max_humans_per_frame * 2LL;
+        if (v > 32767) return false;
+        c.max_humans_per_frame = (int)v;
+        break;
+    }
+    default:
+        return false;
+    }
+    const size_t smem = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
+                                         PF_MAX_KEYPOINTS, kParseThreads / 32) + 2048;
+    if (smem > (size_t)ctx->max_smem) return false;
+    if (c.max_peaks_per_part == ctx->caps.max_peaks_per_part && c.max_candidates == ctx->caps.max_candidates &&
+        c.max_peaks_per_frame == ctx->caps.max_peaks_per_frame &&
+        c.max_humans_per_frame == ctx->caps.max_humans_per_frame)
+        return false;
+    ctx->caps = c;
+    return true;
 }
 
 int prepare_axes(pf_ctx *ctx, int h, int w, const pf_params *p, AxisCache **rows, AxisCache **cols)
@@ -553,21 +635,26 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
     *out = nullptr;
     pf_caps c{};
     if (caps) c = *caps;
-    if (c.max_peaks_per_part <= 0) c.max_peaks_per_part = 128;
-    if (c.max_peaks_per_frame <= 0) c.max_peaks_per_frame = 1024;
-    if (c.max_candidates <= 0) c.max_candidates = 4096;
-    if (c.max_humans_per_frame <= 0) c.max_humans_per_frame = 256;
+    // caps left at 0 are automatic: they start at the defaults and grow (with
+    // a replay of the call) when a frame needs more; explicit caps are fixed
+    int auto_caps = 0;
+    if (c.max_peaks_per_part <= 0) { c.max_peaks_per_part = 128; auto_caps |= 1 << kCapPart; }
+    if (c.max_peaks_per_frame <= 0) { c.max_peaks_per_frame = 1024; auto_caps |= 1 << kCapFrame; }
+    if (c.max_candidates <= 0) { c.max_candidates = 4096; auto_caps |= 1 << kCapCands; }
+    if (c.max_humans_per_frame <= 0) { c.max_humans_per_frame = 256; auto_caps |= 1 << kCapHumans; }
+    if (c.max_humans_total <= 0) auto_caps |= 1 << kCapPool;
     if (c.chunk_frames <= 0) c.chunk_frames = 8192;
-    // candidate storage doubles as the peak staging area; bitonic needs 2^k
+    // bitonic sort over the candidate store needs a power of two
     int pc = 1;
     while (pc < c.max_candidates) pc <<= 1;
     c.max_candidates = pc;
-    if (c.max_peaks_per_frame > 32767 || c.max_peaks_per_frame > 2 * c.max_candidates)
-        return fail(nullptr, PF_ERR_CONFIG, "max_peaks_per_frame must be <= min(32767, 2*max_candidates)");
+    if (c.max_peaks_per_frame > 32767)
+        return fail(nullptr, PF_ERR_CONFIG, "max_peaks_per_frame must be <= 32767");
     if (c.max_humans_per_frame > 32767) return fail(nullptr, PF_ERR_CONFIG, "max_humans_per_frame > 32767");
     pf_ctx *ctx = new pf_ctx();
     ctx->device = device;
     ctx->caps = c;
+    ctx->auto_caps = auto_caps;
     auto bail = [&](int code) {
         g_create_err = ctx->err;
         pf_destroy(ctx);
@@ -601,6 +688,7 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
         cu(cudaHostAlloc(&ctx->h_status, sizeof(Status), cudaHostAllocDefault), "cudaHostAlloc status"))
         return bail(PF_ERR_CUDA);
     const int max_smem = prop.sharedMemPerBlockOptin;
+    ctx->max_smem = max_smem;
     if (cu(configure_nms_kernels(max_smem), "configure k_nms_up") ||
         cu(configure_parse_kernels(max_smem), "configure k_parse_frames"))
         return bail(PF_ERR_CUDA);
@@ -757,6 +845,10 @@ int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch,
     if (rc) return rc;
     ctx->last_batch = batch;
     ctx->last_K = K;
+    ctx->last.kind = 1;
+    ctx->last.conf = conf; ctx->last.paf = paf;
+    ctx->last.batch = batch; ctx->last.h = grid_h; ctx->last.w = grid_w; ctx->last.stride = stride;
+    ctx->last.p = *p;
     if (batch == 0) return PF_OK;
     if (grid_h == 0 || grid_w == 0) {
         // no cells, no peaks: every frame parses to [] (nms_peaks on empty maps)
@@ -803,6 +895,16 @@ int pf_get_results(pf_ctx *ctx, pf_results *out)
         }
         CU(cudaStreamSynchronize(ctx->stream));
         const Status st = *ctx->h_status;
+        if (st.code == PF_ERR_CAPACITY && ctx->last.kind != 0 && grow_cap(ctx, st)) {
+            // an automatic capacity was too small for some frame: it has been
+            // grown to the need and the call is replayed (inputs must stay
+            // valid until results are fetched)
+            const auto L = ctx->last;
+            rc = L.kind == 1 ? pf_parse_device(ctx, L.conf, L.paf, L.batch, L.h, L.w, L.stride, &L.p)
+                             : pf_parse_host(ctx, L.conf, L.paf, L.batch, L.h, L.w, L.stride, &L.p, nullptr);
+            if (rc) return rc;
+            return pf_get_results(ctx, out);
+        }
         if (st.code == PF_ERR_CAPACITY) {
             static const char *what[] = {"?", "max_peaks_per_part", "max_peaks_per_frame",
                                          "max_candidates", "max_humans_per_frame", "max_humans_total"};
@@ -856,6 +958,10 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     if (rc) return rc;
     ctx->last_batch = batch;
     ctx->last_K = K;
+    ctx->last.kind = 2;
+    ctx->last.conf = conf; ctx->last.paf = paf;
+    ctx->last.batch = batch; ctx->last.h = grid_h; ctx->last.w = grid_w; ctx->last.stride = stride;
+    ctx->last.p = *p;
     AxisCache *rows, *cols;
     rc = prepare_axes(ctx, grid_h, grid_w, p, &rows, &cols);
     if (rc) return rc;
@@ -1021,6 +1127,15 @@ int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int 
     CU(launch_resize_planes(src, n_planes, in_h, in_w, dst, out_h, out_w, r->dev(), c->dev(), ctx->sms,
                             ctx->stream));
     return PF_OK;
+}
+
+int pf_gaussian_taps(double sigma, double *taps, int cap)
+{
+    if (!(sigma > 0.0) || !std::isfinite(sigma) || (int)std::ceil(3.0 * sigma) > kMaxBlurRadius) return -1;
+    BlurTaps t;
+    make_taps(sigma, t);
+    for (int k = 0; k <= 2 * t.r && taps && k < cap; ++k) taps[k] = t.w[k];
+    return t.r;
 }
 
 void *pf_host_alloc(size_t bytes)

@@ -1,0 +1,292 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden fixtures and the oracle, bit-exact — peaks, connections (fp64 scores),
+person assignment, human scores and pose_record bytes."""
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2108_11826_b200 as pf
+from conftest import golden_path, record_of
+
+pytestmark = pytest.mark.gpu
+
+SP = pf.SynthParams()
+
+
+@pytest.fixture(scope="module")
+def eng(topo):
+    e = pf.PafParser(topo, debug=True)
+    yield e
+    e.close()
+
+
+def oracle_run(conf, paf, topo, params, stride=8):
+    if params.upsample == 1 and params.blur_sigma == 0:
+        return oracle.parse(conf, paf, topo, params, stride)
+    taps = pf._native.gaussian_taps(params.blur_sigma) if params.blur_sigma > 0 else None
+    return oracle.parse_upsampled(conf, paf, topo, params, stride, params.upsample, taps)
+
+
+def assert_batch_matches(eng, topo, conf, paf, params, stride=8, stages=True):
+    got = eng.parse_arrays(conf, paf, stride, params)
+    for f in range(conf.shape[0]):
+        want = oracle_run(conf[f], paf[f], topo, params, stride)
+        if stages:
+            assert eng.peaks(f) == want.peaks, f"frame {f} peaks"
+            assert eng.connections(f) == want.connections, f"frame {f} connections"
+        assert pf.pose_record(f, got.poses(f), topo) == record_of(want.humans, topo, f), f"frame {f}"
+    return got
+
+
+def render(scenes, topo):
+    return pf.synth.render_batch(scenes, topo, SP)
+
+
+# ---------------------------------------------------------------- golden
+@pytest.mark.parametrize("mode", ["R", "U"])
+def test_reference_golden_frames(eng, topo, golden_frames, mode):
+    data, recs = golden_frames
+    names = [n for n in recs["names"] if mode == "R" or n in recs["U"]]
+    conf = np.stack([data[f"{n}.conf"] for n in names])
+    paf = np.stack([data[f"{n}.paf"] for n in names])
+    params = pf.ParserParams(upsample=1 if mode == "R" else recs["up"])
+    got = eng.parse_arrays(conf, paf, 8, params)
+    for f, name in enumerate(names):
+        pk, ps = data[f"{name}.{mode}.peaks"], data[f"{name}.{mode}.peak_scores"]
+        assert eng.peaks(f) == [(int(a), int(b), int(c), float(s), q)
+                                for q, ((a, b, c), s) in enumerate(zip(pk, ps))], name
+        cn, cv = data[f"{name}.{mode}.conns"], data[f"{name}.{mode}.conn_vals"]
+        assert eng.connections(f) == [(int(a), int(b), int(c), float(s), float(g))
+                                      for (a, b, c), (s, g) in zip(cn, cv)], name
+        assert pf.pose_record(0, got.poses(f), topo) == recs[mode][name], name
+
+
+def test_nms_golden_maps():
+    """nms_peaks on the reference's random / plateau / threshold-edge maps."""
+    g = np.load(golden_path("nms_golden.npz"))
+    one = pf.SkeletonTopology.create(["p"], [])
+    e = pf.PafParser(one, debug=True)
+    maps = g["maps"]
+    off = 0
+    for i in range(maps.shape[0]):
+        conf = np.stack([maps[i], np.zeros_like(maps[i])])[None]
+        paf = np.zeros((1, 0) + maps.shape[1:], np.float32)
+        params = pf.ParserParams(conf_threshold=float(g["thresholds"][i]), nms_window=int(g["windows"][i]))
+        e.parse_arrays(conf, paf, 1, params)
+        n = int(g["counts"][i])
+        want = [(0, int(c[0]), int(c[1]), float(s), q)
+                for q, (c, s) in enumerate(zip(g["cells"][off:off + n], g["scores"][off:off + n]))]
+        off += n
+        assert e.peaks(0) == want, f"case {i}"
+    off = 0
+    for i in range(g["w5_maps"].shape[0]):
+        m = g["w5_maps"][i]
+        e.parse_arrays(np.stack([m, np.zeros_like(m)])[None], np.zeros((1, 0, 10, 10), np.float32), 1,
+                       pf.ParserParams(nms_window=5))
+        n = int(g["w5_counts"][i])
+        want = [(0, int(c[0]), int(c[1]), float(s), q)
+                for q, (c, s) in enumerate(zip(g["w5_cells"][off:off + n], g["w5_scores"][off:off + n]))]
+        off += n
+        assert e.peaks(0) == want
+    e.close()
+
+
+def test_score_limb_golden():
+    """score_limb through the full pipeline: one limb, two single-cell peaks."""
+    g = np.load(golden_path("score_golden.npz"))
+    two = pf.SkeletonTopology.create(["a", "b"], [[0, 1]])
+    e = pf.PafParser(two, debug=True)
+    params = pf.ParserParams(good_fraction_min=0.0, min_parts=1, min_human_score=-1.0)
+    checked = 0
+    for fld, meta, vals in zip(g["fields"], g["meta"], g["vals"]):
+        n, _limb, ai, aj, bi, bj = (int(v) for v in meta)
+        if (ai, aj) == (bi, bj):
+            continue
+        conf = np.zeros((1, 3, n, n), np.float32)
+        conf[0, 0, ai, aj] = 1.0
+        conf[0, 1, bi, bj] = 1.0
+        paf = fld[None, :, :n, :n].astype(np.float32)
+        e.parse_arrays(conf, paf, 1, params)
+        conns = e.connections(0)
+        s, gd = float(vals[0]), float(vals[1])
+        if s > 0.0:
+            assert conns == [(0, 0, 1, s, gd)]
+            checked += 1
+        else:
+            assert conns == []
+    assert checked > 50
+    e.close()
+
+
+# ---------------------------------------------------------------- vs oracle
+@pytest.mark.parametrize("up", [1, 8])
+def test_procedural_frames(eng, topo, up):
+    scenes = [pf.procedural_scene(7, s, 656, 368, SP) for s in range(24 if up == 1 else 8)]
+    conf, paf = render(scenes, topo)
+    assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
+
+
+@pytest.mark.parametrize("up", [1, 8])
+def test_crowded_frames(eng, topo, up):
+    """40-person scenes: merges, part conflicts, slot-taken skips, min_parts drops,
+    and > kCandSmem gated candidates (the global spill path)."""
+    scenes = [pf.crowd_scene(3, s) for s in range(3 if up == 1 else 1)]
+    conf, paf = render(scenes, topo)
+    assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
+
+
+@pytest.mark.parametrize("kw", [dict(nms_window=5), dict(nms_window=7), dict(nms_window=9),
+                                dict(n_samples=2), dict(n_samples=17), dict(n_samples=40),
+                                dict(conf_threshold=0.05), dict(conf_threshold=0.3), dict(conf_threshold=0.7),
+                                dict(sample_dot_threshold=0.5), dict(good_fraction_min=0.5),
+                                dict(good_fraction_min=1.0), dict(min_parts=1), dict(min_parts=12),
+                                dict(min_human_score=0.0), dict(min_human_score=0.9)])
+@pytest.mark.parametrize("up", [1, 8])
+def test_param_variants(eng, topo, kw, up):
+    scenes = [pf.procedural_scene(19, s, 656, 368, SP) for s in range(3)] + [pf.crowd_scene(5, 0)]
+    conf, paf = render(scenes, topo)
+    assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up, **kw))
+
+
+@pytest.mark.parametrize("up", [2, 4])
+def test_other_upsample_factors(eng, topo, up):
+    scenes = [pf.procedural_scene(23, s, 656, 368, SP) for s in range(3)]
+    conf, paf = render(scenes, topo)
+    assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
+
+
+def test_stride_and_odd_grid(eng, topo):
+    # 45x37 grid, stride 8 -> 360x296 input; 1 person near the border
+    scene = pf.GroundTruthScene(humans=(pf.procedural_scene(2, 0, 360, 296, SP).humans), input_w=360,
+                                input_h=296)
+    conf, paf = render([scene], topo)
+    for up in (1, 2, 8):
+        assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
+
+
+def test_random_fields(topo):
+    """Unstructured maps: many peaks, ties (quantised values), random PAFs,
+    thousands of gated candidates per frame (spill slab), many merges."""
+    rng = np.random.default_rng(77)
+    conf = rng.random((4, 19, 12, 14)).astype(np.float32)
+    conf[::2] = np.round(conf[::2] * 8) / 8
+    paf = rng.uniform(-1, 1, (4, 38, 12, 14)).astype(np.float32)
+    e = pf.PafParser(topo, debug=True, caps=dict(max_candidates=16384, max_humans_per_frame=1024))
+    for up in (1, 4):
+        assert_batch_matches(e, topo, conf, paf, pf.ParserParams(upsample=up, good_fraction_min=0.3,
+                                                                  min_parts=2))
+    e.close()
+
+
+def test_blur_paths(eng, topo):
+    scenes = [pf.procedural_scene(29, s, 656, 368, SP) for s in range(2)]
+    conf, paf = render(scenes, topo)
+    for up, sigma in ((8, 1.0), (8, 2.5), (1, 0.8)):
+        assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up, blur_sigma=sigma))
+
+
+def test_materialised_and_generic_paths_agree(topo):
+    scenes = [pf.procedural_scene(31, s, 656, 368, SP) for s in range(4)] + [pf.crowd_scene(8, 1)]
+    conf, paf = render(scenes, topo)
+    params = pf.ParserParams(upsample=8)
+    e = pf.PafParser(topo, debug=True)
+    ref = [pf.pose_record(f, p, topo) for f, p in enumerate(e.parse_arrays(conf, paf, 8, params).all_poses())]
+    e.set_materialise(True)
+    assert [pf.pose_record(f, p, topo) for f, p in enumerate(e.parse_arrays(conf, paf, 8, params).all_poses())] == ref
+    e.set_materialise(False)
+    e.ctx.set_option(pf._native.PF_OPT_GENERIC_FUSED, 1)
+    assert [pf.pose_record(f, p, topo) for f, p in enumerate(e.parse_arrays(conf, paf, 8, params).all_poses())] == ref
+    e.close()
+
+
+# ---------------------------------------------------------------- API contract
+def test_parse_drop_in(topo):
+    """parse(maps, topo, params) returns HumanPose lists equal to the reference's."""
+    scene = pf.procedural_scene(0, 1, 656, 368, SP)
+    maps = pf.render_feature_maps(scene, topo, SP)
+    poses = pf.parse(maps, topo, pf.ParserParams())
+    want = oracle.parse(maps.conf.array, maps.paf.array, topo, pf.ParserParams(), 8)
+    assert pf.pose_record(0, poses, topo) == record_of(want.humans, topo)
+    assert all(isinstance(p, pf.HumanPose) for p in poses) and len(poses) == 3
+    for p in poses:
+        p.validate(input_w=656, input_h=368)
+
+
+def test_parse_batch_equals_per_frame(topo):
+    maps = [pf.render_feature_maps(pf.procedural_scene(4, s, 656, 368, SP), topo, SP) for s in range(5)]
+    params = pf.ParserParams(upsample=8)
+    batch = pf.parse_batch(maps, topo, params)
+    single = [pf.parse(m, topo, params) for m in maps]
+    assert [pf.pose_record(i, p, topo) for i, p in enumerate(batch)] == \
+           [pf.pose_record(i, p, topo) for i, p in enumerate(single)]
+    shuffled = pf.parse_batch(maps[::-1], topo, params)[::-1]
+    assert [pf.pose_record(i, p, topo) for i, p in enumerate(shuffled)] == \
+           [pf.pose_record(i, p, topo) for i, p in enumerate(single)]
+
+
+def test_deterministic(eng, topo):
+    conf, paf = render([pf.crowd_scene(4, s) for s in range(2)], topo)
+    a = eng.parse_arrays(conf, paf, 8, pf.ParserParams(upsample=8))
+    b = eng.parse_arrays(conf, paf, 8, pf.ParserParams(upsample=8))
+    assert [pf.pose_record(f, a.poses(f), topo) for f in range(2)] == \
+           [pf.pose_record(f, b.poses(f), topo) for f in range(2)]
+
+
+def test_device_tensor_path(topo):
+    import torch
+
+    conf, paf = render([pf.procedural_scene(6, s, 656, 368, SP) for s in range(6)], topo)
+    params = pf.ParserParams(upsample=8)
+    e = pf.PafParser(topo)
+    host = e.parse_arrays(conf, paf, 8, params)
+    e.parse_tensors(torch.from_numpy(conf).cuda(), torch.from_numpy(paf).cuda(), 8, params)
+    dev = e.results()
+    assert [pf.pose_record(f, host.poses(f), topo) for f in range(6)] == \
+           [pf.pose_record(f, dev.poses(f), topo) for f in range(6)]
+    assert e.launch_count() >= 4
+    e.close()
+
+
+def test_empty_inputs(eng, topo):
+    assert pf.parse_batch([], topo, pf.ParserParams()) == []
+    zero = pf.render_feature_maps(pf.GroundTruthScene((), 64, 64), topo, SP)
+    assert pf.parse(zero, topo, pf.ParserParams()) == []
+    r = eng.parse_arrays(np.zeros((3, 19, 0, 0), np.float32), np.zeros((3, 38, 0, 0), np.float32), 8,
+                         pf.ParserParams())
+    assert r.n_frames == 3 and r.total_humans == 0
+    tiny = np.zeros((1, 19, 1, 1), np.float32)
+    tiny[0, :18] = 1.0
+    r = eng.parse_arrays(tiny, np.ones((1, 38, 1, 1), np.float32), 8, pf.ParserParams(upsample=8))
+    assert eng.peaks(0)[0][:3] == (0, 0, 0)
+
+
+def test_errors_before_work(topo):
+    maps = pf.render_feature_maps(pf.procedural_scene(0, 1, 656, 368, SP), topo, SP)
+    with pytest.raises(pf.ConfigError):
+        pf.parse(maps, topo, pf.ParserParams(nms_window=4))
+    stub = pf.SkeletonTopology.create(["a", "b"], [[0, 1]])
+    with pytest.raises(pf.ContractError):
+        pf.parse(maps, stub, pf.ParserParams())
+    e = pf.PafParser(topo)
+    with pytest.raises(pf.ContractError):    # stride not divisible by upsample
+        e.parse_arrays(maps.conf.array[None], maps.paf.array[None], 8, pf.ParserParams(upsample=3))
+    e.close()
+
+
+def test_capacity_errors_are_loud(topo):
+    conf, paf = render([pf.crowd_scene(3, 0)], topo)
+    e = pf.PafParser(topo, caps=dict(max_peaks_per_part=8))
+    with pytest.raises(pf.CapacityError, match="max_peaks_per_part"):
+        e.parse_arrays(conf, paf, 8, pf.ParserParams())
+    e.close()
+    e = pf.PafParser(topo, caps=dict(max_candidates=512))
+    with pytest.raises(pf.CapacityError, match="max_candidates"):
+        e.parse_arrays(conf, paf, 8, pf.ParserParams(upsample=8))
+    e.close()
+    e = pf.PafParser(topo, caps=dict(max_humans_total=3))
+    with pytest.raises(pf.CapacityError):
+        e.parse_arrays(conf, paf, 8, pf.ParserParams())
+    e.close()
