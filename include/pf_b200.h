@@ -159,6 +159,7 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_TIMING 2
 #define PF_OPT_MATERIALISE 3
 #define PF_OPT_GENERIC_FUSED 4   /* use the shared-memory tile kernel for Mode U */
+#define PF_OPT_WIN_VARIANT 5     /* register-window kernel: 2 (two columns/lane) or 1 */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch

@@ -29,7 +29,9 @@ struct AxisCache {
     std::vector<int32_t> i0, i1;
     std::vector<double> t, omt;
     std::vector<int32_t> first_out, last_out;   // inverse map: outputs reading input row r
-    int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr;
+    std::vector<int32_t> gend;                  // last output row with the same source pair
+    int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr, *d_gend = nullptr;
+    double2 *d_tw = nullptr;
     double *d_t = nullptr, *d_omt = nullptr;
     AxisTab dev() const { return AxisTab{d_i0, d_i1, d_t, d_omt}; }
 };
@@ -52,6 +54,9 @@ void fill_axis(AxisCache &a, int in_n, int out_n)
         a.i0[o] = (int32_t)(f < 0 ? 0 : (f > in_n - 1 ? in_n - 1 : f));
         a.i1[o] = (int32_t)(f + 1 < 0 ? 0 : (f + 1 > in_n - 1 ? in_n - 1 : f + 1));
     }
+    a.gend.resize(out_n);
+    for (int o = out_n - 1; o >= 0; --o)
+        a.gend[o] = (o + 1 < out_n && a.i0[o + 1] == a.i0[o] && a.i1[o + 1] == a.i1[o]) ? a.gend[o + 1] : o;
     a.first_out.assign(in_n, 0x3fffffff);
     a.last_out.assign(in_n, -1);
     for (int o = 0; o < out_n; ++o) {
@@ -135,6 +140,7 @@ struct pf_ctx {
     int timing = 0;
     int materialise = 0;
     int generic_fused = 0;
+    int win_variant = 3;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double kernel_ms[PF_N_KERNELS] = {0};
@@ -243,6 +249,14 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
         CU(cudaMemcpy(a.d_i1, a.i1.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(a.d_t, a.t.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(a.d_omt, a.omt.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
+        {
+            std::vector<double2> tw(out_n);
+            for (int o = 0; o < out_n; ++o) tw[o] = make_double2(a.t[o], a.omt[o]);
+            CU(dev_alloc(&a.d_tw, out_n));
+            CU(cudaMemcpy(a.d_tw, tw.data(), out_n * sizeof(double2), cudaMemcpyHostToDevice));
+        }
+        CU(dev_alloc(&a.d_gend, out_n));
+        CU(cudaMemcpy(a.d_gend, a.gend.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_first, in_n));
         CU(dev_alloc(&a.d_last, in_n));
         CU(cudaMemcpy(a.d_first, a.first_out.data(), in_n * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -410,6 +424,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.thr = thr; a.half = half; a.cap = ctx->caps.max_peaks_per_part;
         a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
         a.first_out = rows->d_first; a.last_out = rows->d_last;
+        a.variant = ctx->win_variant;
+        a.rows = rows->dev(); a.cols = cols->dev(); a.gend = rows->d_gend; a.tw = rows->d_tw;
         KernelTimer kt(ctx, kNmsUpWin);
         CU(launch_nms_up_win(a, n, s));
     } else if (!blur && half <= kMaxFusedHalf && !ctx->materialise) {
@@ -718,7 +734,7 @@ void pf_destroy(pf_ctx *ctx)
     for (auto &kv : ctx->axes) {
         cudaFree(kv.second.d_i0); cudaFree(kv.second.d_i1);
         cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
-        cudaFree(kv.second.d_first); cudaFree(kv.second.d_last);
+        cudaFree(kv.second.d_first); cudaFree(kv.second.d_last); cudaFree(kv.second.d_gend); cudaFree(kv.second.d_tw);
     }
     for (auto &p : ctx->pending) { ctx->ev_pool.push_back(p.second.first); ctx->ev_pool.push_back(p.second.second); }
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -803,6 +819,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_TIMING: ctx->timing = value ? 1 : 0; return PF_OK;
     case PF_OPT_MATERIALISE: ctx->materialise = value ? 1 : 0; return PF_OK;
     case PF_OPT_GENERIC_FUSED: ctx->generic_fused = value ? 1 : 0; return PF_OK;
+    case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 3) ? value : 3; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }

@@ -244,6 +244,450 @@ __device__ __forceinline__ float max_nan(float a, float b)
     return d;
 }
 
+// ---------------------------------------------------------------------------
+// k_nms_up_win2<HALF>: the same algorithm with two output columns per lane
+// (strips of 60 useful columns; lanes 0 and 31 carry the NMS halo) and an
+// inner row loop per source-row pair, so the interpolant refresh and all
+// row-invariant work leave the hot loop: per output row a lane spends one
+// broadcast LDS.128 (the row weights), 4 DMUL + 2 DADD + 2 F2F for its two
+// outputs, 2*HALF shuffles and a handful of NaN-propagating maxima.
+// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// k_nms_up_win3<HALF>: win2 with the per-plane setup stripped down.
+//  * row tables (source pair, weights, last row of each pair) are built once
+//    per context on the host and read through L1 (warp-uniform loads);
+//  * the "cell >= thr" bits come straight out of the 16-byte plane loads
+//    (a nibble per lane, OR-combined across 8 lanes with shuffles) into a
+//    flat bitmap — no byte array, no per-row ballots;
+//  * no per-row test-range predicate: rows outside a run's tested range are
+//    halo rows whose values are < thr (their sources are cold), so the
+//    threshold compare rejects them, and un-filled window slots are -inf;
+//  * -inf padding rows below the grid are handled after the hot loop;
+//  * the interpolant of a source row is reused when it moves from the lower
+//    to the upper position of the pair.
+// ---------------------------------------------------------------------------
+template <int HALF>
+__device__ __forceinline__ void win3_row(const float v0, const float v1, const bool use0, const bool use1,
+                                         float (&full)[2][2 * HALF + 1], float (&cv)[2][2 * HALF + 1],
+                                         float (&lm)[2][2 * HALF + 1], float (&rm)[2][2 * HALF + 1],
+                                         const UpWinArgs &a, int plane, int yc, const int (&xc)[2])
+{
+    constexpr int WIN = 2 * HALF + 1;
+    const float v[2] = {v0, v1};
+    const float l1 = __shfl_up_sync(0xffffffffu, v1, 1);
+    const float r1 = __shfl_down_sync(0xffffffffu, v0, 1);
+    float lmx[2], rmx[2];
+    if (HALF == 1) {
+        lmx[0] = l1;   rmx[0] = v1;
+        lmx[1] = v0;   rmx[1] = r1;
+    } else {
+        const float l2 = __shfl_up_sync(0xffffffffu, v0, 1);
+        const float r2 = __shfl_down_sync(0xffffffffu, v1, 1);
+        lmx[0] = max_nan(l1, l2);   rmx[0] = max_nan(v1, r1);
+        lmx[1] = max_nan(v0, l1);   rmx[1] = max_nan(r1, r2);
+    }
+    const bool use[2] = {use0, use1};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int t = 0; t < WIN - 1; ++t) {
+            full[c][t] = full[c][t + 1]; cv[c][t] = cv[c][t + 1];
+            lm[c][t] = lm[c][t + 1]; rm[c][t] = rm[c][t + 1];
+        }
+        full[c][WIN - 1] = max_nan(max_nan(lmx[c], v[c]), rmx[c]);
+        cv[c][WIN - 1] = v[c]; lm[c][WIN - 1] = lmx[c]; rm[c][WIN - 1] = rmx[c];
+        float earlier = lm[c][HALF], later = rm[c][HALF];
+#pragma unroll
+        for (int t = 0; t < HALF; ++t) {
+            earlier = max_nan(earlier, full[c][t]);
+            later = max_nan(later, full[c][HALF + 1 + t]);
+        }
+        const float cc = cv[c][HALF];
+        const bool pk = use[c] && cc >= a.thr && cc > earlier && cc >= later;
+        if (__any_sync(0xffffffffu, pk)) {            // rare: keep packing out of the row loop
+            if (pk) emit_peak(a.counts, a.peaks, plane, a.cap, cc, yc, xc[c]);
+        }
+    }
+}
+
+// Rows [y, run_hi] of one run for one strip; EDGE strips mask out-of-grid
+// columns to -inf (the reference's padding), interior strips skip the select.
+template <int HALF, bool EDGE>
+__device__ __forceinline__ void win3_run(const UpWinArgs &a, const float *__restrict__ p, int plane,
+                                         int run_lo, int run_hi, const int (&xc)[2], const int (&j0)[2],
+                                         const int (&j1)[2], const double (&tx)[2], const double (&omtx)[2],
+                                         const bool (&in_grid)[2], const bool (&useful)[2])
+{
+    constexpr int WIN = 2 * HALF + 1;
+    const int w = a.w, H = a.H;
+    float full[2][WIN], cv[2][WIN], lm[2][WIN], rm[2][WIN];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int t = 0; t < WIN; ++t) full[c][t] = cv[c][t] = lm[c][t] = rm[c][t] = -INFINITY;
+    double hA[2] = {0.0, 0.0}, hB[2] = {0.0, 0.0};
+    int ci1 = -1;
+    int y = run_lo;
+    while (y <= run_hi) {
+        const int i0 = __ldg(a.rows.i0 + y), i1 = __ldg(a.rows.i1 + y);
+        if (i0 == ci1) {                   // warp-uniform: the upper row of the last pair
+            hA[0] = hB[0];
+            hA[1] = hB[1];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                hA[c] = dadd(dmul((double)__ldg(p + i0 * w + j0[c]), omtx[c]),
+                             dmul((double)__ldg(p + i0 * w + j1[c]), tx[c]));
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            hB[c] = dadd(dmul((double)__ldg(p + i1 * w + j0[c]), omtx[c]),
+                         dmul((double)__ldg(p + i1 * w + j1[c]), tx[c]));
+        ci1 = i1;
+        const int yend = min(__ldg(a.gend + y), run_hi);
+        for (; y <= yend; ++y) {
+            const double2 wt = __ldg(a.tw + y);          // (t, 1 - t) of output row y
+            float v[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const float val = __double2float_rn(dadd(dmul(hA[c], wt.y), dmul(hB[c], wt.x)));
+                v[c] = (EDGE && !in_grid[c]) ? -INFINITY : val;
+            }
+            win3_row<HALF>(v[0], v[1], useful[0], useful[1], full, cv, lm, rm, a, plane, y - HALF, xc);
+        }
+    }
+    if (run_hi == H - 1) {                 // -inf padding rows below the grid
+#pragma unroll
+        for (int t = 1; t <= HALF; ++t)
+            win3_row<HALF>(-INFINITY, -INFINITY, useful[0], useful[1], full, cv, lm, rm, a, plane,
+                           H - 1 + t - HALF, xc);
+    }
+}
+
+template <int HALF>
+__global__ void __launch_bounds__(128, 8)
+k_nms_up_win3(const UpWinArgs a)
+{
+    constexpr int SW = 2 * (kWarp - 2);
+    constexpr int WIN = 2 * HALF + 1;
+    extern __shared__ __align__(16) uint32_t sm[];
+    const int plane = blockIdx.x;
+    const int b = plane / a.K, k = plane - b * a.K;
+    const float *p = a.conf + ((size_t)b * a.C + k) * (size_t)a.h * a.w;
+    const int h = a.h, w = a.w, H = a.H;
+    const int hw = h * w;
+    const int n_bw = ((hw + 127) & ~127) >> 5;   // words of the flat hot bitmap (128-cell padded)
+    const int n_rw = (h + 31) >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_warps = blockDim.x >> 5;
+    uint32_t *hotbits = sm;                                  // [n_bw]
+    uint32_t *srcmask = sm + n_bw + warp * n_rw;             // per warp [n_rw]
+
+    // ---- phase 1: stream the plane -> flat bitmap of cells >= thr ----
+    // all 16-byte loads of a thread are issued before any is consumed
+    if ((hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const float4 *p4 = reinterpret_cast<const float4 *>(p);
+        const int n4 = hw >> 2, n4_pad = (n4 + 31) & ~31;               // whole warps per pass
+        constexpr int U = 8;
+        for (int e0 = threadIdx.x; e0 < n4_pad; e0 += U * blockDim.x) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                v[u] = e < n4 ? __ldg(p4 + e) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                if (e - lane >= n4_pad) break;                             // warp-uniform tail
+                uint32_t nib = uint32_t(v[u].x >= a.thr) | (uint32_t(v[u].y >= a.thr) << 1) |
+                               (uint32_t(v[u].z >= a.thr) << 2) | (uint32_t(v[u].w >= a.thr) << 3);
+                nib = (e < n4 ? nib : 0u) << (4 * (lane & 7));
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
+                if ((lane & 7) == 0) hotbits[e >> 3] = nib;
+            }
+        }
+    } else {
+        for (int q = threadIdx.x; q < n_bw; q += blockDim.x) hotbits[q] = 0u;
+        __syncthreads();
+        for (int e = threadIdx.x; e < hw; e += blockDim.x)
+            if (__ldg(p + e) >= a.thr) atomicOr(hotbits + (e >> 5), 1u << (e & 31));
+    }
+    __syncthreads();
+
+    // ---- phase 2: strips of SW columns, two per lane ----
+    const int n_strips = (a.W + SW - 1) / SW;
+    for (int s = warp; s < n_strips; s += n_warps) {
+        const int x0 = s * SW;
+        int xc[2], j0[2], j1[2];
+        double tx[2], omtx[2];
+        bool in_grid[2], useful[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            xc[c] = x0 + 2 * (lane - 1) + c;
+            in_grid[c] = xc[c] >= 0 && xc[c] < a.W;
+            useful[c] = lane >= 1 && lane <= kWarp - 2 && in_grid[c];
+            const int xx = min(max(xc[c], 0), a.W - 1);
+            j0[c] = __ldg(a.cols.i0 + xx);
+            j1[c] = __ldg(a.cols.i1 + xx);
+            tx[c] = __ldg(a.cols.t + xx);
+            omtx[c] = __ldg(a.cols.omt + xx);
+        }
+        const int cj0 = __ldg(a.cols.i0 + x0);
+        const int cj1 = __ldg(a.cols.i1 + min(x0 + SW, a.W) - 1);
+        const bool edge = x0 - 2 < 0 || x0 + SW + 2 > a.W;      // strip has out-of-grid lanes
+        // hot source rows of this strip: any bit in [r*w + cj0, r*w + cj1]
+        for (int r0 = 0; r0 < h; r0 += 32) {
+            const int r = r0 + lane;
+            bool any = false;
+            if (r < h) {
+                const int bit0 = r * w + cj0, bit1 = r * w + cj1;
+                for (int q = bit0 >> 5; q <= (bit1 >> 5) && !any; ++q) {
+                    const int lo = max(bit0 - (q << 5), 0), hi = min(bit1 - (q << 5), 31);
+                    const uint32_t span = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+                    any = (hotbits[q] & span) != 0u;
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, any);
+            if (lane == 0) srcmask[r0 >> 5] = bal;
+        }
+        __syncwarp();
+
+        int run_lo = -1, run_hi = -2;
+        for (int q = 0; q <= n_rw; ++q) {
+            uint32_t m = q < n_rw ? srcmask[q] : 0u;
+            bool flush_final = q == n_rw;
+            while (m || flush_final) {
+                int lo = 0, hi = -1;
+                if (m) {
+                    const int r = (q << 5) + __ffs(m) - 1;
+                    m &= m - 1u;
+                    lo = max(__ldg(a.first_out + r) - HALF, 0);
+                    hi = min(__ldg(a.last_out + r) + HALF, H - 1);
+                    if (run_hi >= run_lo && lo <= run_hi + 1) {
+                        run_hi = max(run_hi, hi);
+                        continue;
+                    }
+                } else {
+                    flush_final = false;
+                }
+                if (run_hi >= run_lo) {
+                    if (edge)
+                        win3_run<HALF, true>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
+                    else
+                        win3_run<HALF, false>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
+                }
+                if (hi >= lo) { run_lo = lo; run_hi = hi; }
+                else { run_lo = -1; run_hi = -2; }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int HALF>
+__global__ void __launch_bounds__(128)
+k_nms_up_win2(const UpWinArgs a)
+{
+    static_assert(HALF >= 1 && HALF <= 2, "halo lanes carry at most two columns");
+    constexpr int SW = 2 * (kWarp - 2);      // useful columns per strip (lanes 1..30)
+    constexpr int WIN = 2 * HALF + 1;
+    extern __shared__ __align__(16) uint32_t sm[];
+    const int plane = blockIdx.x;
+    const int b = plane / a.K, k = plane - b * a.K;
+    const float *p = a.conf + ((size_t)b * a.C + k) * (size_t)a.h * a.w;
+    const int h = a.h, w = a.w, H = a.H;
+    const int n_cw = (w + 31) >> 5;
+    const int n_rw = (h + 31) >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_warps = blockDim.x >> 5;
+    // shared: row weights [H] | row source pair [H] | last row of the pair [H] |
+    //         hot bytes [h*w] | row masks [h][n_cw] | strip masks [warps][n_rw]
+    double2 *rt_w = reinterpret_cast<double2 *>(sm);
+    uint32_t *rt_idx = reinterpret_cast<uint32_t *>(rt_w + H);
+    int *rt_gend = reinterpret_cast<int *>(rt_idx + H);
+    uint8_t *hot = reinterpret_cast<uint8_t *>(rt_gend + H);
+    uint32_t *rowmask = reinterpret_cast<uint32_t *>(hot + ((h * w + 15) & ~15));
+    uint32_t *srcmask = rowmask + h * n_cw + warp * n_rw;
+
+    // ---- phase 1: stream the plane -> hot bytes; row table ----
+    const int hw = h * w;
+    if ((hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const float4 *p4 = reinterpret_cast<const float4 *>(p);
+        uchar4 *hot4 = reinterpret_cast<uchar4 *>(hot);
+        for (int e = threadIdx.x; e < (hw >> 2); e += blockDim.x) {
+            const float4 v = __ldg(p4 + e);
+            hot4[e] = make_uchar4(v.x >= a.thr, v.y >= a.thr, v.z >= a.thr, v.w >= a.thr);
+        }
+    } else {
+        for (int e = threadIdx.x; e < hw; e += blockDim.x) hot[e] = __ldg(p + e) >= a.thr;
+    }
+    for (int y = threadIdx.x; y < H; y += blockDim.x) {
+        int i0, i1;
+        double t, omt;
+        axis_at(y, a.ry, h, i0, i1, t, omt);
+        rt_w[y] = make_double2(t, omt);
+        rt_idx[y] = uint32_t(i0) | (uint32_t(i1) << 16);
+    }
+    __syncthreads();
+    for (int y = threadIdx.x; y < H; y += blockDim.x) {
+        int e = y;                               // source pairs are monotone in y
+        while (e + 1 < H && rt_idx[e + 1] == rt_idx[y]) ++e;
+        rt_gend[y] = e;
+    }
+    for (int r = warp; r < h; r += n_warps) {
+        for (int q = 0; q < n_cw; ++q) {
+            const int col = (q << 5) + lane;
+            const uint32_t m = __ballot_sync(0xffffffffu, col < w && hot[r * w + col]);
+            if (lane == 0) rowmask[r * n_cw + q] = m;
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 2: strips of SW columns, two per lane ----
+    const int n_strips = (a.W + SW - 1) / SW;
+    for (int s = warp; s < n_strips; s += n_warps) {
+        const int x0 = s * SW;
+        int xc[2], j0[2], j1[2];
+        double tx[2], omtx[2];
+        bool in_grid[2], useful[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            xc[c] = x0 + 2 * (lane - 1) + c;
+            in_grid[c] = xc[c] >= 0 && xc[c] < a.W;
+            useful[c] = lane >= 1 && lane <= kWarp - 2 && in_grid[c];
+            axis_at(min(max(xc[c], 0), a.W - 1), a.rx, w, j0[c], j1[c], tx[c], omtx[c]);
+        }
+        // source-column span of the strip's useful columns
+        const int last_x = min(x0 + SW, a.W) - 1;
+        int cj0, cj1, dmy;
+        double dt, domt;
+        axis_at(x0, a.rx, w, cj0, dmy, dt, domt);
+        axis_at(last_x, a.rx, w, dmy, cj1, dt, domt);
+        for (int r0 = 0; r0 < h; r0 += 32) {
+            const int r = r0 + lane;
+            bool any = false;
+            if (r < h) {
+                for (int q = cj0 >> 5; q <= (cj1 >> 5) && !any; ++q) {
+                    const uint32_t m = rowmask[r * n_cw + q];
+                    const int lo = max(cj0 - (q << 5), 0), hi = min(cj1 - (q << 5), 31);
+                    const uint32_t span = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+                    any = (m & span) != 0u;
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, any);
+            if (lane == 0) srcmask[r0 >> 5] = bal;
+        }
+        __syncwarp();
+
+        int run_lo = -1, run_hi = -2;
+        for (int q = 0; q <= n_rw; ++q) {
+            uint32_t m = q < n_rw ? srcmask[q] : 0u;
+            bool flush_final = q == n_rw;
+            while (m || flush_final) {
+                int lo = 0, hi = -1;
+                if (m) {
+                    const int r = (q << 5) + __ffs(m) - 1;
+                    m &= m - 1u;
+                    lo = max(__ldg(a.first_out + r) - HALF, 0);
+                    hi = min(__ldg(a.last_out + r) + HALF, H - 1);
+                    if (run_hi >= run_lo && lo <= run_hi + 1) {
+                        run_hi = max(run_hi, hi);
+                        continue;
+                    }
+                } else {
+                    flush_final = false;
+                }
+                if (run_hi >= run_lo) {
+                    // window per column: 0 = oldest row, HALF = centre
+                    float full[2][WIN], cv[2][WIN], lm[2][WIN], rm[2][WIN];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int t = 0; t < WIN; ++t) full[c][t] = cv[c][t] = lm[c][t] = rm[c][t] = -INFINITY;
+                    const int test_lo = run_lo == 0 ? 0 : run_lo + HALF;
+                    const int test_hi = run_hi == H - 1 ? H - 1 : run_hi - HALF;
+                    const int last_eval = run_hi == H - 1 ? run_hi + HALF : run_hi;
+                    double hA[2] = {0.0, 0.0}, hB[2] = {0.0, 0.0};
+                    int y = run_lo;
+                    while (y <= last_eval) {
+                        int yend;
+                        if (y < H) {
+                            // refresh the two source-row interpolants (uniform branch)
+                            const uint32_t idx = rt_idx[y];
+                            const int i0 = int(idx & 0xffffu), i1 = int(idx >> 16);
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                hA[c] = dadd(dmul((double)__ldg(p + i0 * w + j0[c]), omtx[c]),
+                                             dmul((double)__ldg(p + i0 * w + j1[c]), tx[c]));
+                                hB[c] = dadd(dmul((double)__ldg(p + i1 * w + j0[c]), omtx[c]),
+                                             dmul((double)__ldg(p + i1 * w + j1[c]), tx[c]));
+                            }
+                            yend = min(rt_gend[y], last_eval);
+                        } else {
+                            yend = last_eval;       // virtual -inf rows below the grid
+                        }
+                        for (; y <= yend; ++y) {
+                            float v[2];
+                            if (y < H) {
+                                const double2 wy = rt_w[y];
+#pragma unroll
+                                for (int c = 0; c < 2; ++c) {
+                                    const float val = __double2float_rn(dadd(dmul(hA[c], wy.y), dmul(hB[c], wy.x)));
+                                    v[c] = in_grid[c] ? val : -INFINITY;
+                                }
+                            } else {
+                                v[0] = v[1] = -INFINITY;
+                            }
+                            // neighbour columns: x0c-1 = lane-1's col 1, x1c+1 = lane+1's col 0,
+                            // x0c-2 = lane-1's col 0, x1c+2 = lane+1's col 1
+                            const float l1 = __shfl_up_sync(0xffffffffu, v[1], 1);
+                            const float r1 = __shfl_down_sync(0xffffffffu, v[0], 1);
+                            float lmax0, rmax0, lmax1, rmax1;
+                            if (HALF == 1) {
+                                lmax0 = l1;    rmax0 = v[1];
+                                lmax1 = v[0];  rmax1 = r1;
+                            } else {
+                                const float l2 = __shfl_up_sync(0xffffffffu, v[0], 1);
+                                const float r2 = __shfl_down_sync(0xffffffffu, v[1], 1);
+                                lmax0 = max_nan(l1, l2);       rmax0 = max_nan(v[1], r1);
+                                lmax1 = max_nan(v[0], l1);     rmax1 = max_nan(r1, r2);
+                            }
+                            const float lmx[2] = {lmax0, lmax1}, rmx[2] = {rmax0, rmax1};
+                            const int yc = y - HALF;
+                            const bool row_ok = yc >= test_lo && yc <= test_hi;
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+#pragma unroll
+                                for (int t = 0; t < WIN - 1; ++t) {
+                                    full[c][t] = full[c][t + 1]; cv[c][t] = cv[c][t + 1];
+                                    lm[c][t] = lm[c][t + 1]; rm[c][t] = rm[c][t + 1];
+                                }
+                                full[c][WIN - 1] = max_nan(max_nan(lmx[c], v[c]), rmx[c]);
+                                cv[c][WIN - 1] = v[c]; lm[c][WIN - 1] = lmx[c]; rm[c][WIN - 1] = rmx[c];
+                                float earlier = lm[c][HALF], later = rm[c][HALF];
+#pragma unroll
+                                for (int t = 0; t < HALF; ++t) {
+                                    earlier = max_nan(earlier, full[c][t]);
+                                    later = max_nan(later, full[c][HALF + 1 + t]);
+                                }
+                                const float cc = cv[c][HALF];
+                                if (useful[c] && row_ok && cc >= a.thr && cc > earlier && cc >= later)
+                                    emit_peak(a.counts, a.peaks, plane, a.cap, cc, yc, xc[c]);
+                            }
+                        }
+                    }
+                }
+                if (hi >= lo) { run_lo = lo; run_hi = hi; }
+                else { run_lo = -1; run_hi = -2; }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <int HALF>
 __global__ void __launch_bounds__(128)
 k_nms_up_win(const UpWinArgs a)
@@ -417,7 +861,7 @@ k_nms_up_win(const UpWinArgs a)
 size_t nms_up_win_smem(int h, int w, int H, int threads)
 {
     const int n_cw = (w + 31) >> 5, n_rw = (h + 31) >> 5;
-    return (size_t)H * (16 + 4) + (size_t)((h * w + 15) & ~15) + (size_t)h * n_cw * 4 +
+    return (size_t)H * (16 + 4 + 4) + (size_t)((h * w + 15) & ~15) + (size_t)h * n_cw * 4 +
            (size_t)(threads / 32) * n_rw * 4 + 16;
 }
 
@@ -426,26 +870,43 @@ cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s)
     const long long grid = (long long)B * a.K;
     if (grid == 0) return cudaSuccess;
     const size_t smem = nms_up_win_smem(a.h, a.w, a.H, 128);
-    if (a.half == 1) k_nms_up_win<1><<<(unsigned)grid, 128, smem, s>>>(a);
-    else if (a.half == 2) k_nms_up_win<2><<<(unsigned)grid, 128, smem, s>>>(a);
-    else return cudaErrorInvalidValue;
+    if (a.variant == 3) {
+        const size_t smem3 = (size_t)(((a.h * a.w + 127) & ~127) >> 5) * 4 + (size_t)4 * ((a.h + 31) >> 5) * 4;
+        if (a.half == 1) k_nms_up_win3<1><<<(unsigned)grid, 128, smem3, s>>>(a);
+        else if (a.half == 2) k_nms_up_win3<2><<<(unsigned)grid, 128, smem3, s>>>(a);
+        else return cudaErrorInvalidValue;
+    } else if (a.variant == 1) {
+        if (a.half == 1) k_nms_up_win<1><<<(unsigned)grid, 128, smem, s>>>(a);
+        else if (a.half == 2) k_nms_up_win<2><<<(unsigned)grid, 128, smem, s>>>(a);
+        else return cudaErrorInvalidValue;
+    } else {
+        if (a.half == 1) k_nms_up_win2<1><<<(unsigned)grid, 128, smem, s>>>(a);
+        else if (a.half == 2) k_nms_up_win2<2><<<(unsigned)grid, 128, smem, s>>>(a);
+        else return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
+}
+
+template <typename F>
+static cudaError_t raise_smem_limit(F *fn, int max_smem)
+{
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                max_smem - (int)fa.sharedSizeBytes);
 }
 
 cudaError_t configure_nms_kernels(int max_smem)
 {
     {
-        cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, k_nms_up_win<1>);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_nms_up_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 max_smem - (int)fa.sharedSizeBytes);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncGetAttributes(&fa, k_nms_up_win<2>);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_nms_up_win<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 max_smem - (int)fa.sharedSizeBytes);
-        if (e != cudaSuccess) return e;
+        cudaError_t e;
+        if ((e = raise_smem_limit(k_nms_up_win<1>, max_smem)) != cudaSuccess) return e;
+        if ((e = raise_smem_limit(k_nms_up_win<2>, max_smem)) != cudaSuccess) return e;
+        if ((e = raise_smem_limit(k_nms_up_win2<1>, max_smem)) != cudaSuccess) return e;
+        if ((e = raise_smem_limit(k_nms_up_win2<2>, max_smem)) != cudaSuccess) return e;
+        if ((e = raise_smem_limit(k_nms_up_win3<1>, max_smem)) != cudaSuccess) return e;
+        if ((e = raise_smem_limit(k_nms_up_win3<2>, max_smem)) != cudaSuccess) return e;
     }
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k_nms_up);
