@@ -48,6 +48,24 @@ BYTES_NMS_FULL = K_PARTS * PLANE * 64 * 4           # 17,381,376: read full-res 
 BYTES_PARSE = PAF_FRAME_BYTES                       # PAF planes the line integral samples
 
 
+def ncu_traffic(kernel: str, frames_per_launch: float):
+    """dram read+write bytes per launch of `kernel` from the committed ncu
+    capture (profiles/<round>_traffic.json), scaled to this launch size."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except Exception:
+            continue
+        for name, val in d.items():
+            if name != "frames_per_launch" and name.split("<")[0].startswith(kernel):
+                best = (val / d["frames_per_launch"]) * frames_per_launch
+    return best
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -247,15 +265,16 @@ def run_b200(args, rank, world, local_rank):
     for _ in range(max(1, args.warmup)):
         r = eng.parse_arrays(pin_conf.array, pin_paf.array, STRIDE, params)
     barrier()
+    e2e_steps = min(args.steps, args.e2e_steps)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):          # synchronous API: H2D + kernels + D2H of humans
         r = eng.parse_arrays(pin_conf.array, pin_paf.array, STRIDE, params)
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
-    e2e_value = world * E * args.steps / e2e_s
+    e2e_value = world * E * e2e_steps / e2e_s
     h2d = E * (K_PARTS * PLANE * 4 + PAF_FRAME_BYTES)     # background plane not shipped
     d2h = E * 8 + 32 + r.total_humans * (8 + 4 + K_PARTS * (8 + 8 + 4 + 4))
 
@@ -304,11 +323,16 @@ def run_b200(args, rank, world, local_rank):
     roof = None
     if dominant:
         d = stages[dominant]
+        traffic = args.traffic if args.traffic is not None else ncu_traffic(dominant, d["frames_per_launch"])
         roof = {"kernel": dominant, "bound": "hbm", "achieved": d["achieved_gbs"],
                 "peak": peak_gbs, "unit": "GB/s",
                 "frac": (d["achieved_gbs"] / peak_gbs) if d["achieved_gbs"] else None,
-                "traffic": args.traffic, "peak_kind": peak_kind,
-                "bytes_per_frame": per_frame_bytes.get(dominant, 0)}
+                "traffic": traffic, "peak_kind": peak_kind,
+                "bytes_per_launch": d["bytes_per_launch"],
+                "ms_per_launch": d["ms_per_launch"],
+                "bytes_per_frame": per_frame_bytes.get(dominant, 0),
+                "note": "algorithmic bytes = the low-res part maps the fused upsample+NMS must read "
+                        "(SURVEY §8(d) 'fused U+N compulsory'); traffic = ncu dram read+write per launch"}
 
     # ---- CPU baseline (rank 0, N == 1) ----
     cpu = None
@@ -334,7 +358,8 @@ def run_b200(args, rank, world, local_rank):
                        "l2": f"inputs {F * (CONF_FRAME_BYTES + PAF_FRAME_BYTES) / 1e9:.2f} GB/GPU > L2; no flush",
                        "humans_per_step": humans_per_step},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "frames_per_step": E,
+                    "d2h_bytes_per_step": d2h, "frames_per_step": E, "steps": e2e_steps,
+                    "h2d_gbs": h2d * e2e_steps * world / e2e_s / 1e9,
                     "path": "pf_parse_host (pinned host maps -> H2D -> kernels -> D2H humans)"},
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -349,7 +374,8 @@ def run_b200(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--frames", type=int, default=8192, help="frames per GPU per step")
