@@ -426,6 +426,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.first_out = rows->d_first; a.last_out = rows->d_last;
         a.variant = ctx->win_variant;
         a.rows = rows->dev(); a.cols = cols->dev(); a.gend = rows->d_gend; a.tw = rows->d_tw;
+        a.stage = 0;   // measured: staging the plane in smem is slower than L1-cached reads
         KernelTimer kt(ctx, kNmsUpWin);
         CU(launch_nms_up_win(a, n, s));
     } else if (!blur && half <= kMaxFusedHalf && !ctx->materialise) {
@@ -485,7 +486,11 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     ParseArgs a{};
     a.topo = ctx->topo;
     a.paf = paf; a.h = h; a.w = w; a.up = up;
-    if (up > 1) { a.rows = rows->dev(); a.cols = cols->dev(); }
+    if (up > 1) {
+        a.rows = rows->dev(); a.cols = cols->dev();
+        a.ry = (double)h / (double)H;
+        a.rx = (double)w / (double)W;
+    }
     a.stride_eff = stride / up;
     a.n_samples = p->n_samples;
     a.dot_thr = p->sample_dot_threshold;
@@ -655,9 +660,9 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
     // a replay of the call) when a frame needs more; explicit caps are fixed
     int auto_caps = 0;
     if (c.max_peaks_per_part <= 0) { c.max_peaks_per_part = 128; auto_caps |= 1 << kCapPart; }
-    if (c.max_peaks_per_frame <= 0) { c.max_peaks_per_frame = 1024; auto_caps |= 1 << kCapFrame; }
+    if (c.max_peaks_per_frame <= 0) { c.max_peaks_per_frame = 512; auto_caps |= 1 << kCapFrame; }
     if (c.max_candidates <= 0) { c.max_candidates = 4096; auto_caps |= 1 << kCapCands; }
-    if (c.max_humans_per_frame <= 0) { c.max_humans_per_frame = 256; auto_caps |= 1 << kCapHumans; }
+    if (c.max_humans_per_frame <= 0) { c.max_humans_per_frame = 128; auto_caps |= 1 << kCapHumans; }
     if (c.max_humans_total <= 0) auto_caps |= 1 << kCapPool;
     if (c.chunk_frames <= 0) c.chunk_frames = 8192;
     // bitonic sort over the candidate store needs a power of two

@@ -48,6 +48,21 @@ __device__ __forceinline__ float bilerp(double a, double b, double c, double d,
     return __double2float_rn(dadd(dmul(top, omty), dmul(bot, ty)));
 }
 
+// operators.py:87-96 for one output coordinate, evaluated in registers with
+// the same fp64 op order as the host tables: s = (o + 0.5) * ratio - 0.5,
+// f = floor(s), t = s - f, 1 - t, indices clipped to [0, n_in - 1].
+__device__ __forceinline__ void axis_coord(int o, double ratio, int n_in, int &i0, int &i1, double &t,
+                                           double &omt)
+{
+    const double s = dadd(dmul(dadd((double)o, 0.5), ratio), -0.5);
+    const double f = floor(s);
+    const int fi = (int)f;
+    t = __dsub_rn(s, f);
+    omt = __dsub_rn(1.0, t);
+    i0 = min(max(fi, 0), n_in - 1);
+    i1 = min(max(fi + 1, 0), n_in - 1);
+}
+
 // Peak record produced by the NMS kernels: fp32 score bits + packed cell.
 __device__ __forceinline__ uint2 pack_peak(float v, int i, int j)
 {

@@ -36,6 +36,7 @@ struct UpWinArgs {
     AxisTab rows, cols;  // host-built operators.py:86-96 tables (variant 3)
     const int32_t *gend; // [H]: last output row sharing row y's source pair (variant 3)
     const double2 *tw;   // [H]: (t, 1 - t) per output row, packed for one 16-byte load
+    int stage;           // 1: low-res plane staged in shared memory (variant 3)
 };
 size_t nms_up_win_smem(int h, int w, int H, int threads);
 cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s);
@@ -75,6 +76,7 @@ struct ParseArgs {
     int *dbg_conn_i;
     double *dbg_conn_d;
     void *cand_spill;    // [frames][cap_cands - kCandSmem] candidate records (crowded frames)
+    double ry, rx;       // h / H, w / W: operators.py:88-89 ratios (up > 1)
 };
 constexpr int kCandSmem = 256;       // gated candidates kept in shared memory per frame
 constexpr int kParseThreads = 128;   // k_parse_frames CTA size

@@ -310,6 +310,87 @@ __device__ __forceinline__ void win3_row(const float v0, const float v1, const b
     }
 }
 
+// 3x3 window, two columns per lane (x0 = 2*(lane-1)+c): minimal carried state.
+// After row y-1:  c0, c1 = centre values (row y-1) of the lane's columns,
+// cl = value at x0-1 (lane-1's col 1), cr = value at x1+1 (lane+1's col 0),
+// f0, f1 = max over the 3 columns around x0 / x1 of row y-2.
+struct Win1 {
+    float c0, c1, cl, cr, f0, f1;
+};
+
+__device__ __forceinline__ void win1_init(Win1 &s)
+{
+    s.c0 = s.c1 = s.cl = s.cr = s.f0 = s.f1 = -INFINITY;
+}
+
+// Consume row y (values n0, n1); test the centre row y-1 (paf.py:87-99).
+__device__ __forceinline__ void win1_row(Win1 &s, float n0, float n1, float thr, bool use0, bool use1,
+                                         const UpWinArgs &a, int plane, int yc, int x0)
+{
+    const float nl = __shfl_up_sync(0xffffffffu, n1, 1);
+    const float nr = __shfl_down_sync(0xffffffffu, n0, 1);
+    const float fn0 = max_nan(max_nan(nl, n0), n1);      // row y maxima around x0, x1
+    const float fn1 = max_nan(max_nan(n0, n1), nr);
+    // earlier neighbours: row y-2 (3 cells) + left cell of row y-1; later: right cell + row y
+    const bool p0 = use0 && s.c0 >= thr && s.c0 > max_nan(s.f0, s.cl) && s.c0 >= max_nan(s.c1, fn0);
+    const bool p1 = use1 && s.c1 >= thr && s.c1 > max_nan(s.f1, s.c0) && s.c1 >= max_nan(s.cr, fn1);
+    if (__any_sync(0xffffffffu, p0 || p1)) {             // rare
+        if (p0) emit_peak(a.counts, a.peaks, plane, a.cap, s.c0, yc, x0);
+        if (p1) emit_peak(a.counts, a.peaks, plane, a.cap, s.c1, yc, x0 + 1);
+    }
+    s.f0 = max_nan(max_nan(s.cl, s.c0), s.c1);
+    s.f1 = max_nan(max_nan(s.c0, s.c1), s.cr);
+    s.c0 = n0; s.c1 = n1; s.cl = nl; s.cr = nr;
+}
+
+// Low-res source values: shared-memory copy of the plane (SMEM) or L1-cached global.
+template <bool SMEM>
+__device__ __forceinline__ float ldsrc(const float *src, int idx)
+{
+    return SMEM ? src[idx] : __ldg(src + idx);
+}
+
+template <bool EDGE, bool SMEM>
+__device__ __forceinline__ void win1_run(const UpWinArgs &a, const float *__restrict__ p, int plane,
+                                         int run_lo, int run_hi, const int (&xc)[2], const int (&j0)[2],
+                                         const int (&j1)[2], const double (&tx)[2], const double (&omtx)[2],
+                                         const bool (&in_grid)[2], const bool (&useful)[2])
+{
+    const int w = a.w, H = a.H;
+    const float thr = a.thr;
+    Win1 s;
+    win1_init(s);
+    double hA0 = 0.0, hA1 = 0.0, hB0 = 0.0, hB1 = 0.0;
+    int ci1 = -1;
+    int y = run_lo;
+    while (y <= run_hi) {
+        const int i0 = __ldg(a.rows.i0 + y), i1 = __ldg(a.rows.i1 + y);
+        if (i0 == ci1) {                     // warp-uniform: last pair's upper row
+            hA0 = hB0;
+            hA1 = hB1;
+        } else {
+            hA0 = dadd(dmul((double)ldsrc<SMEM>(p, i0 * w + j0[0]), omtx[0]), dmul((double)ldsrc<SMEM>(p, i0 * w + j1[0]), tx[0]));
+            hA1 = dadd(dmul((double)ldsrc<SMEM>(p, i0 * w + j0[1]), omtx[1]), dmul((double)ldsrc<SMEM>(p, i0 * w + j1[1]), tx[1]));
+        }
+        hB0 = dadd(dmul((double)ldsrc<SMEM>(p, i1 * w + j0[0]), omtx[0]), dmul((double)ldsrc<SMEM>(p, i1 * w + j1[0]), tx[0]));
+        hB1 = dadd(dmul((double)ldsrc<SMEM>(p, i1 * w + j0[1]), omtx[1]), dmul((double)ldsrc<SMEM>(p, i1 * w + j1[1]), tx[1]));
+        ci1 = i1;
+        const int yend = min(__ldg(a.gend + y), run_hi);
+        for (; y <= yend; ++y) {
+            const double2 wt = __ldg(a.tw + y);
+            float v0 = __double2float_rn(dadd(dmul(hA0, wt.y), dmul(hB0, wt.x)));
+            float v1 = __double2float_rn(dadd(dmul(hA1, wt.y), dmul(hB1, wt.x)));
+            if (EDGE) {
+                v0 = in_grid[0] ? v0 : -INFINITY;
+                v1 = in_grid[1] ? v1 : -INFINITY;
+            }
+            win1_row(s, v0, v1, thr, useful[0], useful[1], a, plane, y - 1, xc[0]);
+        }
+    }
+    if (run_hi == H - 1)                     // -inf padding row below the grid
+        win1_row(s, -INFINITY, -INFINITY, thr, useful[0], useful[1], a, plane, H - 1, xc[0]);
+}
+
 // Rows [y, run_hi] of one run for one strip; EDGE strips mask out-of-grid
 // columns to -inf (the reference's padding), interior strips skip the select.
 template <int HALF, bool EDGE>
@@ -382,6 +463,7 @@ k_nms_up_win3(const UpWinArgs a)
     const int n_warps = blockDim.x >> 5;
     uint32_t *hotbits = sm;                                  // [n_bw]
     uint32_t *srcmask = sm + n_bw + warp * n_rw;             // per warp [n_rw]
+    float *plane_s = reinterpret_cast<float *>(sm + n_bw + 4 * n_rw);   // [h*w] if a.stage (16B aligned)
 
     // ---- phase 1: stream the plane -> flat bitmap of cells >= thr ----
     // all 16-byte loads of a thread are issued before any is consumed
@@ -395,6 +477,13 @@ k_nms_up_win3(const UpWinArgs a)
             for (int u = 0; u < U; ++u) {
                 const int e = e0 + u * blockDim.x;
                 v[u] = e < n4 ? __ldg(p4 + e) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            }
+            if (a.stage) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * blockDim.x;
+                    if (e < n4) reinterpret_cast<float4 *>(plane_s)[e] = v[u];
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -412,8 +501,11 @@ k_nms_up_win3(const UpWinArgs a)
     } else {
         for (int q = threadIdx.x; q < n_bw; q += blockDim.x) hotbits[q] = 0u;
         __syncthreads();
-        for (int e = threadIdx.x; e < hw; e += blockDim.x)
-            if (__ldg(p + e) >= a.thr) atomicOr(hotbits + (e >> 5), 1u << (e & 31));
+        for (int e = threadIdx.x; e < hw; e += blockDim.x) {
+            const float v = __ldg(p + e);
+            if (a.stage) plane_s[e] = v;
+            if (v >= a.thr) atomicOr(hotbits + (e >> 5), 1u << (e & 31));
+        }
     }
     __syncthreads();
 
@@ -474,10 +566,22 @@ k_nms_up_win3(const UpWinArgs a)
                     flush_final = false;
                 }
                 if (run_hi >= run_lo) {
-                    if (edge)
+                    if (HALF == 1) {
+                        if (a.stage) {
+                            if (edge)
+                                win1_run<true, true>(a, plane_s, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
+                            else
+                                win1_run<false, true>(a, plane_s, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
+                        } else if (edge) {
+                            win1_run<true, false>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
+                        } else {
+                            win1_run<false, false>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
+                        }
+                    } else if (edge) {
                         win3_run<HALF, true>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
-                    else
+                    } else {
                         win3_run<HALF, false>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
+                    }
                 }
                 if (hi >= lo) { run_lo = lo; run_hi = hi; }
                 else { run_lo = -1; run_hi = -2; }
@@ -871,7 +975,9 @@ cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s)
     if (grid == 0) return cudaSuccess;
     const size_t smem = nms_up_win_smem(a.h, a.w, a.H, 128);
     if (a.variant == 3) {
-        const size_t smem3 = (size_t)(((a.h * a.w + 127) & ~127) >> 5) * 4 + (size_t)4 * ((a.h + 31) >> 5) * 4;
+        size_t smem3 = (size_t)(((a.h * a.w + 127) & ~127) >> 5) * 4 + (size_t)4 * ((a.h + 31) >> 5) * 4;
+        smem3 = (smem3 + 15) & ~size_t(15);
+        if (a.stage) smem3 += (size_t)a.h * a.w * sizeof(float);
         if (a.half == 1) k_nms_up_win3<1><<<(unsigned)grid, 128, smem3, s>>>(a);
         else if (a.half == 2) k_nms_up_win3<2><<<(unsigned)grid, 128, smem3, s>>>(a);
         else return cudaErrorInvalidValue;

@@ -60,12 +60,14 @@ __device__ __forceinline__ double sample_paf(const ParseArgs &a, const float *__
                                              int ci, int cj)
 {
     if (a.up == 1) return (double)__ldg(ch + (size_t)ci * a.w + cj);
-    const int i0 = __ldg(a.rows.i0 + ci), i1 = __ldg(a.rows.i1 + ci);
-    const int j0 = __ldg(a.cols.i0 + cj), j1 = __ldg(a.cols.i1 + cj);
+    // axis parameters recomputed in registers (no dependent table loads)
+    int i0, i1, j0, j1;
+    double ty, omty, tx, omtx;
+    axis_coord(ci, a.ry, a.h, i0, i1, ty, omty);
+    axis_coord(cj, a.rx, a.w, j0, j1, tx, omtx);
     const float v = bilerp(__ldg(ch + (size_t)i0 * a.w + j0), __ldg(ch + (size_t)i0 * a.w + j1),
                            __ldg(ch + (size_t)i1 * a.w + j0), __ldg(ch + (size_t)i1 * a.w + j1),
-                           __ldg(a.cols.t + cj), __ldg(a.cols.omt + cj),
-                           __ldg(a.rows.t + ci), __ldg(a.rows.omt + ci));
+                           tx, omtx, ty, omty);
     return (double)v;
 }
 
