@@ -205,8 +205,11 @@ def run_b200(args, rank, world, local_rank):
     import paper_2108_11826_b200 as pf
     from paper_2108_11826_b200 import _native
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one GPU per rank; ranks share devices only in the plumbing test (more
+    # ranks than GPUs, PF_BENCH_BACKEND=gloo)
+    gpu = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     topo, conf_h, paf_h = make_inputs(args.distinct, seed=5 + 1000 * rank)
     params = pf.ParserParams(upsample=UP if args.mode == "U" else 1)
     F = args.frames
@@ -214,7 +217,7 @@ def run_b200(args, rank, world, local_rank):
     idx = torch.arange(F) % conf_h.shape[0]
     conf_d = torch.from_numpy(conf_h).to(dev)[idx.to(dev)].contiguous()
     paf_d = torch.from_numpy(paf_h).to(dev)[idx.to(dev)].contiguous()
-    eng = pf.PafParser(topo, device=local_rank)
+    eng = pf.PafParser(topo, device=gpu)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -231,7 +234,7 @@ def run_b200(args, rank, world, local_rank):
     # ---- timed region: device-resident maps ----
     eng.set_timing(True)
     eng.kernel_times(reset=True)
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(gpu)
     clocks.start()
     time.sleep(0.3)  # let the sampler attach
     barrier()
@@ -249,10 +252,9 @@ def run_b200(args, rank, world, local_rank):
     elapsed_ms = ev0.elapsed_time(ev1)
     ktimes = eng.kernel_times(reset=True)
     eng.set_timing(False)
-    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t_max.item())
+    from paper_2108_11826_b200.sharding import max_over_ranks
+
+    elapsed_ms = max_over_ranks(elapsed_ms)      # the job's time is its slowest rank's
     value = world * F * args.steps / (elapsed_ms / 1e3)
 
     # ---- e2e: through the C ABI from pinned host memory ----
@@ -270,10 +272,7 @@ def run_b200(args, rank, world, local_rank):
     for _ in range(e2e_steps):          # synchronous API: H2D + kernels + D2H of humans
         r = eng.parse_arrays(pin_conf.array, pin_paf.array, STRIDE, params)
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te.item())
+    e2e_s = max_over_ranks(e2e_s)
     e2e_value = world * E * e2e_steps / e2e_s
     h2d = E * (K_PARTS * PLANE * 4 + PAF_FRAME_BYTES)     # background plane not shipped
     d2h = E * 8 + 32 + r.total_humans * (8 + 4 + K_PARTS * (8 + 8 + 4 + 4))
@@ -338,7 +337,7 @@ def run_b200(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        frames = max(64, 4 * cores)
+        frames = max(256, 16 * cores)      # ~15-60 s of CPU work, a few s wall
         t = cpu_oracle_run(conf_h, paf_h, topo, params, frames, cores)
         cpu = {"value": frames / t, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{frames} frames of the same stream, Mode U oracle (C restatement of "
@@ -398,11 +397,11 @@ def main():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "gloo" if args.impl == "reference" else "nccl"
+        backend = "gloo" if args.impl == "reference" else os.environ.get("PF_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             import torch
 
-            torch.cuda.set_device(local_rank)
+            torch.cuda.set_device(local_rank % torch.cuda.device_count())
         dist.init_process_group(backend=backend)
     try:
         if args.impl == "reference":
