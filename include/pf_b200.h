@@ -159,12 +159,12 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_TIMING 2
 #define PF_OPT_MATERIALISE 3
 #define PF_OPT_GENERIC_FUSED 4   /* use the shared-memory tile kernel for Mode U */
-#define PF_OPT_WIN_VARIANT 5     /* register-window kernel: 2 (two columns/lane) or 1 */
+#define PF_OPT_WIN_VARIANT 5     /* Mode U 3x3 kernel: 4 corner-pruned (default), 3/2/1 strip kernels */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch
  * counts accumulated since the last reset; ids index pf_kernel_name(). */
-#define PF_N_KERNELS 8
+#define PF_N_KERNELS 9
 const char *pf_kernel_name(int id);
 int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset);
 int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,

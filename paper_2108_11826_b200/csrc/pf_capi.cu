@@ -9,6 +9,7 @@
 // k_parse_frames resets the per-slab peak counters it consumed, so the
 // steady state needs no memset between chunks; one 32-byte memset clears
 // the status/pool counter per call.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -30,6 +31,13 @@ struct AxisCache {
     std::vector<double> t, omt;
     std::vector<int32_t> first_out, last_out;   // inverse map: outputs reading input row r
     std::vector<int32_t> gend;                  // last output row with the same source pair
+    std::vector<int4> bands;                    // (first, last, src0, src1) per band
+    std::vector<double> band_dt;                // min t step inside each band (inf if 1 wide)
+    int max_band = 0;
+    std::vector<int2> src_band;                 // per source index: [lo, hi] bands reading it
+    int4 *d_bands = nullptr;
+    double *d_band_dt = nullptr;
+    int2 *d_src_band = nullptr;
     int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr, *d_gend = nullptr;
     double2 *d_tw = nullptr;
     double *d_t = nullptr, *d_omt = nullptr;
@@ -57,6 +65,24 @@ void fill_axis(AxisCache &a, int in_n, int out_n)
     a.gend.resize(out_n);
     for (int o = out_n - 1; o >= 0; --o)
         a.gend[o] = (o + 1 < out_n && a.i0[o + 1] == a.i0[o] && a.i1[o + 1] == a.i1[o]) ? a.gend[o + 1] : o;
+    a.bands.clear();
+    a.band_dt.clear();
+    a.max_band = 0;
+    for (int o = 0; o < out_n; o = a.gend[o] + 1) {
+        const int e = a.gend[o];
+        a.bands.push_back(make_int4(o, e, a.i0[o], a.i1[o]));
+        double dt = 1e300;
+        for (int u = o; u < e; ++u) dt = std::min(dt, a.t[u + 1] - a.t[u]);
+        a.band_dt.push_back(dt);
+        a.max_band = std::max(a.max_band, e - o + 1);
+    }
+    a.src_band.assign(in_n, make_int2(0x3fffffff, -1));
+    for (int b = 0; b < (int)a.bands.size(); ++b) {
+        for (int r : {a.bands[b].z, a.bands[b].w}) {
+            a.src_band[r].x = std::min(a.src_band[r].x, b);
+            a.src_band[r].y = std::max(a.src_band[r].y, b);
+        }
+    }
     a.first_out.assign(in_n, 0x3fffffff);
     a.last_out.assign(in_n, -1);
     for (int o = 0; o < out_n; ++o) {
@@ -140,7 +166,7 @@ struct pf_ctx {
     int timing = 0;
     int materialise = 0;
     int generic_fused = 0;
-    int win_variant = 3;
+    int win_variant = 4;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double kernel_ms[PF_N_KERNELS] = {0};
@@ -186,10 +212,10 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
     } while (0)
 
 enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
-                kNmsUpWin };
+                kNmsUpWin, kNmsUpCorner };
 const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
                                           "k_resize_planes", "k_blur_rows", "k_blur_cols",
-                                          "k_preprocess", "k_nms_up_win"};
+                                          "k_preprocess", "k_nms_up_win", "k_nms_up_corner"};
 
 cudaEvent_t take_event(pf_ctx *ctx)
 {
@@ -255,6 +281,12 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
             CU(dev_alloc(&a.d_tw, out_n));
             CU(cudaMemcpy(a.d_tw, tw.data(), out_n * sizeof(double2), cudaMemcpyHostToDevice));
         }
+        CU(dev_alloc(&a.d_bands, a.bands.size()));
+        CU(cudaMemcpy(a.d_bands, a.bands.data(), a.bands.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        CU(dev_alloc(&a.d_src_band, a.src_band.size()));
+        CU(cudaMemcpy(a.d_src_band, a.src_band.data(), a.src_band.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        CU(dev_alloc(&a.d_band_dt, a.band_dt.size()));
+        CU(cudaMemcpy(a.d_band_dt, a.band_dt.data(), a.band_dt.size() * sizeof(double), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_gend, out_n));
         CU(cudaMemcpy(a.d_gend, a.gend.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_first, in_n));
@@ -415,6 +447,22 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         KernelTimer kt(ctx, kNmsPlane);
         CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
+    } else if (!blur && half == 1 && !ctx->materialise && !ctx->generic_fused && ctx->win_variant == 4 &&
+               rows->max_band + 2 <= 64 && cols->max_band + 2 <= 64 &&
+               nms_up_corner_smem(h, w, (int)rows->bands.size(), (int)cols->bands.size(), rows->max_band + 2,
+                                  cols->max_band + 2) <= 96 * 1024) {
+        UpCornerArgs a{};
+        a.conf = conf; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
+        a.thr = thr; a.cap = ctx->caps.max_peaks_per_part;
+        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+        a.rows = rows->dev(); a.cols = cols->dev();
+        a.rband = rows->d_bands; a.cband = cols->d_bands;
+        a.rdt = rows->d_band_dt; a.cdt = cols->d_band_dt;
+        a.nbr = (int)rows->bands.size(); a.nbc = (int)cols->bands.size();
+        a.scr_rows = rows->max_band + 2; a.scr_cols = cols->max_band + 2;
+        a.src_rband = rows->d_src_band; a.src_cband = cols->d_src_band;
+        KernelTimer kt(ctx, kNmsUpCorner);
+        CU(launch_nms_up_corner(a, n, s));
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
                nms_up_win_smem(h, w, H, 128) <= 96 * 1024) {
         UpWinArgs a{};
@@ -711,6 +759,7 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
     const int max_smem = prop.sharedMemPerBlockOptin;
     ctx->max_smem = max_smem;
     if (cu(configure_nms_kernels(max_smem), "configure k_nms_up") ||
+        cu(configure_corner_kernels(max_smem), "configure k_nms_up_corner") ||
         cu(configure_parse_kernels(max_smem), "configure k_parse_frames"))
         return bail(PF_ERR_CUDA);
     const size_t need = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
@@ -740,6 +789,7 @@ void pf_destroy(pf_ctx *ctx)
         cudaFree(kv.second.d_i0); cudaFree(kv.second.d_i1);
         cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
         cudaFree(kv.second.d_first); cudaFree(kv.second.d_last); cudaFree(kv.second.d_gend); cudaFree(kv.second.d_tw);
+        cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt); cudaFree(kv.second.d_src_band);
     }
     for (auto &p : ctx->pending) { ctx->ev_pool.push_back(p.second.first); ctx->ev_pool.push_back(p.second.second); }
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -824,7 +874,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_TIMING: ctx->timing = value ? 1 : 0; return PF_OK;
     case PF_OPT_MATERIALISE: ctx->materialise = value ? 1 : 0; return PF_OK;
     case PF_OPT_GENERIC_FUSED: ctx->generic_fused = value ? 1 : 0; return PF_OK;
-    case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 3) ? value : 3; return PF_OK;
+    case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 4) ? value : 4; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }

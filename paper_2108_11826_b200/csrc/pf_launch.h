@@ -39,6 +39,26 @@ struct UpWinArgs {
     int stage;           // 1: low-res plane staged in shared memory (variant 3)
 };
 size_t nms_up_win_smem(int h, int w, int H, int threads);
+
+// k_nms_up_corner (pf_corner.cu): exact slope-pruned fused upsample + 3x3 NMS.
+struct UpCornerArgs {
+    const float *conf;   // low-res [B][C][h][w]
+    int C, K, h, w;
+    int H, W;
+    float thr;
+    int cap;
+    int *counts;
+    uint2 *peaks;
+    AxisTab rows, cols;                  // per output row / column
+    const int4 *rband, *cband;           // bands: (first, last, src0, src1)
+    const double *rdt, *cdt;             // per band: min t step between adjacent outputs
+    int nbr, nbc;                        // band counts
+    int scr_rows, scr_cols;              // fallback scratch tile (max band + 2)
+    const int2 *src_rband, *src_cband;   // per source row / column: range of bands reading it
+};
+size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int scr_rows, int scr_cols);
+cudaError_t launch_nms_up_corner(const UpCornerArgs &a, int B, cudaStream_t s);
+cudaError_t configure_corner_kernels(int max_smem);
 cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s);
 cudaError_t launch_nms_plane(const float *conf, int B, int C, int K, int H, int W, float thr,
                              int half, int cap, int *counts, uint2 *peaks, cudaStream_t s);
