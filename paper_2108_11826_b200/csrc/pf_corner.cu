@@ -204,7 +204,7 @@ __device__ __forceinline__ void process_partial(const UpCornerArgs &a, const flo
     }
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 8)
 k_nms_up_corner(const UpCornerArgs a)
 {
     extern __shared__ __align__(16) unsigned char smc[];
@@ -220,13 +220,11 @@ k_nms_up_corner(const UpCornerArgs a)
     uint32_t *hotbits = reinterpret_cast<uint32_t *>(S + ((hw + 3) & ~3));         // [n_bw]
     uint32_t *cellbits = hotbits + n_bw;                                           // [n_cw]
     uint16_t *list = reinterpret_cast<uint16_t *>(cellbits + n_cw);                // [ncell] hot cells
-    uint16_t *plist = list + ((ncell + 7) & ~7);                                   // [ncell] partial cells
-    uint8_t *pok = reinterpret_cast<uint8_t *>(plist + ((ncell + 7) & ~7));        // [ncell] their h/v flags
-    __shared__ int n_hot, n_part;
+    __shared__ int n_hot;
 
     // ---- phase 1: the plane (the compulsory HBM read) -> shared memory + hot bitmap
     for (int c = threadIdx.x; c < n_cw; c += blockDim.x) cellbits[c] = 0u;
-    if (threadIdx.x == 0) { n_hot = 0; n_part = 0; }
+    if (threadIdx.x == 0) n_hot = 0;
     if ((hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
         const float4 *p4 = reinterpret_cast<const float4 *>(p);
         float4 *s4 = reinterpret_cast<float4 *>(S);
@@ -296,40 +294,44 @@ k_nms_up_corner(const UpCornerArgs a)
     }
     __syncthreads();
 
-    // ---- phase 3: classify hot cells; corners of normal cells; queue partial cells
+    // ---- phase 3: a warp takes 32 hot cells at a time (lane = cell): classify;
+    // corners of normal cells per lane; then the warp's partial cells, one at a
+    // time with all lanes over the candidate pixels.  No CTA barrier after this.
     const int nh = n_hot;
-    for (int idx = threadIdx.x; idx < nh; idx += blockDim.x) {
-        const int cell = list[idx];
-        const int pr = cell / nbc, q = cell - pr * nbc;
-        const int4 rb = __ldg(a.rband + pr), cb = __ldg(a.cband + q);
-        unsigned corners;
-        const unsigned ok = classify_cell(a, S, pr, q, rb, cb, corners);
-        if (ok != 3u) {
-            const int slot = atomicAdd(&n_part, 1);
-            plist[slot] = uint16_t(cell);
-            pok[slot] = uint8_t(ok);
-            continue;
+    for (int base = warp * kWarp; base < nh; base += blockDim.x) {
+        const int idx = base + lane;
+        unsigned ok = 3u;
+        int pr = 0, q = 0;
+        if (idx < nh) {
+            const int cell = list[idx];
+            pr = cell / nbc;
+            q = cell - pr * nbc;
+            const int4 rb = __ldg(a.rband + pr), cb = __ldg(a.cband + q);
+            unsigned corners;
+            ok = classify_cell(a, S, pr, q, rb, cb, corners);
+            if (ok == 3u) {
+                while (corners) {
+                    const int bit = __ffs(corners) - 1;
+                    corners &= corners - 1u;
+                    const int i = bit >> 1, j = bit & 1;
+                    if (i == 1 && rb.x == rb.y) continue;     // a 1-row band's pixel is visited once
+                    if (j == 1 && cb.x == cb.y) continue;
+                    if (!corner_cross_ok(a, S, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
+                    const int yy = i ? rb.x : rb.y, xx = j ? cb.x : cb.y;
+                    float v;
+                    if (exact_peak(a, S, yy, xx, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, yy, xx);
+                }
+            }
         }
-        while (corners) {
-            const int bit = __ffs(corners) - 1;
-            corners &= corners - 1u;
-            const int i = bit >> 1, j = bit & 1;
-            if (i == 1 && rb.x == rb.y) continue;         // a 1-row band's pixel is visited once
-            if (j == 1 && cb.x == cb.y) continue;
-            if (!corner_cross_ok(a, S, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
-            const int yy = i ? rb.x : rb.y, xx = j ? cb.x : cb.y;
-            float v;
-            if (exact_peak(a, S, yy, xx, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, yy, xx);
+        uint32_t part = __ballot_sync(0xffffffffu, idx < nh && ok != 3u);
+        while (part) {
+            const int src = __ffs(part) - 1;
+            part &= part - 1u;
+            const int ppr = __shfl_sync(0xffffffffu, pr, src);
+            const int pq = __shfl_sync(0xffffffffu, q, src);
+            const unsigned pok_ = __shfl_sync(0xffffffffu, ok, src);
+            process_partial(a, S, plane, ppr, pq, pok_, lane);
         }
-    }
-    __syncthreads();
-
-    // ---- phase 4: partial cells, one warp each (lanes over candidate pixels)
-    const int np = n_part;
-    for (int f = warp; f < np; f += blockDim.x >> 5) {
-        const int cell = plist[f];
-        const int pr = cell / nbc, q = cell - pr * nbc;
-        process_partial(a, S, plane, pr, q, pok[f], lane);
     }
 }
 
@@ -339,7 +341,7 @@ size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int scr_rows, int scr_
     (void)scr_cols;
     const int hw = h * w, ncell = nbr * nbc;
     return (size_t)((hw + 3) & ~3) * sizeof(float) + (size_t)(((hw + 127) & ~127) >> 5) * 4 +
-           (size_t)((ncell + 31) >> 5) * 4 + (size_t)((ncell + 7) & ~7) * (2 + 2 + 1) + 16;
+           (size_t)((ncell + 31) >> 5) * 4 + (size_t)((ncell + 7) & ~7) * 2 + 16;
 }
 
 cudaError_t launch_nms_up_corner(const UpCornerArgs &a, int B, cudaStream_t s)
