@@ -307,7 +307,7 @@ def run_b200(args, rank, world, local_rank):
     chunk = 1024
     launches_per_step = {name: n / args.steps for name, (ms, n) in ktimes.items()}
     per_frame_bytes = {"k_nms_up": BYTES_FUSED_UN, "k_nms_up_win": BYTES_FUSED_UN,
-                       "k_nms_plane": BYTES_FUSED_UN,
+                       "k_nms_up_corner": BYTES_FUSED_UN, "k_nms_plane": BYTES_FUSED_UN,
                        "k_parse_frames": BYTES_PARSE}
     for name, (ms, n) in ktimes.items():
         frames_per_launch = F / launches_per_step[name]

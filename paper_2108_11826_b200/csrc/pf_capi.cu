@@ -34,10 +34,9 @@ struct AxisCache {
     std::vector<int4> bands;                    // (first, last, src0, src1) per band
     std::vector<double> band_dt;                // min t step inside each band (inf if 1 wide)
     int max_band = 0;
-    std::vector<int2> src_band;                 // per source index: [lo, hi] bands reading it
+    bool canonical = false;                     // band b reads sources (b-1, b) clipped: b = 0..in_n
     int4 *d_bands = nullptr;
     double *d_band_dt = nullptr;
-    int2 *d_src_band = nullptr;
     int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr, *d_gend = nullptr;
     double2 *d_tw = nullptr;
     double *d_t = nullptr, *d_omt = nullptr;
@@ -76,13 +75,9 @@ void fill_axis(AxisCache &a, int in_n, int out_n)
         a.band_dt.push_back(dt);
         a.max_band = std::max(a.max_band, e - o + 1);
     }
-    a.src_band.assign(in_n, make_int2(0x3fffffff, -1));
-    for (int b = 0; b < (int)a.bands.size(); ++b) {
-        for (int r : {a.bands[b].z, a.bands[b].w}) {
-            a.src_band[r].x = std::min(a.src_band[r].x, b);
-            a.src_band[r].y = std::max(a.src_band[r].y, b);
-        }
-    }
+    a.canonical = (int)a.bands.size() == in_n + 1 && in_n >= 2;
+    for (int b = 0; a.canonical && b <= in_n; ++b)
+        a.canonical = a.bands[b].z == std::max(b - 1, 0) && a.bands[b].w == std::min(b, in_n - 1);
     a.first_out.assign(in_n, 0x3fffffff);
     a.last_out.assign(in_n, -1);
     for (int o = 0; o < out_n; ++o) {
@@ -283,8 +278,6 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
         }
         CU(dev_alloc(&a.d_bands, a.bands.size()));
         CU(cudaMemcpy(a.d_bands, a.bands.data(), a.bands.size() * sizeof(int4), cudaMemcpyHostToDevice));
-        CU(dev_alloc(&a.d_src_band, a.src_band.size()));
-        CU(cudaMemcpy(a.d_src_band, a.src_band.data(), a.src_band.size() * sizeof(int2), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_band_dt, a.band_dt.size()));
         CU(cudaMemcpy(a.d_band_dt, a.band_dt.data(), a.band_dt.size() * sizeof(double), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_gend, out_n));
@@ -448,21 +441,19 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
     } else if (!blur && half == 1 && !ctx->materialise && !ctx->generic_fused && ctx->win_variant == 4 &&
-               rows->max_band + 2 <= 64 && cols->max_band + 2 <= 64 &&
-               nms_up_corner_smem(h, w, (int)rows->bands.size(), (int)cols->bands.size(), rows->max_band + 2,
-                                  cols->max_band + 2) <= 96 * 1024) {
+               rows->canonical && cols->canonical && (long long)(h + 1) * (w + 1) <= 65535 &&
+               nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) <= 100 * 1024) {
         UpCornerArgs a{};
-        a.conf = conf; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
+        a.conf = conf; a.B = n; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
         a.thr = thr; a.cap = ctx->caps.max_peaks_per_part;
         a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
         a.rows = rows->dev(); a.cols = cols->dev();
         a.rband = rows->d_bands; a.cband = cols->d_bands;
         a.rdt = rows->d_band_dt; a.cdt = cols->d_band_dt;
         a.nbr = (int)rows->bands.size(); a.nbc = (int)cols->bands.size();
-        a.scr_rows = rows->max_band + 2; a.scr_cols = cols->max_band + 2;
-        a.src_rband = rows->d_src_band; a.src_cband = cols->d_src_band;
+        a.nst = kCornerStages;
         KernelTimer kt(ctx, kNmsUpCorner);
-        CU(launch_nms_up_corner(a, n, s));
+        CU(launch_nms_up_corner(a, s));
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
                nms_up_win_smem(h, w, H, 128) <= 96 * 1024) {
         UpWinArgs a{};
@@ -789,7 +780,7 @@ void pf_destroy(pf_ctx *ctx)
         cudaFree(kv.second.d_i0); cudaFree(kv.second.d_i1);
         cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
         cudaFree(kv.second.d_first); cudaFree(kv.second.d_last); cudaFree(kv.second.d_gend); cudaFree(kv.second.d_tw);
-        cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt); cudaFree(kv.second.d_src_band);
+        cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt);
     }
     for (auto &p : ctx->pending) { ctx->ev_pool.push_back(p.second.first); ctx->ev_pool.push_back(p.second.second); }
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

@@ -36,11 +36,34 @@
 // ("> left" for x2) whenever it clears n, and likewise vertically.  Every
 // surviving pixel (a few per plane) gets the exact 3x3 test on exactly
 // computed values.
+//
+// Pipeline (B200).  Persistent CTAs (grid = resident CTAs, planes
+// round-robin).  Each low-res plane is one contiguous h*w fp32 block, so it
+// is fetched by a single 1-D bulk copy (cp.async.bulk, the TMA unit) into a
+// ring of shared-memory stages signalled by mbarriers; the next plane lands
+// while the current one is processed, so the kernel never waits on HBM
+// latency.  Per plane: (A) the hot-source bitmap from shared memory, (B) the
+// hot cells as row-band bit masks — with integer upsampling the bands are
+// canonical (band b reads sources b-1, b), so cell (p, q) is hot iff
+// M_p bit q-1 or bit q, M_p = hot row p-1 | hot row p — compacted into a list,
+// (C) one warp per 32 hot cells: classify, test surviving corners, and walk
+// partial cells with all lanes.  The per-band slope weights live in shared
+// memory for the whole kernel.
+#include <algorithm>
+
 #include "pf_launch.h"
 
 namespace pf {
 
 constexpr float kNoise = 7.62939453125e-06f;   // 2^-17
+constexpr int kCornerThreads = 128;
+constexpr int kCornerCands = 1024;   // candidate pixels per plane kept in shared memory
+
+// Per band, fp32 copies of the axis weights the classification uses.
+struct BandT {
+    float omt_f, t_f, omt_l, t_l;   // (1 - t), t at the band's first and last output
+    float s_l, s_f, dt, pad;        // t step into the last output, out of the first; min step
+};
 
 __device__ __forceinline__ void emit_peak_c(int *counts, uint2 *peaks, int plane, int cap, float v, int i, int j)
 {
@@ -116,30 +139,48 @@ __device__ __forceinline__ float sl_v(const CellF &c, float omtx, float tx)
     return (c.b0 - c.a0) * omtx + (c.b1 - c.a1) * tx;
 }
 
+// Shared-memory view of one CTA's band tables.
+struct Bands {
+    const int4 *rb, *cb;      // (first, last, src0, src1)
+    const BandT *rt, *ct;
+};
+
 // Cross-boundary part of the corner test for the corner pixel (row role i,
 // column role j) of corner (P, Q): the pixel is (i ? first(P+1) : last(P),
 // j ? first(Q+1) : last(Q)) in cell (P+i, Q+j).  The own-cell in-band
-// neighbours were checked by the caller.
-__device__ __forceinline__ bool corner_cross_ok(const UpCornerArgs &a, const float *S, int P, int Q, int i, int j)
+// neighbours were checked by the caller.  Canonical bands: the four cells
+// around the corner read the 3x3 sources rows (R0.z, R0.w = R1.z, R1.w) x
+// columns (C0.z, C0.w = C1.z, C1.w), so both boundaries are piecewise affine.
+__device__ __forceinline__ bool corner_cross_ok(const Bands &bd, const float *S, int w, int P, int Q, int i, int j)
 {
-    const int4 R0 = __ldg(a.rband + P), R1 = __ldg(a.rband + P + 1);
-    const int4 C0 = __ldg(a.cband + Q), C1 = __ldg(a.cband + Q + 1);
-    const CellF c00 = cellf(S, a.w, R0, C0), c01 = cellf(S, a.w, R0, C1);
-    const CellF c10 = cellf(S, a.w, R1, C0), c11 = cellf(S, a.w, R1, C1);
-    const float n = fmaxf(fmaxf(mag(c00), mag(c01)), fmaxf(mag(c10), mag(c11))) * kNoise;
-    const int y1 = R0.y, y2 = R1.x, x1 = C0.y, x2 = C1.x;
-    const int yy = i ? y2 : y1, xx = j ? x2 : x1;
-    if (C0.w == C1.z) {              // bands share the source column: piecewise affine across it
-        const float omty = (float)__ldg(a.rows.omt + yy), ty = (float)__ldg(a.rows.t + yy);
-        const float mq = sl_h(i ? c10 : c00, omty, ty), mq1 = sl_h(i ? c11 : c01, omty, ty);
-        const float cross = mq * (float)__ldg(a.cols.omt + x1) + mq1 * (float)__ldg(a.cols.t + x2);
-        if (j == 0 ? cross > n : cross < -n) return false;     // ~ G(x2) - G(x1)
+    const int4 R0 = bd.rb[P], R1 = bd.rb[P + 1];
+    const int4 C0 = bd.cb[Q], C1 = bd.cb[Q + 1];
+    const float *s0 = S + R0.z * w, *s1 = S + R0.w * w, *s2 = S + R1.w * w;
+    const float v00 = s0[C0.z], v01 = s0[C0.w], v02 = s0[C1.w];
+    const float v10 = s1[C0.z], v11 = s1[C0.w], v12 = s1[C1.w];
+    const float v20 = s2[C0.z], v21 = s2[C0.w], v22 = s2[C1.w];
+    const float n = fmaxf(fmaxf(fmaxf(fabsf(v00), fabsf(v01)), fmaxf(fabsf(v02), fabsf(v10))),
+                          fmaxf(fmaxf(fabsf(v11), fabsf(v12)), fmaxf(fmaxf(fabsf(v20), fabsf(v21)), fabsf(v22)))) *
+                    kNoise;
+    const BandT &rt0 = bd.rt[P], &rt1 = bd.rt[P + 1], &ct0 = bd.ct[Q], &ct1 = bd.ct[Q + 1];
+    {
+        // horizontal step across the column boundary, on row yy of cell row P+i
+        const float omty = i ? rt1.omt_f : rt0.omt_l, ty = i ? rt1.t_f : rt0.t_l;
+        const float ua0 = i ? v10 : v00, ua1 = i ? v11 : v01, ua2 = i ? v12 : v02;   // upper source row
+        const float ub0 = i ? v20 : v10, ub1 = i ? v21 : v11, ub2 = i ? v22 : v12;   // lower source row
+        const float mq = (ua1 - ua0) * omty + (ub1 - ub0) * ty;
+        const float mq1 = (ua2 - ua1) * omty + (ub2 - ub1) * ty;
+        const float cross = mq * ct0.omt_l + mq1 * ct1.t_f;                           // ~ G(x2) - G(x1)
+        if (j == 0 ? cross > n : cross < -n) return false;
     }
-    if (R0.w == R1.z) {
-        const float omtx = (float)__ldg(a.cols.omt + xx), tx = (float)__ldg(a.cols.t + xx);
-        const float mp = sl_v(j ? c01 : c00, omtx, tx), mp1 = sl_v(j ? c11 : c10, omtx, tx);
-        const float cross = mp * (float)__ldg(a.rows.omt + y1) + mp1 * (float)__ldg(a.rows.t + y2);
-        if (i == 0 ? cross > n : cross < -n) return false;     // ~ G(y2) - G(y1)
+    {
+        const float omtx = j ? ct1.omt_f : ct0.omt_l, tx = j ? ct1.t_f : ct0.t_l;
+        const float la0 = j ? v01 : v00, la1 = j ? v11 : v10, la2 = j ? v21 : v20;   // left source column
+        const float lb0 = j ? v02 : v01, lb1 = j ? v12 : v11, lb2 = j ? v22 : v21;   // right source column
+        const float mp = (la1 - la0) * omtx + (lb1 - lb0) * tx;
+        const float mp1 = (la2 - la1) * omtx + (lb2 - lb1) * tx;
+        const float cross = mp * rt0.omt_l + mp1 * rt1.t_f;                           // ~ G(y2) - G(y1)
+        if (i == 0 ? cross > n : cross < -n) return false;
     }
     return true;
 }
@@ -147,168 +188,293 @@ __device__ __forceinline__ bool corner_cross_ok(const UpCornerArgs &a, const flo
 // Classify a hot cell.  Returns bit 0 = h_ok, bit 1 = v_ok (3 = normal) and,
 // for the own-cell corner tests, a bitmask of corners (bit 2*i + j) whose
 // in-band neighbours do not strictly beat them.
-__device__ __forceinline__ unsigned classify_cell(const UpCornerArgs &a, const float *S, int p, int q, int4 rb,
-                                                  int4 cb, unsigned &corners)
+__device__ __forceinline__ unsigned classify_cell(const Bands &bd, const float *S, int w, int nbr, int nbc,
+                                                  int p, int q, int4 rb, int4 cb, unsigned &corners)
 {
     corners = 0u;
-    const CellF c = cellf(S, a.w, rb, cb);
+    const CellF c = cellf(S, w, rb, cb);
     const float n = mag(c) * kNoise;
     if (!(n <= 3.0e38f)) return 0u;                                     // NaN / inf sources: all pixels
-    const float d_first = sl_h(c, (float)__ldg(a.rows.omt + rb.x), (float)__ldg(a.rows.t + rb.x));
-    const float d_last = sl_h(c, (float)__ldg(a.rows.omt + rb.y), (float)__ldg(a.rows.t + rb.y));
-    const float e_first = sl_v(c, (float)__ldg(a.cols.omt + cb.x), (float)__ldg(a.cols.t + cb.x));
-    const float e_last = sl_v(c, (float)__ldg(a.cols.omt + cb.y), (float)__ldg(a.cols.t + cb.y));
-    bool h_ok = q != 0 && q != a.nbc - 1, v_ok = p != 0 && p != a.nbr - 1;   // border bands: flat
+    const BandT rt = bd.rt[p], ct = bd.ct[q];
+    const float d_first = sl_h(c, rt.omt_f, rt.t_f), d_last = sl_h(c, rt.omt_l, rt.t_l);
+    const float e_first = sl_v(c, ct.omt_f, ct.t_f), e_last = sl_v(c, ct.omt_l, ct.t_l);
+    bool h_ok = q != 0 && q != nbc - 1, v_ok = p != 0 && p != nbr - 1;   // border bands: flat
     if (h_ok && cb.y - cb.x >= 2) {                                     // interior columns exist
         h_ok = ((d_first > 0.f && d_last > 0.f) || (d_first < 0.f && d_last < 0.f)) &&
-               fminf(fabsf(d_first), fabsf(d_last)) * (float)__ldg(a.cdt + q) > n;
+               fminf(fabsf(d_first), fabsf(d_last)) * ct.dt > n;
     }
     if (v_ok && rb.y - rb.x >= 2) {                                     // interior rows exist
         v_ok = ((e_first > 0.f && e_last > 0.f) || (e_first < 0.f && e_last < 0.f)) &&
-               fminf(fabsf(e_first), fabsf(e_last)) * (float)__ldg(a.rdt + p) > n;
+               fminf(fabsf(e_first), fabsf(e_last)) * rt.dt > n;
     }
     if (h_ok && v_ok) {
         // in-band neighbour steps of each corner (i = 1 top row, j = 1 left column)
-        const float sxl = (float)(__ldg(a.cols.t + cb.y) - __ldg(a.cols.t + max(cb.y - 1, cb.x)));
-        const float sxr = (float)(__ldg(a.cols.t + min(cb.x + 1, cb.y)) - __ldg(a.cols.t + cb.x));
-        const float syu = (float)(__ldg(a.rows.t + rb.y) - __ldg(a.rows.t + max(rb.y - 1, rb.x)));
-        const float syd = (float)(__ldg(a.rows.t + min(rb.x + 1, rb.y)) - __ldg(a.rows.t + rb.x));
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const float d = i ? d_first : d_last, e = j ? e_first : e_last;
                 bool ok = true;
-                if (cb.y > cb.x) ok = ok && (j == 0 ? !(d * sxl < -n) : !(d * sxr > n));
-                if (rb.y > rb.x) ok = ok && (i == 0 ? !(e * syu < -n) : !(e * syd > n));
+                if (cb.y > cb.x) ok = ok && (j == 0 ? !(d * ct.s_l < -n) : !(d * ct.s_f > n));
+                if (rb.y > rb.x) ok = ok && (i == 0 ? !(e * rt.s_l < -n) : !(e * rt.s_f > n));
                 if (ok) corners |= 1u << (2 * i + j);
             }
     }
     return (h_ok ? 1u : 0u) | (v_ok ? 2u : 0u);
 }
 
-// Candidate pixels of a partial cell, exactly tested by the warp's lanes.
-__device__ __forceinline__ void process_partial(const UpCornerArgs &a, const float *S, int plane, int p, int q,
-                                                unsigned ok, int lane)
+// Candidate list of one plane (shared memory): packed (y << 16 | x).
+struct CandList {
+    uint32_t *c;
+    int *n;
+    int cap;
+};
+
+__device__ __forceinline__ void push_cand(const UpCornerArgs &a, const CandList &cl, const float *S, int plane,
+                                          int y, int x)
 {
-    const int4 rb = __ldg(a.rband + p), cb = __ldg(a.cband + q);
-    const int bh = rb.y - rb.x + 1, bw = cb.y - cb.x + 1;
-    // candidate rows: the two boundary rows when v_ok, else all rows; same for columns
-    const int nr = (ok & 2u) ? min(bh, 2) : bh, nc = (ok & 1u) ? min(bw, 2) : bw;
-    for (int e = lane; e < nr * nc; e += kWarp) {
-        const int r = e / nc, c = e - r * nc;
-        const int y = (ok & 2u) ? (r ? rb.y : rb.x) : rb.x + r;
-        const int x = (ok & 1u) ? (c ? cb.y : cb.x) : cb.x + c;
+    const int slot = atomicAdd(cl.n, 1);
+    if (slot < cl.cap) {
+        cl.c[slot] = (uint32_t(y) << 16) | uint32_t(x);
+    } else {   // list full (pathological planes): test in place
         float v;
         if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
     }
 }
 
-__global__ void __launch_bounds__(128, 8)
+// Candidate pixels of a partial cell.  Rows restricted to the boundary rows
+// when v_ok, columns to the boundary columns when h_ok; further, a row whose
+// own slope clears the noise bound is strictly monotone inside the cell, so
+// only its rising-end column can be "> left and >= right" (and likewise a
+// monotone column keeps only its rising-end row).
+__device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands &bd, const CandList &cl,
+                                              const float *S, int plane, int p, int q, unsigned ok)
+{
+    const int4 rb = bd.rb[p], cb = bd.cb[q];
+    const CellF c = cellf(S, a.w, rb, cb);
+    const float n = mag(c) * kNoise;              // NaN / inf: no compare passes, nothing pruned
+    const float cdt = bd.ct[q].dt, rdt = bd.rt[p].dt;
+    const bool q_in = q != 0 && q != a.nbc - 1 && cb.y > cb.x;
+    const bool p_in = p != 0 && p != a.nbr - 1 && rb.y > rb.x;
+    const int bh = rb.y - rb.x + 1, bw = cb.y - cb.x + 1;
+    const int nr = (ok & 2u) ? min(bh, 2) : bh, nc = (ok & 1u) ? min(bw, 2) : bw;
+    for (int r = 0; r < nr; ++r) {
+        const int y = (ok & 2u) ? (r ? rb.y : rb.x) : rb.x + r;
+        int only_x = -1;
+        if (q_in) {
+            const float d = sl_h(c, (float)__ldg(a.rows.omt + y), (float)__ldg(a.rows.t + y));
+            if (fabsf(d) * cdt > n) only_x = d > 0.f ? cb.y : cb.x;
+        }
+        for (int k = 0; k < nc; ++k) {
+            const int x = (ok & 1u) ? (k ? cb.y : cb.x) : cb.x + k;
+            if (only_x >= 0 && x != only_x) continue;
+            if (p_in) {
+                const float e = sl_v(c, (float)__ldg(a.cols.omt + x), (float)__ldg(a.cols.t + x));
+                if (fabsf(e) * rdt > n && y != (e > 0.f ? rb.y : rb.x)) continue;
+            }
+            push_cand(a, cl, S, plane, y, x);
+        }
+    }
+}
+
+// ---- mbarrier + 1-D bulk copy (TMA) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+// Shared-memory layout of one CTA (byte offsets).
+struct CornerLayout {
+    int plane_floats;    // h*w rounded up to 128 (padding = -inf)
+    int n_hw;            // hot-bitmap words per plane
+    size_t planes, bars, rb, cb, rt, ct, hot, list, cand, total;
+};
+
+__host__ __device__ inline CornerLayout corner_layout(int h, int w, int nbr, int nbc, int nst)
+{
+    CornerLayout L;
+    const int hw = h * w;
+    L.plane_floats = (hw + 127) & ~127;
+    L.n_hw = L.plane_floats >> 5;
+    size_t o = 0;
+    L.planes = o; o += (size_t)nst * L.plane_floats * sizeof(float);
+    L.bars = o;   o += (size_t)nst * 8;
+    o = (o + 15) & ~(size_t)15;
+    L.rb = o;     o += (size_t)nbr * sizeof(int4);
+    L.cb = o;     o += (size_t)nbc * sizeof(int4);
+    L.rt = o;     o += (size_t)nbr * sizeof(BandT);
+    L.ct = o;     o += (size_t)nbc * sizeof(BandT);
+    L.hot = o;    o += (size_t)(L.n_hw + 4) * sizeof(uint32_t);
+    L.list = o;   o += (size_t)((nbr * nbc + 7) & ~7) * sizeof(uint16_t);
+    L.cand = o;   o += (size_t)kCornerCands * sizeof(uint32_t);
+    L.total = (o + 15) & ~(size_t)15;
+    return L;
+}
+
+__device__ __forceinline__ void fill_band(const AxisTab &tab, const double *dt, const int4 *bands, int b, int4 &B,
+                                          BandT &T)
+{
+    B = __ldg(bands + b);
+    const int f = B.x, l = B.y;
+    T.omt_f = (float)__ldg(tab.omt + f);
+    T.t_f = (float)__ldg(tab.t + f);
+    T.omt_l = (float)__ldg(tab.omt + l);
+    T.t_l = (float)__ldg(tab.t + l);
+    T.s_l = (float)(__ldg(tab.t + l) - __ldg(tab.t + max(l - 1, f)));
+    T.s_f = (float)(__ldg(tab.t + min(f + 1, l)) - __ldg(tab.t + f));
+    T.dt = (float)__ldg(dt + b);
+    T.pad = 0.f;
+}
+
+// Hot bits of source row r, columns [32j, 32j+32), from the
+// linear hot bitmap (bits beyond the row masked off).
+__device__ __forceinline__ uint32_t row_word(const uint32_t *hot, int h, int w, int r, int j)
+{
+    const int c0 = j << 5;
+    if (r < 0 || r >= h || c0 >= w) return 0u;
+    const int o = r * w + c0;
+    uint32_t v = __funnelshift_r(hot[o >> 5], hot[(o >> 5) + 1], o & 31);
+    const int rem = w - c0;
+    if (rem < 32) v &= (1u << rem) - 1u;
+    return v;
+}
+
+__global__ void __launch_bounds__(kCornerThreads, 4)
 k_nms_up_corner(const UpCornerArgs a)
 {
-    extern __shared__ __align__(16) unsigned char smc[];
-    const int plane = blockIdx.x;
-    const int b = plane / a.K, k = plane - b * a.K;
-    const float *p = a.conf + ((size_t)b * a.C + k) * (size_t)a.h * a.w;
+    extern __shared__ __align__(128) unsigned char smc[];
     const int h = a.h, w = a.w, hw = h * w;
-    const int nbc = a.nbc, ncell = a.nbr * nbc;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_bw = ((hw + 127) & ~127) >> 5;
-    const int n_cw = (ncell + 31) >> 5;
-    float *S = reinterpret_cast<float *>(smc);                                     // [h*w]
-    uint32_t *hotbits = reinterpret_cast<uint32_t *>(S + ((hw + 3) & ~3));         // [n_bw]
-    uint32_t *cellbits = hotbits + n_bw;                                           // [n_cw]
-    uint16_t *list = reinterpret_cast<uint16_t *>(cellbits + n_cw);                // [ncell] hot cells
-    __shared__ int n_hot;
+    const int nbr = a.nbr, nbc = a.nbc, nst = a.nst;
+    const CornerLayout L = corner_layout(h, w, nbr, nbc, nst);
+    float *planes = reinterpret_cast<float *>(smc + L.planes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smc + L.bars);
+    int4 *RB = reinterpret_cast<int4 *>(smc + L.rb);
+    int4 *CB = reinterpret_cast<int4 *>(smc + L.cb);
+    BandT *RT = reinterpret_cast<BandT *>(smc + L.rt);
+    BandT *CT = reinterpret_cast<BandT *>(smc + L.ct);
+    uint32_t *hot = reinterpret_cast<uint32_t *>(smc + L.hot);
+    uint16_t *list = reinterpret_cast<uint16_t *>(smc + L.list);
+    uint32_t *cand = reinterpret_cast<uint32_t *>(smc + L.cand);
+    __shared__ int n_hot, n_cand;
+    const CandList cl{cand, &n_cand, kCornerCands};
+    const Bands bd{RB, CB, RT, CT};
+    const int lane = threadIdx.x & 31;
+    const long long P = (long long)a.B * a.K;
+    const uint32_t plane_bytes = (uint32_t)hw * 4u;
 
-    // ---- phase 1: the plane (the compulsory HBM read) -> shared memory + hot bitmap
-    for (int c = threadIdx.x; c < n_cw; c += blockDim.x) cellbits[c] = 0u;
-    if (threadIdx.x == 0) n_hot = 0;
-    if ((hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-        const float4 *p4 = reinterpret_cast<const float4 *>(p);
-        float4 *s4 = reinterpret_cast<float4 *>(S);
-        const int n4 = hw >> 2, n4_pad = (n4 + 31) & ~31;
-        constexpr int U = 8;
-        for (int e0 = threadIdx.x; e0 < n4_pad; e0 += U * blockDim.x) {
-            float4 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                v[u] = e < n4 ? __ldg(p4 + e) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    // ---- prologue: band tables, -inf plane padding, barriers, first loads
+    for (int b = threadIdx.x; b < nbr + nbc; b += kCornerThreads) {
+        if (b < nbr) fill_band(a.rows, a.rdt, a.rband, b, RB[b], RT[b]);
+        else fill_band(a.cols, a.cdt, a.cband, b - nbr, CB[b - nbr], CT[b - nbr]);
+    }
+    for (int s = 0; s < nst; ++s)
+        for (int e = hw + threadIdx.x; e < L.plane_floats; e += kCornerThreads) planes[s * L.plane_floats + e] = -INFINITY;
+    for (int e = L.n_hw + threadIdx.x; e < L.n_hw + 4; e += kCornerThreads) hot[e] = 0u;
+    if (threadIdx.x == 0) {
+        n_hot = 0;
+        n_cand = 0;
+        if (a.bulk) {
+            for (int s = 0; s < nst; ++s) mbar_init(bars + s, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int s = 0; s < nst; ++s) {
+                const long long pl = blockIdx.x + (long long)s * gridDim.x;
+                if (pl < P) {
+                    const long long b = pl / a.K, k = pl - b * a.K;
+                    bulk_load(planes + s * L.plane_floats, a.conf + ((size_t)b * a.C + k) * (size_t)hw, plane_bytes,
+                              bars + s);
+                }
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                if (e - lane >= n4_pad) break;                                     // warp-uniform tail
-                if (e < n4) s4[e] = v[u];
-                uint32_t nib = uint32_t(v[u].x >= a.thr) | (uint32_t(v[u].y >= a.thr) << 1) |
-                               (uint32_t(v[u].z >= a.thr) << 2) | (uint32_t(v[u].w >= a.thr) << 3);
-                nib = (e < n4 ? nib : 0u) << (4 * (lane & 7));
+        }
+    }
+    __syncthreads();
+
+    int it = 0;
+    for (long long pl = blockIdx.x; pl < P; pl += gridDim.x, ++it) {
+        const int stage = it % nst;
+        float *S = planes + stage * L.plane_floats;
+        const int plane = (int)pl;
+        if (a.bulk) {
+            mbar_wait(bars + stage, (uint32_t)(it / nst) & 1u);
+        } else {
+            const long long b = pl / a.K, k = pl - b * a.K;
+            const float *src = a.conf + ((size_t)b * a.C + k) * (size_t)hw;
+            for (int e = threadIdx.x; e < hw; e += kCornerThreads) S[e] = __ldg(src + e);
+            __syncthreads();
+        }
+
+        // ---- (A) hot-source bitmap: 8 lanes x float4 = one 32-bit word
+        {
+            const float4 *s4 = reinterpret_cast<const float4 *>(S);
+            const int n4 = L.plane_floats >> 2;            // multiple of 32: warp-uniform trip count
+            for (int e = threadIdx.x; e < n4; e += kCornerThreads) {
+                const float4 v = s4[e];
+                uint32_t nib = uint32_t(v.x >= a.thr) | (uint32_t(v.y >= a.thr) << 1) |
+                               (uint32_t(v.z >= a.thr) << 2) | (uint32_t(v.w >= a.thr) << 3);
+                nib <<= 4 * (lane & 7);
                 nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
                 nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
                 nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
-                if ((lane & 7) == 0) hotbits[e >> 3] = nib;
+                if ((lane & 7) == 0) hot[e >> 3] = nib;
             }
         }
-    } else {
-        for (int q = threadIdx.x; q < n_bw; q += blockDim.x) hotbits[q] = 0u;
         __syncthreads();
-        for (int e = threadIdx.x; e < hw; e += blockDim.x) {
-            const float v = __ldg(p + e);
-            S[e] = v;
-            if (v >= a.thr) atomicOr(hotbits + (e >> 5), 1u << (e & 31));
-        }
-    }
-    __syncthreads();
 
-    // ---- phase 2: hot cells = the cells reading a hot source (bitmap, then a dense list)
-    for (int q = threadIdx.x; q < n_bw; q += blockDim.x) {
-        uint32_t m = hotbits[q];
-        if (!m) continue;
-        const int base = q << 5;
-        int r = base / w;                    // a 32-bit word spans at most ceil(32/w)+1 rows
-        int c0 = base - r * w;
-        while (m) {
-            const int bit = __ffs(m) - 1;
-            m &= m - 1u;
-            int rr = r, c = c0 + bit;
-            while (c >= w) { c -= w; ++rr; }
-            const int2 br = __ldg(a.src_rband + rr), bc = __ldg(a.src_cband + c);
-            for (int pp = br.x; pp <= br.y; ++pp)
-                for (int qq = bc.x; qq <= bc.y; ++qq) {
-                    const int cell = pp * nbc + qq;
-                    atomicOr(cellbits + (cell >> 5), 1u << (cell & 31));
+        // ---- (B) hot cells of canonical bands: C_p = M_p | M_p << 1 (+ carry)
+        {
+            const int nwc = (w + 32) >> 5;                  // words per band row (nbc = w + 1 bits)
+            const int ntask = (h + 1) * nwc;
+            for (int t = threadIdx.x; t < ntask; t += kCornerThreads) {
+                const int p = t / nwc, j = t - p * nwc;
+                const uint32_t m = row_word(hot, h, w, p - 1, j) | row_word(hot, h, w, p, j);
+                uint32_t c = m | (m << 1);
+                if (j) c |= (row_word(hot, h, w, p - 1, j - 1) | row_word(hot, h, w, p, j - 1)) >> 31;
+                if (c) {
+                    int slot = atomicAdd(&n_hot, __popc(c));
+                    const int base = p * nbc + (j << 5);
+                    while (c) {
+                        list[slot++] = uint16_t(base + __ffs(c) - 1);
+                        c &= c - 1u;
+                    }
                 }
+            }
         }
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < n_cw; q += blockDim.x) {
-        uint32_t m = cellbits[q];
-        if (!m) continue;
-        int slot = atomicAdd(&n_hot, __popc(m));
-        while (m) {
-            list[slot++] = uint16_t((q << 5) + __ffs(m) - 1);
-            m &= m - 1u;
-        }
-    }
-    __syncthreads();
+        __syncthreads();
 
-    // ---- phase 3: a warp takes 32 hot cells at a time (lane = cell): classify;
-    // corners of normal cells per lane; then the warp's partial cells, one at a
-    // time with all lanes over the candidate pixels.  No CTA barrier after this.
-    const int nh = n_hot;
-    for (int base = warp * kWarp; base < nh; base += blockDim.x) {
-        const int idx = base + lane;
-        unsigned ok = 3u;
-        int pr = 0, q = 0;
-        if (idx < nh) {
+        // ---- (C1) lane = hot cell: classify; normal cells push their surviving
+        // corner, partial cells their candidate pixels
+        const int nh = n_hot;
+        for (int idx = threadIdx.x; idx < nh; idx += kCornerThreads) {
             const int cell = list[idx];
-            pr = cell / nbc;
-            q = cell - pr * nbc;
-            const int4 rb = __ldg(a.rband + pr), cb = __ldg(a.cband + q);
+            const int pr = cell / nbc, q = cell - pr * nbc;
+            const int4 rb = RB[pr], cb = CB[q];
             unsigned corners;
-            ok = classify_cell(a, S, pr, q, rb, cb, corners);
+            const unsigned ok = classify_cell(bd, S, w, nbr, nbc, pr, q, rb, cb, corners);
             if (ok == 3u) {
                 while (corners) {
                     const int bit = __ffs(corners) - 1;
@@ -316,40 +482,59 @@ k_nms_up_corner(const UpCornerArgs a)
                     const int i = bit >> 1, j = bit & 1;
                     if (i == 1 && rb.x == rb.y) continue;     // a 1-row band's pixel is visited once
                     if (j == 1 && cb.x == cb.y) continue;
-                    if (!corner_cross_ok(a, S, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
-                    const int yy = i ? rb.x : rb.y, xx = j ? cb.x : cb.y;
-                    float v;
-                    if (exact_peak(a, S, yy, xx, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, yy, xx);
+                    if (!corner_cross_ok(bd, S, w, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
+                    push_cand(a, cl, S, plane, i ? rb.x : rb.y, j ? cb.x : cb.y);
                 }
+            } else {
+                partial_cands(a, bd, cl, S, plane, pr, q, ok);
             }
         }
-        uint32_t part = __ballot_sync(0xffffffffu, idx < nh && ok != 3u);
-        while (part) {
-            const int src = __ffs(part) - 1;
-            part &= part - 1u;
-            const int ppr = __shfl_sync(0xffffffffu, pr, src);
-            const int pq = __shfl_sync(0xffffffffu, q, src);
-            const unsigned pok_ = __shfl_sync(0xffffffffu, ok, src);
-            process_partial(a, S, plane, ppr, pq, pok_, lane);
+        __syncthreads();
+
+        // ---- (C2) lane = candidate pixel: the exact 3x3 test
+        const int nc = min(n_cand, kCornerCands);
+        for (int e = threadIdx.x; e < nc; e += kCornerThreads) {
+            const uint32_t yx = cand[e];
+            const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
+            float v;
+            if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
+        }
+        __syncthreads();                                     // stage + list free again
+        if (threadIdx.x == 0) {
+            n_hot = 0;
+            n_cand = 0;
+            const long long nx = pl + (long long)nst * gridDim.x;
+            if (a.bulk && nx < P) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const long long b = nx / a.K, k = nx - b * a.K;
+                bulk_load(S, a.conf + ((size_t)b * a.C + k) * (size_t)hw, plane_bytes, bars + stage);
+            }
         }
     }
 }
 
-size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int scr_rows, int scr_cols)
+size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst)
 {
-    (void)scr_rows;
-    (void)scr_cols;
-    const int hw = h * w, ncell = nbr * nbc;
-    return (size_t)((hw + 3) & ~3) * sizeof(float) + (size_t)(((hw + 127) & ~127) >> 5) * 4 +
-           (size_t)((ncell + 31) >> 5) * 4 + (size_t)((ncell + 7) & ~7) * 2 + 16;
+    return corner_layout(h, w, nbr, nbc, nst).total;
 }
 
-cudaError_t launch_nms_up_corner(const UpCornerArgs &a, int B, cudaStream_t s)
+cudaError_t launch_nms_up_corner(const UpCornerArgs &a_in, cudaStream_t s)
 {
-    const long long grid = (long long)B * a.K;
-    if (grid == 0) return cudaSuccess;
-    const size_t smem = nms_up_corner_smem(a.h, a.w, a.nbr, a.nbc, a.scr_rows, a.scr_cols);
-    k_nms_up_corner<<<(unsigned)grid, 128, smem, s>>>(a);
+    UpCornerArgs a = a_in;
+    const long long P = (long long)a.B * a.K;
+    if (P == 0) return cudaSuccess;
+    const size_t smem = nms_up_corner_smem(a.h, a.w, a.nbr, a.nbc, a.nst);
+    int dev = 0, sms = 0, occ = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nms_up_corner, kCornerThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    // bulk copies need 16-byte aligned, 16-byte multiple planes
+    a.bulk = ((size_t)a.h * a.w * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(a.conf) & 15) == 0;
+    const long long grid = std::min<long long>(P, (long long)occ * sms);
+    k_nms_up_corner<<<(unsigned)grid, kCornerThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -40,10 +40,12 @@ struct UpWinArgs {
 };
 size_t nms_up_win_smem(int h, int w, int H, int threads);
 
-// k_nms_up_corner (pf_corner.cu): exact slope-pruned fused upsample + 3x3 NMS.
+// k_nms_up_corner (pf_corner.cu): exact slope-pruned fused upsample + 3x3 NMS,
+// persistent, planes streamed by 1-D bulk copies.  Canonical bands only
+// (band b reads sources b-1, b: any integer upsample of a >= 2 wide axis).
 struct UpCornerArgs {
     const float *conf;   // low-res [B][C][h][w]
-    int C, K, h, w;
+    int B, C, K, h, w;
     int H, W;
     float thr;
     int cap;
@@ -52,12 +54,13 @@ struct UpCornerArgs {
     AxisTab rows, cols;                  // per output row / column
     const int4 *rband, *cband;           // bands: (first, last, src0, src1)
     const double *rdt, *cdt;             // per band: min t step between adjacent outputs
-    int nbr, nbc;                        // band counts
-    int scr_rows, scr_cols;              // fallback scratch tile (max band + 2)
-    const int2 *src_rband, *src_cband;   // per source row / column: range of bands reading it
+    int nbr, nbc;                        // band counts (h + 1, w + 1)
+    int nst;                             // plane stages in shared memory
+    int bulk;                            // set by the launcher: planes fetched by cp.async.bulk
 };
-size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int scr_rows, int scr_cols);
-cudaError_t launch_nms_up_corner(const UpCornerArgs &a, int B, cudaStream_t s);
+size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
+constexpr int kCornerStages = 2;
+cudaError_t launch_nms_up_corner(const UpCornerArgs &a, cudaStream_t s);
 cudaError_t configure_corner_kernels(int max_smem);
 cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s);
 cudaError_t launch_nms_plane(const float *conf, int B, int C, int K, int H, int W, float thr,

@@ -34,5 +34,6 @@ for r in rows:
 ti = sum(v[0] for v in agg.values()) or 1
 ts = sum(v[1] for v in agg.values()) or 1
 print(f"total warp-instructions {ti}, stall samples {ts}")
-for key, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+order = 0 if len(sys.argv) > 4 and sys.argv[4] == "inst" else 1
+for key, v in sorted(agg.items(), key=lambda kv: -kv[1][order])[:top]:
     print(f"{v[1]/ts*100:5.1f}% stall {v[0]/ti*100:5.1f}% inst  {key[0]}:{key[1]}  {v[2]}")
