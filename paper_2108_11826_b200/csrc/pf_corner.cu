@@ -57,7 +57,8 @@ namespace pf {
 
 constexpr float kNoise = 7.62939453125e-06f;   // 2^-17
 constexpr int kCornerThreads = 128;
-constexpr int kCornerCands = 1024;   // candidate pixels per plane kept in shared memory
+constexpr int kCornerCands = 512;    // candidate pixels per plane kept in shared memory
+constexpr int kCornerList = 1024;    // hot cells per plane kept in shared memory
 
 // Per band, fp32 copies of the axis weights the classification uses.
 struct BandT {
@@ -277,6 +278,35 @@ __device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands
     }
 }
 
+// One hot cell: classify; a normal cell pushes its surviving corner, a partial
+// cell its candidate pixels.
+__device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands &bd, const CandList &cl,
+                                             const float *S, int plane, int pr, int q)
+{
+    const int4 rb = bd.rb[pr], cb = bd.cb[q];
+    unsigned corners;
+    const unsigned ok = classify_cell(bd, S, a.w, a.nbr, a.nbc, pr, q, rb, cb, corners);
+    if (ok == 3u) {
+        while (corners) {
+            const int bit = __ffs(corners) - 1;
+            corners &= corners - 1u;
+            const int i = bit >> 1, j = bit & 1;
+            if (i == 1 && rb.x == rb.y) continue;     // a 1-row band's pixel is visited once
+            if (j == 1 && cb.x == cb.y) continue;
+            if (!corner_cross_ok(bd, S, a.w, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
+            push_cand(a, cl, S, plane, i ? rb.x : rb.y, j ? cb.x : cb.y);
+        }
+    } else {
+        partial_cands(a, bd, cl, S, plane, pr, q, ok);
+    }
+}
+
+// Exact value of output pixel (y, x); -inf off the grid (paf.py:87-93 pads).
+__device__ __forceinline__ float exact_value(const UpCornerArgs &a, const float *S, int y, int x)
+{
+    return up_val(S, a.w, ax_load(a.rows, y, a.H), ax_load(a.cols, x, a.W));
+}
+
 // ---- mbarrier + 1-D bulk copy (TMA) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -331,7 +361,7 @@ __host__ __device__ inline CornerLayout corner_layout(int h, int w, int nbr, int
     L.rt = o;     o += (size_t)nbr * sizeof(BandT);
     L.ct = o;     o += (size_t)nbc * sizeof(BandT);
     L.hot = o;    o += (size_t)(L.n_hw + 4) * sizeof(uint32_t);
-    L.list = o;   o += (size_t)((nbr * nbc + 7) & ~7) * sizeof(uint16_t);
+    L.list = o;   o += (size_t)kCornerList * sizeof(uint16_t);
     L.cand = o;   o += (size_t)kCornerCands * sizeof(uint32_t);
     L.total = (o + 15) & ~(size_t)15;
     return L;
@@ -384,7 +414,7 @@ k_nms_up_corner(const UpCornerArgs a)
     __shared__ int n_hot, n_cand;
     const CandList cl{cand, &n_cand, kCornerCands};
     const Bands bd{RB, CB, RT, CT};
-    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long P = (long long)a.B * a.K;
     const uint32_t plane_bytes = (uint32_t)hw * 4u;
 
@@ -456,10 +486,12 @@ k_nms_up_corner(const UpCornerArgs a)
                 if (j) c |= (row_word(hot, h, w, p - 1, j - 1) | row_word(hot, h, w, p, j - 1)) >> 31;
                 if (c) {
                     int slot = atomicAdd(&n_hot, __popc(c));
-                    const int base = p * nbc + (j << 5);
                     while (c) {
-                        list[slot++] = uint16_t(base + __ffs(c) - 1);
+                        const int q = (j << 5) + __ffs(c) - 1;
                         c &= c - 1u;
+                        if (slot < kCornerList) list[slot] = uint16_t(p * nbc + q);
+                        else process_cell(a, bd, cl, S, plane, p, q);    // list full: in place
+                        ++slot;
                     }
                 }
             }
@@ -468,36 +500,42 @@ k_nms_up_corner(const UpCornerArgs a)
 
         // ---- (C1) lane = hot cell: classify; normal cells push their surviving
         // corner, partial cells their candidate pixels
-        const int nh = n_hot;
+        const int nh = min(n_hot, kCornerList);
         for (int idx = threadIdx.x; idx < nh; idx += kCornerThreads) {
             const int cell = list[idx];
-            const int pr = cell / nbc, q = cell - pr * nbc;
-            const int4 rb = RB[pr], cb = CB[q];
-            unsigned corners;
-            const unsigned ok = classify_cell(bd, S, w, nbr, nbc, pr, q, rb, cb, corners);
-            if (ok == 3u) {
-                while (corners) {
-                    const int bit = __ffs(corners) - 1;
-                    corners &= corners - 1u;
-                    const int i = bit >> 1, j = bit & 1;
-                    if (i == 1 && rb.x == rb.y) continue;     // a 1-row band's pixel is visited once
-                    if (j == 1 && cb.x == cb.y) continue;
-                    if (!corner_cross_ok(bd, S, w, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
-                    push_cand(a, cl, S, plane, i ? rb.x : rb.y, j ? cb.x : cb.y);
-                }
-            } else {
-                partial_cands(a, bd, cl, S, plane, pr, q, ok);
-            }
+            const int pr = cell / nbc;
+            process_cell(a, bd, cl, S, plane, pr, cell - pr * nbc);
         }
         __syncthreads();
 
-        // ---- (C2) lane = candidate pixel: the exact 3x3 test
-        const int nc = min(n_cand, kCornerCands);
-        for (int e = threadIdx.x; e < nc; e += kCornerThreads) {
-            const uint32_t yx = cand[e];
-            const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
-            float v;
-            if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
+        // ---- (C2) the exact 3x3 test, 9 lanes per candidate (one pixel each),
+        // three candidates per warp, gathered by shuffles
+        {
+            const int nc = min(n_cand, kCornerCands);
+            const int grp = lane / 9, nb = lane - grp * 9;
+            const int src = min(grp, 2) * 9;
+            for (int base = warp * 3; base < nc; base += 3 * (kCornerThreads / kWarp)) {
+                const int ci = base + grp;
+                const bool act = grp < 3 && ci < nc;
+                int y = 0, x = 0;
+                float val = -INFINITY;
+                if (act) {
+                    const uint32_t yx = cand[ci];
+                    y = (int)(yx >> 16);
+                    x = (int)(yx & 0xffffu);
+                    val = exact_value(a, S, y + nb / 3 - 1, x + nb % 3 - 1);
+                }
+                float nv[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) nv[k] = __shfl_sync(0xffffffffu, val, src + k);
+                if (act && nb == 4) {
+                    const float v = nv[4];
+                    // paf.py:95-99: earlier neighbours strictly, later ones non-strictly
+                    if (v >= a.thr && v > nv[0] && v > nv[1] && v > nv[2] && v > nv[3] && v >= nv[5] &&
+                        v >= nv[6] && v >= nv[7] && v >= nv[8])
+                        emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
+                }
+            }
         }
         __syncthreads();                                     // stage + list free again
         if (threadIdx.x == 0) {
