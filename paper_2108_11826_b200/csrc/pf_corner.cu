@@ -231,16 +231,10 @@ struct CandList {
     int cap;
 };
 
-__device__ __forceinline__ void push_cand(const UpCornerArgs &a, const CandList &cl, const float *S, int plane,
-                                          int y, int x)
+__device__ __forceinline__ void push_cand(const CandList &cl, int y, int x)
 {
     const int slot = atomicAdd(cl.n, 1);
-    if (slot < cl.cap) {
-        cl.c[slot] = (uint32_t(y) << 16) | uint32_t(x);
-    } else {   // list full (pathological planes): test in place
-        float v;
-        if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
-    }
+    if (slot < cl.cap) cl.c[slot] = (uint32_t(y) << 16) | uint32_t(x);   // beyond: plane redone (slow path)
 }
 
 // Candidate pixels of a partial cell.  Rows restricted to the boundary rows
@@ -273,7 +267,7 @@ __device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands
                 const float e = sl_v(c, (float)__ldg(a.cols.omt + x), (float)__ldg(a.cols.t + x));
                 if (fabsf(e) * rdt > n && y != (e > 0.f ? rb.y : rb.x)) continue;
             }
-            push_cand(a, cl, S, plane, y, x);
+            push_cand(cl, y, x);
         }
     }
 }
@@ -294,7 +288,7 @@ __device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands 
             if (i == 1 && rb.x == rb.y) continue;     // a 1-row band's pixel is visited once
             if (j == 1 && cb.x == cb.y) continue;
             if (!corner_cross_ok(bd, S, a.w, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
-            push_cand(a, cl, S, plane, i ? rb.x : rb.y, j ? cb.x : cb.y);
+            push_cand(cl, i ? rb.x : rb.y, j ? cb.x : cb.y);
         }
     } else {
         partial_cands(a, bd, cl, S, plane, pr, q, ok);
@@ -395,7 +389,33 @@ __device__ __forceinline__ uint32_t row_word(const uint32_t *hot, int h, int w, 
     return v;
 }
 
-__global__ void __launch_bounds__(kCornerThreads, 4)
+// Slow path for a plane whose hot cells or candidates overflowed the shared
+// lists: forget its peaks and exactly test every pixel of every hot cell.
+__device__ __noinline__ void redo_plane(const UpCornerArgs &a, const Bands &bd, const float *S,
+                                        const uint32_t *hot, int plane)
+{
+    if (threadIdx.x == 0) a.counts[plane] = 0;
+    __syncthreads();
+    const int h = a.h, w = a.w, nwc = (w + 32) >> 5;
+    for (int t = threadIdx.x; t < (h + 1) * nwc; t += kCornerThreads) {
+        const int p = t / nwc, j = t - p * nwc;
+        const uint32_t m = row_word(hot, h, w, p - 1, j) | row_word(hot, h, w, p, j);
+        uint32_t c = m | (m << 1);
+        if (j) c |= (row_word(hot, h, w, p - 1, j - 1) | row_word(hot, h, w, p, j - 1)) >> 31;
+        while (c) {
+            const int q = (j << 5) + __ffs(c) - 1;
+            c &= c - 1u;
+            const int4 rb = bd.rb[p], cb = bd.cb[q];
+            for (int y = rb.x; y <= rb.y; ++y)
+                for (int x = cb.x; x <= cb.y; ++x) {
+                    float v;
+                    if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
+                }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kCornerThreads, 5)
 k_nms_up_corner(const UpCornerArgs a)
 {
     extern __shared__ __align__(128) unsigned char smc[];
@@ -489,8 +509,7 @@ k_nms_up_corner(const UpCornerArgs a)
                     while (c) {
                         const int q = (j << 5) + __ffs(c) - 1;
                         c &= c - 1u;
-                        if (slot < kCornerList) list[slot] = uint16_t(p * nbc + q);
-                        else process_cell(a, bd, cl, S, plane, p, q);    // list full: in place
+                        if (slot < kCornerList) list[slot] = uint16_t(p * nbc + q);   // beyond: slow path
                         ++slot;
                     }
                 }
@@ -536,6 +555,10 @@ k_nms_up_corner(const UpCornerArgs a)
                         emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
                 }
             }
+        }
+        __syncthreads();
+        if (n_hot > kCornerList || n_cand > kCornerCands) {    // CTA-uniform: a list overflowed
+            redo_plane(a, bd, S, hot, plane);
         }
         __syncthreads();                                     // stage + list free again
         if (threadIdx.x == 0) {

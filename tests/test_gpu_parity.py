@@ -181,6 +181,26 @@ def test_random_fields(topo):
     e.close()
 
 
+def test_corner_kernel_overflow_and_nonfinite(eng, topo):
+    """Mode U corner kernel edge cases: an all-hot smooth frame (hot cells beyond
+    the shared list -> whole-plane slow path), a noise part map (candidate list
+    overflow), NaN / +inf / -inf sources; Mode R sees the same non-finite maps."""
+    scenes = [pf.procedural_scene(41, s, 656, 368, SP) for s in range(4)]
+    conf, paf = render(scenes, topo)
+    K = topo.n_keypoints
+    yy, xx = np.mgrid[0:conf.shape[2], 0:conf.shape[3]].astype(np.float32)
+    conf[0, :K] = (0.55 + 0.35 * np.sin(xx / 3.0 + np.arange(K)[:, None, None]) * np.cos(yy / 4.0)).astype(np.float32)
+    rng = np.random.default_rng(5)
+    conf[1, 3] = rng.random(conf.shape[2:]).astype(np.float32)
+    conf[1, 7] = np.round(rng.random(conf.shape[2:]) * 4).astype(np.float32) / 4   # ties
+    for k, (i, j, v) in enumerate([(10, 20, np.nan), (11, 20, np.inf), (30, 40, -np.inf), (0, 0, np.nan),
+                                   (45, 81, np.inf), (20, 60, np.nan)]):
+        conf[2, k % K, i, j] = v
+        conf[3, (3 * k) % K, (i + 7) % conf.shape[2], (j + 11) % conf.shape[3]] = v
+    for up in (8, 1):
+        assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
+
+
 def test_blur_paths(eng, topo):
     scenes = [pf.procedural_scene(29, s, 656, 368, SP) for s in range(2)]
     conf, paf = render(scenes, topo)
