@@ -34,11 +34,14 @@ struct AxisCache {
     std::vector<int4> bands;                    // (first, last, src0, src1) per band
     std::vector<double> band_dt;                // min t step inside each band (inf if 1 wide)
     int max_band = 0;
+    double min_step = 0.0;                      // min t distance of adjacent outputs off the border bands
     bool canonical = false;                     // band b reads sources (b-1, b) clipped: b = 0..in_n
     int4 *d_bands = nullptr;
     double *d_band_dt = nullptr;
+    BandT *d_bandt = nullptr;
     int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr, *d_gend = nullptr;
     double2 *d_tw = nullptr;
+    AxisRec *d_rec = nullptr;
     double *d_t = nullptr, *d_omt = nullptr;
     AxisTab dev() const { return AxisTab{d_i0, d_i1, d_t, d_omt}; }
 };
@@ -76,6 +79,14 @@ void fill_axis(AxisCache &a, int in_n, int out_n)
         a.max_band = std::max(a.max_band, e - o + 1);
     }
     a.canonical = (int)a.bands.size() == in_n + 1 && in_n >= 2;
+    // adjacent outputs o, o+1 in interior bands: t[o+1] - t[o] inside a band,
+    // (1 - t[o]) + t[o+1] across a band boundary (k_nms_up_corner chain_pruned)
+    a.min_step = 1e300;
+    for (size_t b = 1; b + 1 < a.bands.size(); ++b) {
+        const int4 B = a.bands[b];
+        for (int u = B.x; u < B.y; ++u) a.min_step = std::min(a.min_step, a.t[u + 1] - a.t[u]);
+        if (b + 2 < a.bands.size()) a.min_step = std::min(a.min_step, a.omt[B.y] + a.t[B.y + 1]);
+    }
     for (int b = 0; a.canonical && b <= in_n; ++b)
         a.canonical = a.bands[b].z == std::max(b - 1, 0) && a.bands[b].w == std::min(b, in_n - 1);
     a.first_out.assign(in_n, 0x3fffffff);
@@ -162,6 +173,8 @@ struct pf_ctx {
     int materialise = 0;
     int generic_fused = 0;
     int win_variant = 4;
+    int no_chain = 0;
+    int corner_warp_rows = 0;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double kernel_ms[PF_N_KERNELS] = {0};
@@ -275,11 +288,36 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
             for (int o = 0; o < out_n; ++o) tw[o] = make_double2(a.t[o], a.omt[o]);
             CU(dev_alloc(&a.d_tw, out_n));
             CU(cudaMemcpy(a.d_tw, tw.data(), out_n * sizeof(double2), cudaMemcpyHostToDevice));
+            std::vector<AxisRec> rec(out_n);
+            for (int o = 0; o < out_n; ++o) {
+                rec[o].i01 = a.i0[o] | (a.i1[o] << 16);
+                rec[o].pad = 0;
+                rec[o].t = a.t[o];
+            }
+            CU(dev_alloc(&a.d_rec, out_n));
+            CU(cudaMemcpy(a.d_rec, rec.data(), out_n * sizeof(AxisRec), cudaMemcpyHostToDevice));
         }
         CU(dev_alloc(&a.d_bands, a.bands.size()));
         CU(cudaMemcpy(a.d_bands, a.bands.data(), a.bands.size() * sizeof(int4), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_band_dt, a.band_dt.size()));
         CU(cudaMemcpy(a.d_band_dt, a.band_dt.data(), a.band_dt.size() * sizeof(double), cudaMemcpyHostToDevice));
+        {
+            // the same fp32 roundings as pf_corner.cu fill_band (double -> float is RN on both sides)
+            std::vector<BandT> bt(a.bands.size());
+            for (size_t b = 0; b < a.bands.size(); ++b) {
+                const int f = a.bands[b].x, l = a.bands[b].y;
+                bt[b].omt_f = (float)a.omt[f];
+                bt[b].t_f = (float)a.t[f];
+                bt[b].omt_l = (float)a.omt[l];
+                bt[b].t_l = (float)a.t[l];
+                bt[b].s_l = (float)(a.t[l] - a.t[std::max(l - 1, f)]);
+                bt[b].s_f = (float)(a.t[std::min(f + 1, l)] - a.t[f]);
+                bt[b].dt = (float)a.band_dt[b];
+                bt[b].pad = 0.f;
+            }
+            CU(dev_alloc(&a.d_bandt, bt.size()));
+            CU(cudaMemcpy(a.d_bandt, bt.data(), bt.size() * sizeof(BandT), cudaMemcpyHostToDevice));
+        }
         CU(dev_alloc(&a.d_gend, out_n));
         CU(cudaMemcpy(a.d_gend, a.gend.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_first, in_n));
@@ -452,6 +490,10 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.rdt = rows->d_band_dt; a.cdt = cols->d_band_dt;
         a.nbr = (int)rows->bands.size(); a.nbc = (int)cols->bands.size();
         a.nst = kCornerStages;
+        a.chain = rows->min_step >= 0.03125 && cols->min_step >= 0.03125 && !ctx->no_chain;
+        a.warp_rows = ctx->corner_warp_rows == 1;
+        a.variant = ctx->corner_warp_rows == 2 ? 1 : 0;
+        a.rbt = rows->d_bandt; a.cbt = cols->d_bandt;
         KernelTimer kt(ctx, kNmsUpCorner);
         CU(launch_nms_up_corner(a, s));
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
@@ -529,11 +571,23 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.rows = rows->dev(); a.cols = cols->dev();
         a.ry = (double)h / (double)H;
         a.rx = (double)w / (double)W;
+        a.rrec = rows->d_rec; a.crec = cols->d_rec;
     }
     a.stride_eff = stride / up;
     a.n_samples = p->n_samples;
     a.dot_thr = p->sample_dot_threshold;
     a.good_min = p->good_fraction_min;
+    {
+        // paf.py:160-162 gate good >= good_min with good = n_good / n (IEEE
+        // double division, the same on host and device): the least passing
+        // n_good lets the kernel drop a pair as soon as it cannot pass
+        const volatile double nd = (double)p->n_samples;
+        a.good_need = p->n_samples + 1;
+        for (int g = 0; g <= p->n_samples; ++g) {
+            const volatile double q = (double)g / nd;
+            if (q >= p->good_fraction_min) { a.good_need = g; break; }
+        }
+    }
     a.min_score = p->min_human_score;
     a.min_parts = p->min_parts;
     a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
@@ -780,7 +834,8 @@ void pf_destroy(pf_ctx *ctx)
         cudaFree(kv.second.d_i0); cudaFree(kv.second.d_i1);
         cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
         cudaFree(kv.second.d_first); cudaFree(kv.second.d_last); cudaFree(kv.second.d_gend); cudaFree(kv.second.d_tw);
-        cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt);
+        cudaFree(kv.second.d_rec);
+        cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt); cudaFree(kv.second.d_bandt);
     }
     for (auto &p : ctx->pending) { ctx->ev_pool.push_back(p.second.first); ctx->ev_pool.push_back(p.second.second); }
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -866,6 +921,8 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_MATERIALISE: ctx->materialise = value ? 1 : 0; return PF_OK;
     case PF_OPT_GENERIC_FUSED: ctx->generic_fused = value ? 1 : 0; return PF_OK;
     case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 4) ? value : 4; return PF_OK;
+    case PF_OPT_NO_CHAIN: ctx->no_chain = value ? 1 : 0; return PF_OK;
+    case PF_OPT_CORNER_WARP_ROWS: ctx->corner_warp_rows = (value >= 0 && value <= 2) ? value : 2; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }

@@ -40,6 +40,13 @@ struct UpWinArgs {
 };
 size_t nms_up_win_smem(int h, int w, int H, int threads);
 
+// Per band, fp32 copies of the axis weights the corner kernels' classification
+// uses (built on the host for k_nms_up_corner_g, in-kernel for the others).
+struct BandT {
+    float omt_f, t_f, omt_l, t_l;   // (1 - t), t at the band's first and last output
+    float s_l, s_f, dt, pad;        // t step into the last output, out of the first; min step
+};
+
 // k_nms_up_corner (pf_corner.cu): exact slope-pruned fused upsample + 3x3 NMS,
 // persistent, planes streamed by 1-D bulk copies.  Canonical bands only
 // (band b reads sources b-1, b: any integer upsample of a >= 2 wide axis).
@@ -57,6 +64,10 @@ struct UpCornerArgs {
     int nbr, nbc;                        // band counts (h + 1, w + 1)
     int nst;                             // plane stages in shared memory
     int bulk;                            // set by the launcher: planes fetched by cp.async.bulk
+    int chain;                           // chain pre-filter allowed (output t steps >= 2^-5)
+    int warp_rows;                       // k_nms_up_corner_w (warp-autonomous band rows)
+    int variant;                         // 0: CTA per plane (smem stages), 1: warp per plane (global)
+    const BandT *rbt, *cbt;              // per band fp32 weights (variant 1)
 };
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
 constexpr int kCornerStages = 2;
@@ -70,6 +81,14 @@ cudaError_t launch_nms_up(const UpArgs &a, int B, size_t smem, cudaStream_t s);
 cudaError_t configure_nms_kernels(int max_smem);
 
 // pf_parse.cu
+// One output coordinate of operators.bilinear_resize packed for a single
+// 16-byte load: i0 | i1 << 16, t (1 - t is recomputed: the host's omt is the
+// same single rounded subtraction).
+struct __align__(16) AxisRec {
+    int32_t i01;
+    int32_t pad;
+    double t;
+};
 struct ParseArgs {
     Topo topo;
     const float *paf;
@@ -100,6 +119,8 @@ struct ParseArgs {
     double *dbg_conn_d;
     void *cand_spill;    // [frames][cap_cands - kCandSmem] candidate records (crowded frames)
     double ry, rx;       // h / H, w / W: operators.py:88-89 ratios (up > 1)
+    const AxisRec *rrec, *crec;   // packed operators.py:86-96 axis records (up > 1)
+    int good_need;       // least n_good with fl(n_good / n) >= good_min (n + 1: none)
 };
 constexpr int kCandSmem = 256;       // gated candidates kept in shared memory per frame
 constexpr int kParseThreads = 128;   // k_parse_frames CTA size

@@ -32,6 +32,8 @@
 
 namespace pf {
 
+constexpr int kParseTTab = 64;     // sample positions kept in shared memory
+
 struct Cand {
     double score;
     uint32_t ab;     // id_a << 16 | id_b ; bit 31 = accepted
@@ -56,31 +58,29 @@ struct CandStore {
     __device__ __forceinline__ Cand &operator[](int i) const { return i < kCandSmem ? s[i] : g[i - kCandSmem]; }
 };
 
-__device__ __forceinline__ double sample_paf(const ParseArgs &a, const float *__restrict__ ch,
-                                             int ci, int cj)
+// PAF value pair at parse-grid cell (ci, cj): the feature grid itself
+// (up == 1), or the x`up` bilinear value of operators.py:102-107 re-derived
+// from the low-res PAF with one packed axis record per axis.
+__device__ __forceinline__ void sample_pair(const ParseArgs &a, const float *__restrict__ chx,
+                                            const float *__restrict__ chy, int ci, int cj, double &px, double &py)
 {
-    if (a.up == 1) return (double)__ldg(ch + (size_t)ci * a.w + cj);
-    // axis parameters recomputed in registers (no dependent table loads)
-    int i0, i1, j0, j1;
-    double ty, omty, tx, omtx;
-    axis_coord(ci, a.ry, a.h, i0, i1, ty, omty);
-    axis_coord(cj, a.rx, a.w, j0, j1, tx, omtx);
-    const float v = bilerp(__ldg(ch + (size_t)i0 * a.w + j0), __ldg(ch + (size_t)i0 * a.w + j1),
-                           __ldg(ch + (size_t)i1 * a.w + j0), __ldg(ch + (size_t)i1 * a.w + j1),
-                           tx, omtx, ty, omty);
-    return (double)v;
-}
-
-// One sample of score_limb (paf.py:138-143): nearest cell at t = u/(n-1),
-// dot of the PAF vector with the unit limb direction.
-__device__ __forceinline__ double limb_sample(const ParseArgs &a, const float *chx, const float *chy,
-                                              int ai, int aj, int di, int dj, double vx, double vy,
-                                              int u, double den)
-{
-    const double t = __ddiv_rn((double)u, den);
-    const int ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
-    const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
-    return dadd(dmul(sample_paf(a, chx, ci, cj), vx), dmul(sample_paf(a, chy, ci, cj), vy));
+    if (a.up == 1) {
+        const size_t o = (size_t)ci * a.w + cj;
+        px = (double)__ldg(chx + o);
+        py = (double)__ldg(chy + o);
+        return;
+    }
+    const int4 ry = __ldg(reinterpret_cast<const int4 *>(a.rrec + ci));
+    const int4 rx = __ldg(reinterpret_cast<const int4 *>(a.crec + cj));
+    const int i0 = ry.x & 0xffff, i1 = ry.x >> 16, j0 = rx.x & 0xffff, j1 = rx.x >> 16;
+    const double ty = __hiloint2double(ry.w, ry.z), tx = __hiloint2double(rx.w, rx.z);
+    const double omty = __dsub_rn(1.0, ty), omtx = __dsub_rn(1.0, tx);
+    const size_t o00 = (size_t)i0 * a.w + j0, o01 = (size_t)i0 * a.w + j1;
+    const size_t o10 = (size_t)i1 * a.w + j0, o11 = (size_t)i1 * a.w + j1;
+    const float x00 = __ldg(chx + o00), x01 = __ldg(chx + o01), x10 = __ldg(chx + o10), x11 = __ldg(chx + o11);
+    const float y00 = __ldg(chy + o00), y01 = __ldg(chy + o01), y10 = __ldg(chy + o10), y11 = __ldg(chy + o11);
+    px = (double)bilerp(x00, x01, x10, x11, tx, omtx, ty, omty);
+    py = (double)bilerp(y00, y01, y10, y11, tx, omtx, ty, omty);
 }
 
 // CPython 3.12 builtin sum() over floats starting from int 0 (Neumaier).
@@ -108,6 +108,9 @@ k_parse_frames(const ParseArgs a)
     __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base;
     __shared__ int8_t s_la[PF_MAX_LIMBS], s_lb[PF_MAX_LIMBS];
     __shared__ int16_t s_cx[PF_MAX_LIMBS], s_cy[PF_MAX_LIMBS];
+    __shared__ double s_t[kParseTTab];          // u / (n - 1), paf.py:139
+    for (int u = tid; u < kParseTTab && u < a.n_samples; u += nthr)
+        s_t[u] = __ddiv_rn((double)u, (double)(a.n_samples - 1));
     for (int l = tid; l < L; l += nthr) {
         s_la[l] = a.topo.la[l]; s_lb[l] = a.topo.lb[l];
         s_cx[l] = a.topo.cx[l]; s_cy[l] = a.topo.cy[l];
@@ -201,68 +204,57 @@ k_parse_frames(const ParseArgs a)
         if (tid == 0) a.dbg_npeaks[gframe] = P;
     }
 
-    // ---- 3. line integral: a lane group per pair, a lane per sample ----
+    // ---- 3. line integral: a lane per (limb, a, b) pair (paf.py:149-165).
+    // The lane walks the samples in order (paf.py:138-145), so the fp64
+    // running total is the reference's `total += d` exactly, and it leaves a
+    // pair as soon as the pair can no longer pass the gate (more failing
+    // samples than n - good_need): such pairs are never candidates.
     const float *paf_f = a.paf + (size_t)b * (2 * L) * a.h * a.w;
     const int n_pairs = s_pp[L];
     const int n = a.n_samples;
-    const double den = (double)(n - 1);
-    const int G = n <= 32 ? n : 32;                       // lanes per pair (one per sample)
-    const int gpw = kWarp / G;                            // pairs per warp pass
-    const int grp = min(lane / G, gpw - 1), gl = lane - grp * G;
-    const bool in_group = lane < gpw * G;
-    const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
-    int l_cur = 0;                                        // limb search resumes (p grows)
-    for (int p0 = warp * gpw; p0 < n_pairs; p0 += n_warps * gpw) {
-        const int p = p0 + grp;
-        bool live = in_group && p < n_pairs;
-        int l = l_cur, ia = 0, ib = 0, ai = 0, aj = 0, di = 0, dj = 0;
-        double vx = 0.0, vy = 0.0;
-        if (live) {
+    const int max_fail = n - a.good_need;            // < 0: nothing can pass
+    if (max_fail >= 0) {
+        const double den = (double)(n - 1);
+        for (int p = tid; p < n_pairs; p += nthr) {
+            int l = 0;
             while (p >= s_pp[l + 1]) ++l;
-            l_cur = l;
             const int pa_part = s_la[l], pb_part = s_lb[l];
             const int nb = s_base[pb_part + 1] - s_base[pb_part];
             const int local = p - s_pp[l];
-            ia = s_base[pa_part] + local / nb;
-            ib = s_base[pb_part] + local % nb;
-            ai = int(p_cell[ia] >> 16); aj = int(p_cell[ia] & 0xffff);
-            const int bi = int(p_cell[ib] >> 16), bj = int(p_cell[ib] & 0xffff);
-            di = bi - ai; dj = bj - aj;
-            live = (di | dj) != 0;          // coincident cells score (0, 0): never gated
-            if (live) {
-                const double norm = __dsqrt_rn((double)(di * di + dj * dj));
-                vx = __ddiv_rn((double)dj, norm);
-                vy = __ddiv_rn((double)di, norm);
-            }
-        }
-        const float *chx = paf_f + (size_t)s_cx[l] * a.h * a.w;
-        const float *chy = paf_f + (size_t)s_cy[l] * a.h * a.w;
-        double total = 0.0;
-        int ngood = 0;
-        if (n <= 32) {
-            double d = 0.0;
-            if (live && gl < n) d = limb_sample(a, chx, chy, ai, aj, di, dj, vx, vy, gl, den);
-            ngood = __popc(__ballot_sync(0xffffffffu, live && gl < n && d >= a.dot_thr) & gmask);
-            for (int u = 0; u < n; ++u) total = dadd(total, __shfl_sync(0xffffffffu, d, grp * G + u));
-        } else if (live && gl == 0) {       // long line integrals: one lane, sequential
+            const int qa = local / nb;
+            const int ia = s_base[pa_part] + qa;
+            const int ib = s_base[pb_part] + (local - qa * nb);
+            const int ai = int(p_cell[ia] >> 16), aj = int(p_cell[ia] & 0xffff);
+            const int di = int(p_cell[ib] >> 16) - ai, dj = int(p_cell[ib] & 0xffff) - aj;
+            if ((di | dj) == 0) continue;                 // coincident cells score (0, 0): never gated
+            const double norm = __dsqrt_rn((double)(di * di + dj * dj));
+            const double vx = __ddiv_rn((double)dj, norm);
+            const double vy = __ddiv_rn((double)di, norm);
+            const float *chx = paf_f + (size_t)s_cx[l] * a.h * a.w;
+            const float *chy = paf_f + (size_t)s_cy[l] * a.h * a.w;
+            double total = 0.0;
+            int ngood = 0, nfail = 0;
             for (int u = 0; u < n; ++u) {
-                const double d = limb_sample(a, chx, chy, ai, aj, di, dj, vx, vy, u, den);
+                const double t = u < kParseTTab ? s_t[u] : __ddiv_rn((double)u, den);
+                const int ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
+                const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
+                double px, py;
+                sample_pair(a, chx, chy, ci, cj, px, py);
+                const double d = dadd(dmul(px, vx), dmul(py, vy));
                 total = dadd(total, d);
-                ngood += (d >= a.dot_thr);
+                if (d >= a.dot_thr) ++ngood;
+                else if (++nfail > max_fail) break;
             }
-        }
-        if (live && gl == 0) {
+            if (nfail > max_fail) continue;
             const double score = __ddiv_rn(total, (double)n);
-            const double good = __ddiv_rn((double)ngood, (double)n);
-            if (good >= a.good_min && score > 0.0) {
-                const int slot = atomicAdd(&s_ncand, 1);
-                if (slot < a.cap_cands) {
-                    Cand c;
-                    c.score = score;
-                    c.ab = (uint32_t(ia) << 16) | uint32_t(ib);
-                    c.lg = (uint32_t(l) << 24) | uint32_t(ngood);
-                    cand[slot] = c;
-                }
+            if (!(score > 0.0)) continue;                  // paf.py:162 (good already passed)
+            const int slot = atomicAdd(&s_ncand, 1);
+            if (slot < a.cap_cands) {
+                Cand c;
+                c.score = score;
+                c.ab = (uint32_t(ia) << 16) | uint32_t(ib);
+                c.lg = (uint32_t(l) << 24) | uint32_t(ngood);
+                cand[slot] = c;
             }
         }
     }

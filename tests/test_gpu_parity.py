@@ -310,3 +310,60 @@ def test_capacity_errors_are_loud(topo):
     with pytest.raises(pf.CapacityError):
         e.parse_arrays(conf, paf, 8, pf.ParserParams())
     e.close()
+
+
+def _chain_fields(rng, K, h, w):
+    """Adversarial part maps for the corner kernel's chain pre-filter: ramps
+    (every interior cell chain-prunable), slopes near the 2^-16 M margin,
+    exact plateaus / ties, saddles, checkerboards, huge and tiny magnitudes."""
+    yy, xx = np.mgrid[0:h, 0:w].astype(np.float64)
+    f = []
+    f.append(0.2 + 0.7 * xx / w)                                          # ramp right
+    f.append(0.9 - 0.7 * yy / h)                                          # ramp up
+    f.append(0.5 + 1e-5 * (xx - w / 2) ** 2 / w)                          # slopes ~ the margin
+    f.append(0.5 + 2e-6 * np.sin(xx / 2) * np.cos(yy / 3))                # below the margin: exact path
+    f.append(np.round(rng.random((h, w)) * 3) / 3 * 0.8 + 0.1)           # plateaus / ties
+    f.append(0.5 + 0.3 * ((xx - w / 2) ** 2 - (yy - h / 2) ** 2) / (w * w))   # saddle
+    f.append(0.4 + 0.2 * ((np.arange(h)[:, None] + np.arange(w)[None, :]) % 2))   # checkerboard
+    f.append((0.5 + 0.4 * np.sin(xx / 4) * np.sin(yy / 5)) * 1e30)       # huge
+    f.append((0.5 + 0.4 * np.sin(xx / 4) * np.sin(yy / 5)) * 1e-30)      # tiny (cold at thr 0.1)
+    f.append(0.5 + 0.4 * np.exp(-((xx - 20.5) ** 2 + (yy - 10.25) ** 2) / 8)
+             + 0.4 * np.exp(-((xx - 23.5) ** 2 + (yy - 10.25) ** 2) / 8))   # two close blobs: ridge
+    f.append(np.full((h, w), 0.5))                                        # flat
+    out = np.zeros((K, h, w), np.float32)
+    for k in range(K):
+        out[k] = f[k % len(f)]
+    return out
+
+
+@pytest.mark.parametrize("up", [2, 3, 8, 16])
+def test_corner_chain_prefilter_is_exact(topo, up):
+    """The chain pre-filter only removes cells that provably hold no peak: the
+    corner kernel with and without it gives identical peaks, and both equal
+    the oracle."""
+    rng = np.random.default_rng(2024 + up)
+    K = topo.n_keypoints
+    h, w = 23, 41
+    conf = np.zeros((3, K + 1, h, w), np.float32)
+    for f in range(3):
+        conf[f, :K] = _chain_fields(rng, K, h, w)
+        conf[f, :K] = np.roll(conf[f, :K], f * 5, axis=0)
+    conf[2, :K] = conf[2, :K] * np.float32(0.99) + rng.random((K, h, w)).astype(np.float32) * np.float32(0.01)
+    paf = np.zeros((3, 38, h, w), np.float32)      # peaks are the subject; no limbs
+    for thr in (0.1, 0.0):
+        params = pf.ParserParams(upsample=up, conf_threshold=thr)
+        e1 = pf.PafParser(topo, debug=True)
+        runs = []
+        for layout, no_chain in ((2, 0), (2, 1), (1, 0), (0, 1), (0, 0)):
+            # 2: warp per plane (default), 1: warp band rows, 0: CTA phases
+            e1.ctx.set_option(pf._native.PF_OPT_CORNER_WARP_ROWS, layout)
+            e1.ctx.set_option(pf._native.PF_OPT_NO_CHAIN, no_chain)
+            e1.parse_arrays(conf, paf, 48, params)      # stride divisible by every tested factor
+            runs.append([e1.peaks(f) for f in range(3)])
+        e1.close()
+        with_chain = runs[0]
+        assert all(r == with_chain for r in runs)
+        if thr > 0 and up in (3, 8):
+            for f in range(3):
+                want = oracle_run(conf[f], paf[f], topo, params, 48)
+                assert with_chain[f] == want.peaks, f"frame {f}"
