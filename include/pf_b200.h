@@ -77,9 +77,9 @@ typedef struct pf_params {
  * PF_ERR_CAPACITY for the call with the offending frame index. */
 typedef struct pf_caps {
     int32_t max_peaks_per_part;    /* default 128 */
-    int32_t max_peaks_per_frame;   /* default 1024 */
+    int32_t max_peaks_per_frame;   /* default 256 (automatic caps grow on demand) */
     int32_t max_candidates;        /* gated candidate pairs per frame, default 4096 */
-    int32_t max_humans_per_frame;  /* builders per frame before filtering, default 256 */
+    int32_t max_humans_per_frame;  /* builders per frame before filtering, default 64 */
     int32_t chunk_frames;          /* frames per internal launch chunk, default 8192 */
     int32_t max_humans_total;      /* output pool per call, default 64 * batch */
 } pf_caps;

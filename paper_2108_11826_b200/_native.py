@@ -16,7 +16,8 @@ import numpy as np
 from .errors import CapacityError, ConfigError, ContractError, DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpf_b200.so")
+# PF_B200_LIB: load another build of the same sources (A/B of build variants)
+LIB_PATH = os.environ.get("PF_B200_LIB") or os.path.join(_HERE, "libpf_b200.so")
 
 PF_OK, PF_ERR_CONFIG, PF_ERR_CONTRACT, PF_ERR_CAPACITY, PF_ERR_CUDA = 0, 1, 2, 3, 4
 PF_MAX_KEYPOINTS, PF_MAX_LIMBS = 32, 64

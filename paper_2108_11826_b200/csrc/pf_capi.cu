@@ -753,9 +753,9 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
     // a replay of the call) when a frame needs more; explicit caps are fixed
     int auto_caps = 0;
     if (c.max_peaks_per_part <= 0) { c.max_peaks_per_part = 128; auto_caps |= 1 << kCapPart; }
-    if (c.max_peaks_per_frame <= 0) { c.max_peaks_per_frame = 512; auto_caps |= 1 << kCapFrame; }
+    if (c.max_peaks_per_frame <= 0) { c.max_peaks_per_frame = 256; auto_caps |= 1 << kCapFrame; }
     if (c.max_candidates <= 0) { c.max_candidates = 4096; auto_caps |= 1 << kCapCands; }
-    if (c.max_humans_per_frame <= 0) { c.max_humans_per_frame = 128; auto_caps |= 1 << kCapHumans; }
+    if (c.max_humans_per_frame <= 0) { c.max_humans_per_frame = 64; auto_caps |= 1 << kCapHumans; }
     if (c.max_humans_total <= 0) auto_caps |= 1 << kCapPool;
     if (c.chunk_frames <= 0) c.chunk_frames = 8192;
     // bitonic sort over the candidate store needs a power of two

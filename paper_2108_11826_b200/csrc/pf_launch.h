@@ -122,8 +122,14 @@ struct ParseArgs {
     const AxisRec *rrec, *crec;   // packed operators.py:86-96 axis records (up > 1)
     int good_need;       // least n_good with fl(n_good / n) >= good_min (n + 1: none)
 };
-constexpr int kCandSmem = 256;       // gated candidates kept in shared memory per frame
-constexpr int kParseThreads = 128;   // k_parse_frames CTA size
+#ifndef PF_CAND_SMEM
+#define PF_CAND_SMEM 256
+#endif
+constexpr int kCandSmem = PF_CAND_SMEM;   // gated candidates kept in shared memory per frame
+#ifndef PF_PARSE_THREADS
+#define PF_PARSE_THREADS 128
+#endif
+constexpr int kParseThreads = PF_PARSE_THREADS;   // k_parse_frames CTA size
 size_t cand_spill_bytes_per_frame(int cap_cands);
 enum { kCapPart = 1, kCapFrame = 2, kCapCands = 3, kCapHumans = 4, kCapPool = 5 };
 size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps);

@@ -60,27 +60,47 @@ struct CandStore {
 
 // PAF value pair at parse-grid cell (ci, cj): the feature grid itself
 // (up == 1), or the x`up` bilinear value of operators.py:102-107 re-derived
-// from the low-res PAF with one packed axis record per axis.
-__device__ __forceinline__ void sample_pair(const ParseArgs &a, const float *__restrict__ chx,
-                                            const float *__restrict__ chy, int ci, int cj, double &px, double &py)
+// from the low-res PAF with one packed axis record per axis.  Loads (fetch)
+// and arithmetic (finish) are separate steps; software-pipelining the next
+// sample's loads was measured slower (registers -> residency).
+struct SampleRaw {
+    float x00, x01, x10, x11, y00, y01, y10, y11;
+    double tx, ty;
+};
+
+__device__ __forceinline__ void fetch_sample(const ParseArgs &a, const float *__restrict__ chx,
+                                             const float *__restrict__ chy, int ci, int cj, SampleRaw &r)
 {
     if (a.up == 1) {
         const size_t o = (size_t)ci * a.w + cj;
-        px = (double)__ldg(chx + o);
-        py = (double)__ldg(chy + o);
+        r.x00 = __ldg(chx + o);
+        r.y00 = __ldg(chy + o);
         return;
     }
     const int4 ry = __ldg(reinterpret_cast<const int4 *>(a.rrec + ci));
     const int4 rx = __ldg(reinterpret_cast<const int4 *>(a.crec + cj));
     const int i0 = ry.x & 0xffff, i1 = ry.x >> 16, j0 = rx.x & 0xffff, j1 = rx.x >> 16;
-    const double ty = __hiloint2double(ry.w, ry.z), tx = __hiloint2double(rx.w, rx.z);
-    const double omty = __dsub_rn(1.0, ty), omtx = __dsub_rn(1.0, tx);
+    r.ty = __hiloint2double(ry.w, ry.z);
+    r.tx = __hiloint2double(rx.w, rx.z);
     const size_t o00 = (size_t)i0 * a.w + j0, o01 = (size_t)i0 * a.w + j1;
     const size_t o10 = (size_t)i1 * a.w + j0, o11 = (size_t)i1 * a.w + j1;
-    const float x00 = __ldg(chx + o00), x01 = __ldg(chx + o01), x10 = __ldg(chx + o10), x11 = __ldg(chx + o11);
-    const float y00 = __ldg(chy + o00), y01 = __ldg(chy + o01), y10 = __ldg(chy + o10), y11 = __ldg(chy + o11);
-    px = (double)bilerp(x00, x01, x10, x11, tx, omtx, ty, omty);
-    py = (double)bilerp(y00, y01, y10, y11, tx, omtx, ty, omty);
+    r.x00 = __ldg(chx + o00); r.x01 = __ldg(chx + o01); r.x10 = __ldg(chx + o10); r.x11 = __ldg(chx + o11);
+    r.y00 = __ldg(chy + o00); r.y01 = __ldg(chy + o01); r.y10 = __ldg(chy + o10); r.y11 = __ldg(chy + o11);
+}
+
+// dot of the sampled PAF vector with the unit limb direction (paf.py:142-143)
+__device__ __forceinline__ double finish_sample(const ParseArgs &a, const SampleRaw &r, double vx, double vy)
+{
+    double px, py;
+    if (a.up == 1) {
+        px = (double)r.x00;
+        py = (double)r.y00;
+    } else {
+        const double omty = __dsub_rn(1.0, r.ty), omtx = __dsub_rn(1.0, r.tx);
+        px = (double)bilerp(r.x00, r.x01, r.x10, r.x11, r.tx, omtx, r.ty, omty);
+        py = (double)bilerp(r.y00, r.y01, r.y10, r.y11, r.tx, omtx, r.ty, omty);
+    }
+    return dadd(dmul(px, vx), dmul(py, vy));
 }
 
 // CPython 3.12 builtin sum() over floats starting from int 0 (Neumaier).
@@ -92,7 +112,10 @@ __device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
     f = t;
 }
 
-__global__ void __launch_bounds__(kParseThreads)
+#ifndef PF_PARSE_MINB
+#define PF_PARSE_MINB 8
+#endif
+__global__ void __launch_bounds__(kParseThreads, PF_PARSE_MINB)
 k_parse_frames(const ParseArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -106,6 +129,8 @@ k_parse_frames(const ParseArgs a)
     __shared__ int s_pp[PF_MAX_LIMBS + 1];      // pair prefix per limb
     __shared__ int s_seg[PF_MAX_LIMBS + 1];     // candidate segment start per limb
     __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base;
+    __shared__ int s_lcnt[PF_MAX_LIMBS], s_lcur[PF_MAX_LIMBS];
+    __shared__ uint16_t s_bucket[kCandSmem], s_order[kCandSmem];   // by limb; sorted within limb
     __shared__ int8_t s_la[PF_MAX_LIMBS], s_lb[PF_MAX_LIMBS];
     __shared__ int16_t s_cx[PF_MAX_LIMBS], s_cy[PF_MAX_LIMBS];
     __shared__ double s_t[kParseTTab];          // u / (n - 1), paf.py:139
@@ -193,6 +218,7 @@ k_parse_frames(const ParseArgs a)
         s_pp[L] = acc;
     }
     for (int l = tid; l <= L; l += nthr) s_seg[l] = 0x7fffffff;
+    for (int l = tid; l < L; l += nthr) s_lcnt[l] = 0;
     __syncthreads();
     if (a.debug) {
         for (int e = tid; e < P; e += nthr) {
@@ -232,15 +258,20 @@ k_parse_frames(const ParseArgs a)
             const double vy = __ddiv_rn((double)di, norm);
             const float *chx = paf_f + (size_t)s_cx[l] * a.h * a.w;
             const float *chy = paf_f + (size_t)s_cy[l] * a.h * a.w;
+            // nearest cell of sample u (paf.py:139-141)
+            auto cell_of = [&](int u, int &ci, int &cj) {
+                const double t = u < kParseTTab ? s_t[u] : __ddiv_rn((double)u, den);
+                ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
+                cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
+            };
             double total = 0.0;
             int ngood = 0, nfail = 0;
             for (int u = 0; u < n; ++u) {
-                const double t = u < kParseTTab ? s_t[u] : __ddiv_rn((double)u, den);
-                const int ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
-                const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
-                double px, py;
-                sample_pair(a, chx, chy, ci, cj, px, py);
-                const double d = dadd(dmul(px, vx), dmul(py, vy));
+                int ci, cj;
+                cell_of(u, ci, cj);
+                SampleRaw r;
+                fetch_sample(a, chx, chy, ci, cj, r);
+                const double d = finish_sample(a, r, vx, vy);
                 total = dadd(total, d);
                 if (d >= a.dot_thr) ++ngood;
                 else if (++nfail > max_fail) break;
@@ -249,6 +280,7 @@ k_parse_frames(const ParseArgs a)
             const double score = __ddiv_rn(total, (double)n);
             if (!(score > 0.0)) continue;                  // paf.py:162 (good already passed)
             const int slot = atomicAdd(&s_ncand, 1);
+            atomicAdd(&s_lcnt[l], 1);
             if (slot < a.cap_cands) {
                 Cand c;
                 c.score = score;
@@ -270,10 +302,32 @@ k_parse_frames(const ParseArgs a)
         return;
     }
 
-    // ---- 4. sort candidates by (limb, -score, id_a, id_b), bitonic ----
-    int n2 = 1;
-    while (n2 < nc) n2 <<= 1;
-    if (nc > 1) {
+    // ---- 4+5. order candidates by (limb, -score, id_a, id_b) (paf.py:173)
+    // and run the greedy per limb (paf.py:174-181).  Usual frames (all
+    // candidates in shared memory): bucket by limb, then one warp per limb
+    // ranks its bucket (the key is a total order, so ranks are distinct) and
+    // its lane 0 walks the ranks with used-bitmaps — no CTA-wide sort.
+    // Crowded frames (spill slab): bitonic sort over the whole store.
+    const bool fast = nc <= kCandSmem;
+    if (fast) {
+        if (tid == 0) {
+            int acc = 0;
+            for (int l = 0; l < L; ++l) {
+                s_seg[l] = acc;
+                s_lcur[l] = acc;
+                acc += s_lcnt[l];
+            }
+            s_seg[L] = acc;
+        }
+        __syncthreads();
+        for (int i = tid; i < nc; i += nthr) {
+            const int l = int(cand_s[i].lg >> 24);
+            s_bucket[atomicAdd(&s_lcur[l], 1)] = uint16_t(i);
+        }
+        __syncthreads();
+    } else {
+        int n2 = 1;
+        while (n2 < nc) n2 <<= 1;
         for (int e = nc + tid; e < n2; e += nthr) {
             Cand pad;
             pad.score = 0.0; pad.ab = 0x7fffffffu; pad.lg = 0xff000000u;
@@ -293,40 +347,51 @@ k_parse_frames(const ParseArgs a)
                 __syncthreads();
             }
         }
-    }
-    // segment starts: first index of each limb
-    for (int e = tid; e < nc; e += nthr) {
-        const int l = int(cand[e].lg >> 24);
-        const int prev = e ? int(cand[e - 1].lg >> 24) : -1;
-        for (int q = prev + 1; q <= l; ++q) s_seg[q] = e;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        // limbs after the last candidate start at nc; fill gaps backwards
-        int next = nc;
-        for (int l = L; l >= 0; --l) {
-            if (s_seg[l] == 0x7fffffff) s_seg[l] = next;
-            next = s_seg[l];
+        // segment starts: first index of each limb
+        for (int e = tid; e < nc; e += nthr) {
+            const int l = int(cand[e].lg >> 24);
+            const int prev = e ? int(cand[e - 1].lg >> 24) : -1;
+            for (int q = prev + 1; q <= l; ++q) s_seg[q] = e;
         }
+        __syncthreads();
+        if (tid == 0) {
+            int next = nc;
+            for (int l = L; l >= 0; --l) {
+                if (s_seg[l] == 0x7fffffff) s_seg[l] = next;
+                next = s_seg[l];
+            }
+        }
+        __syncthreads();
     }
-    __syncthreads();
+    // sorted position e -> candidate
+    auto at = [&](int e) -> Cand & { return fast ? cand_s[s_order[e]] : cand[e]; };
 
-    // ---- 5. greedy per limb (one warp per limb) ----
     uint32_t *used_a = used + warp * 2 * bm_words;
     uint32_t *used_b = used_a + bm_words;
     for (int l = warp; l < L; l += n_warps) {
-        if (s_seg[l] == s_seg[l + 1]) continue;           // warp-uniform
+        const int s0 = s_seg[l], s1 = s_seg[l + 1];
+        if (s0 == s1) continue;                           // warp-uniform
+        if (fast) {
+            for (int k = s0 + lane; k < s1; k += kWarp) {
+                const int i = s_bucket[k];
+                const Cand c = cand_s[i];
+                int rank = 0;
+                for (int k2 = s0; k2 < s1; ++k2) rank += cand_less(cand_s[s_bucket[k2]], c);
+                s_order[s0 + rank] = uint16_t(i);
+            }
+        }
         for (int q = lane; q < bm_words; q += kWarp) { used_a[q] = 0u; used_b[q] = 0u; }
         __syncwarp();
         if (lane == 0) {
-            for (int e = s_seg[l]; e < s_seg[l + 1]; ++e) {
-                const uint32_t ab = cand[e].ab;
+            for (int e = s0; e < s1; ++e) {
+                Cand &c = at(e);
+                const uint32_t ab = c.ab;
                 const int ia = int((ab >> 16) & 0x7fff), ib = int(ab & 0xffff);
                 if ((used_a[ia >> 5] >> (ia & 31)) & 1u) continue;
                 if ((used_b[ib >> 5] >> (ib & 31)) & 1u) continue;
                 used_a[ia >> 5] |= 1u << (ia & 31);
                 used_b[ib >> 5] |= 1u << (ib & 31);
-                cand[e].ab = ab | kAccepted;
+                c.ab = ab | kAccepted;
             }
         }
         __syncwarp();
@@ -335,13 +400,14 @@ k_parse_frames(const ParseArgs a)
     if (a.debug && tid == 0) {
         int q = 0;
         for (int e = 0; e < nc; ++e) {
-            if (!(cand[e].ab & kAccepted)) continue;
+            const Cand ce = at(e);
+            if (!(ce.ab & kAccepted)) continue;
             const size_t o = (size_t)gframe * a.cap_cands + q;
-            a.dbg_conn_i[o * 3 + 0] = int(cand[e].lg >> 24);
-            a.dbg_conn_i[o * 3 + 1] = int((cand[e].ab >> 16) & 0x7fff);
-            a.dbg_conn_i[o * 3 + 2] = int(cand[e].ab & 0xffff);
-            a.dbg_conn_d[o * 2 + 0] = cand[e].score;
-            a.dbg_conn_d[o * 2 + 1] = __ddiv_rn((double)(cand[e].lg & 0xffffffu), (double)n);
+            a.dbg_conn_i[o * 3 + 0] = int(ce.lg >> 24);
+            a.dbg_conn_i[o * 3 + 1] = int((ce.ab >> 16) & 0x7fff);
+            a.dbg_conn_i[o * 3 + 2] = int(ce.ab & 0xffff);
+            a.dbg_conn_d[o * 2 + 0] = ce.score;
+            a.dbg_conn_d[o * 2 + 1] = __ddiv_rn((double)(ce.lg & 0xffffffu), (double)n);
             ++q;
         }
         a.dbg_nconns[gframe] = q;
@@ -351,7 +417,7 @@ k_parse_frames(const ParseArgs a)
     if (tid == 0) {
         int nh = 0, err = 0;
         for (int e = 0; e < nc && !err; ++e) {
-            const Cand c = cand[e];
+            const Cand c = at(e);
             if (!(c.ab & kAccepted)) continue;
             const int l = int(c.lg >> 24);
             const int a_part = s_la[l], b_part = s_lb[l];

@@ -20,7 +20,8 @@ idx = torch.arange(F) % conf_h.shape[0]
 conf = torch.from_numpy(conf_h).cuda()[idx.cuda()].contiguous()
 paf = torch.from_numpy(paf_h).cuda()[idx.cuda()].contiguous()
 params = pf.ParserParams(upsample=int(os.environ.get("UP", "8")))
-e = pf.PafParser(topo)
+caps = dict(kv.split("=") for kv in os.environ["CAPS"].split(",")) if os.environ.get("CAPS") else {}
+e = pf.PafParser(topo, caps={k: int(v) for k, v in caps.items()})
 ref = None
 for rep in range(2):
     for v in values:
