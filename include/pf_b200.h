@@ -161,8 +161,6 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_GENERIC_FUSED 4   /* use the shared-memory tile kernel for Mode U */
 #define PF_OPT_WIN_VARIANT 5     /* Mode U 3x3 kernel: 4 corner-pruned (default), 3/2/1 strip kernels */
 #define PF_OPT_NO_CHAIN 6        /* corner kernel: disable the chain pre-filter (A/B parity checks) */
-#define PF_OPT_CORNER_WARP_ROWS 7 /* corner kernel layout: 2 warp per plane from L2 (default),
-                                     1 warp-autonomous band rows, 0 CTA phases (both smem-staged) */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch

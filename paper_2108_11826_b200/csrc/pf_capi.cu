@@ -38,7 +38,6 @@ struct AxisCache {
     bool canonical = false;                     // band b reads sources (b-1, b) clipped: b = 0..in_n
     int4 *d_bands = nullptr;
     double *d_band_dt = nullptr;
-    BandT *d_bandt = nullptr;
     int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr, *d_gend = nullptr;
     double2 *d_tw = nullptr;
     AxisRec *d_rec = nullptr;
@@ -174,7 +173,6 @@ struct pf_ctx {
     int generic_fused = 0;
     int win_variant = 4;
     int no_chain = 0;
-    int corner_warp_rows = 0;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double kernel_ms[PF_N_KERNELS] = {0};
@@ -301,23 +299,6 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
         CU(cudaMemcpy(a.d_bands, a.bands.data(), a.bands.size() * sizeof(int4), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_band_dt, a.band_dt.size()));
         CU(cudaMemcpy(a.d_band_dt, a.band_dt.data(), a.band_dt.size() * sizeof(double), cudaMemcpyHostToDevice));
-        {
-            // the same fp32 roundings as pf_corner.cu fill_band (double -> float is RN on both sides)
-            std::vector<BandT> bt(a.bands.size());
-            for (size_t b = 0; b < a.bands.size(); ++b) {
-                const int f = a.bands[b].x, l = a.bands[b].y;
-                bt[b].omt_f = (float)a.omt[f];
-                bt[b].t_f = (float)a.t[f];
-                bt[b].omt_l = (float)a.omt[l];
-                bt[b].t_l = (float)a.t[l];
-                bt[b].s_l = (float)(a.t[l] - a.t[std::max(l - 1, f)]);
-                bt[b].s_f = (float)(a.t[std::min(f + 1, l)] - a.t[f]);
-                bt[b].dt = (float)a.band_dt[b];
-                bt[b].pad = 0.f;
-            }
-            CU(dev_alloc(&a.d_bandt, bt.size()));
-            CU(cudaMemcpy(a.d_bandt, bt.data(), bt.size() * sizeof(BandT), cudaMemcpyHostToDevice));
-        }
         CU(dev_alloc(&a.d_gend, out_n));
         CU(cudaMemcpy(a.d_gend, a.gend.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_first, in_n));
@@ -479,7 +460,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
     } else if (!blur && half == 1 && !ctx->materialise && !ctx->generic_fused && ctx->win_variant == 4 &&
-               rows->canonical && cols->canonical && (long long)(h + 1) * (w + 1) <= 65535 &&
+               rows->canonical && cols->canonical && h + 1 <= 256 && w + 1 <= 256 &&
                nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) <= 100 * 1024) {
         UpCornerArgs a{};
         a.conf = conf; a.B = n; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
@@ -491,9 +472,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.nbr = (int)rows->bands.size(); a.nbc = (int)cols->bands.size();
         a.nst = kCornerStages;
         a.chain = rows->min_step >= 0.03125 && cols->min_step >= 0.03125 && !ctx->no_chain;
-        a.warp_rows = ctx->corner_warp_rows == 1;
-        a.variant = ctx->corner_warp_rows == 2 ? 1 : 0;
-        a.rbt = rows->d_bandt; a.cbt = cols->d_bandt;
+        a.rrec = rows->d_rec; a.crec = cols->d_rec;
         KernelTimer kt(ctx, kNmsUpCorner);
         CU(launch_nms_up_corner(a, s));
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
@@ -835,7 +814,7 @@ void pf_destroy(pf_ctx *ctx)
         cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
         cudaFree(kv.second.d_first); cudaFree(kv.second.d_last); cudaFree(kv.second.d_gend); cudaFree(kv.second.d_tw);
         cudaFree(kv.second.d_rec);
-        cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt); cudaFree(kv.second.d_bandt);
+        cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt);
     }
     for (auto &p : ctx->pending) { ctx->ev_pool.push_back(p.second.first); ctx->ev_pool.push_back(p.second.second); }
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -922,7 +901,6 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_GENERIC_FUSED: ctx->generic_fused = value ? 1 : 0; return PF_OK;
     case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 4) ? value : 4; return PF_OK;
     case PF_OPT_NO_CHAIN: ctx->no_chain = value ? 1 : 0; return PF_OK;
-    case PF_OPT_CORNER_WARP_ROWS: ctx->corner_warp_rows = (value >= 0 && value <= 2) ? value : 2; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }

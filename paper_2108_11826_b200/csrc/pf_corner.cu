@@ -55,15 +55,25 @@
 
 namespace pf {
 
+#ifdef PF_CORNER_PROF
+__device__ unsigned long long g_corner_prof[16];  // cycles per phase [0, 12) (thread 0 of each CTA), planes, hot, survivors, candidates
+#endif
+
 constexpr float kNoise = 7.62939453125e-06f;   // 2^-17
-constexpr int kCornerThreads = 128;
+#ifndef PF_CORNER_THREADS
+#define PF_CORNER_THREADS 128
+#endif
+constexpr int kCornerThreads = PF_CORNER_THREADS;
 constexpr int kCornerCands = 512;    // candidate pixels per plane kept in shared memory
 constexpr int kCornerList = 1024;    // hot cells per plane kept in shared memory
+constexpr int kCornerSurv = 256;     // chain survivors per plane kept in shared memory
 
 
-__device__ __forceinline__ void emit_peak_c(int *counts, uint2 *peaks, int plane, int cap, float v, int i, int j)
+// One CTA owns a plane, so its peak count lives in shared memory (no global
+// atomic round trip on the critical path) and is stored once per plane.
+__device__ __forceinline__ void emit_peak_c(int *npk, uint2 *peaks, int plane, int cap, float v, int i, int j)
 {
-    const int slot = atomicAdd(counts + plane, 1);
+    const int slot = atomicAdd(npk, 1);
     if (slot < cap) peaks[(size_t)plane * cap + slot] = pack_peak(v, i, j);
 }
 
@@ -74,17 +84,21 @@ struct Ax {
     bool in;
 };
 
-__device__ __forceinline__ Ax ax_load(const AxisTab &tab, int o, int n_out)
+// one 16-byte load of the packed record (i0 | i1 << 16, t); 1 - t is the
+// host table's own single rounded subtraction
+__device__ __forceinline__ Ax ax_load(const AxisRec *tab, int o, int n_out)
 {
     Ax r;
     r.in = o >= 0 && o < n_out;
     const int oc = min(max(o, 0), n_out - 1);
-    r.i0 = __ldg(tab.i0 + oc);
-    r.i1 = __ldg(tab.i1 + oc);
-    r.t = __ldg(tab.t + oc);
-    r.omt = __ldg(tab.omt + oc);
+    const int4 v = __ldg(reinterpret_cast<const int4 *>(tab + oc));
+    r.i0 = v.x & 0xffff;
+    r.i1 = v.x >> 16;
+    r.t = __hiloint2double(v.w, v.z);
+    r.omt = __dsub_rn(1.0, r.t);
     return r;
 }
+
 
 // Exact upsampled value (operators.py:104-107 op order); -inf off-grid.
 __device__ __forceinline__ float up_val(const float *S, int w, const Ax &ry, const Ax &cx)
@@ -98,8 +112,8 @@ __device__ __forceinline__ float up_val(const float *S, int w, const Ax &ry, con
 // and column parameter is loaded once.
 __device__ __noinline__ bool exact_peak(const UpCornerArgs &a, const float *S, int y, int x, float &v)
 {
-    const Ax ym = ax_load(a.rows, y - 1, a.H), yc = ax_load(a.rows, y, a.H), yp = ax_load(a.rows, y + 1, a.H);
-    const Ax xm = ax_load(a.cols, x - 1, a.W), xc = ax_load(a.cols, x, a.W), xp = ax_load(a.cols, x + 1, a.W);
+    const Ax ym = ax_load(a.rrec, y - 1, a.H), yc = ax_load(a.rrec, y, a.H), yp = ax_load(a.rrec, y + 1, a.H);
+    const Ax xm = ax_load(a.crec, x - 1, a.W), xc = ax_load(a.crec, x, a.W), xp = ax_load(a.crec, x + 1, a.W);
     v = up_val(S, a.w, yc, xc);
     if (!(v >= a.thr)) return false;
     // earlier neighbours: strictly greater; later: greater or equal
@@ -252,14 +266,16 @@ __device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands
         const int y = (ok & 2u) ? (r ? rb.y : rb.x) : rb.x + r;
         int only_x = -1;
         if (q_in) {
-            const float d = sl_h(c, (float)__ldg(a.rows.omt + y), (float)__ldg(a.rows.t + y));
+            const double ty = __ldg(&a.rrec[y].t);
+            const float d = sl_h(c, (float)__dsub_rn(1.0, ty), (float)ty);
             if (fabsf(d) * cdt > n) only_x = d > 0.f ? cb.y : cb.x;
         }
         for (int k = 0; k < nc; ++k) {
             const int x = (ok & 1u) ? (k ? cb.y : cb.x) : cb.x + k;
             if (only_x >= 0 && x != only_x) continue;
             if (p_in) {
-                const float e = sl_v(c, (float)__ldg(a.cols.omt + x), (float)__ldg(a.cols.t + x));
+                const double tx = __ldg(&a.crec[x].t);
+                const float e = sl_v(c, (float)__dsub_rn(1.0, tx), (float)tx);
                 if (fabsf(e) * rdt > n && y != (e > 0.f ? rb.y : rb.x)) continue;
             }
             push_cand(cl, y, x);
@@ -285,42 +301,35 @@ __device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands
 // direction are never pruned in that direction (their sources coincide, so
 // the differences are 0 and the strict compares fail by themselves).
 // NaN/inf sources make every compare false: nothing is pruned.
-__device__ __forceinline__ bool chain_pruned(const Bands &bd, const float *S, int w, int nbr, int nbc, int p, int q)
+__device__ __forceinline__ bool chain_pruned(const float *S, int w, int nbr, int nbc, int p, int q)
 {
-    const int4 rb = bd.rb[p], cb = bd.cb[q];
-    const float *r0 = S + rb.z * w, *r1 = S + rb.w * w;
-    const float a0 = r0[cb.z], a1 = r0[cb.w], b0 = r1[cb.z], b1 = r1[cb.w];
+    // canonical bands: cell (p, q) reads source rows p-1, p and columns q-1, q;
+    // border cells (clamped sources) take the exact path
+    if (p < 1 || p > nbr - 2 || q < 1 || q > nbc - 2) return false;
+    const float *s = S + (p - 1) * w + (q - 1);
+    const float a0 = s[0], a1 = s[1], b0 = s[w], b1 = s[w + 1];
     const float m4 = fmaxf(fmaxf(fabsf(a0), fabsf(a1)), fmaxf(fabsf(b0), fabsf(b1)));
     if (!(m4 >= 8.673617379884035e-19f)) return false;   // 2^-60: tiny or NaN -> exact path
     const float d4 = m4 * 1.52587890625e-05f;              // 2^-16 (exact scaling)
     const float ha = a1 - a0, hb = b1 - b0, va = b0 - a0, vb = b1 - a1;
     const bool hR = ha > d4 && hb > d4, hL = ha < -d4 && hb < -d4;
     const bool vD = va > d4 && vb > d4, vU = va < -d4 && vb < -d4;
-    if (hR || hL) {
-        // the neighbouring cell in the rising direction: column pair (c1, c2) or (c_-1, c0)
-        const int qn = hR ? q + 1 : q - 1;
-        if (qn >= 0 && qn < nbc) {
-            const int4 cn = bd.cb[qn];
-            const float e0 = r0[cn.z], e1 = r0[cn.w], f0 = r1[cn.z], f1 = r1[cn.w];
-            const float m = fmaxf(m4, fmaxf(fmaxf(fabsf(e0), fabsf(e1)), fmaxf(fabsf(f0), fabsf(f1))));
-            const float d = m * 1.52587890625e-05f;
-            const float ea = e1 - e0, eb = f1 - f0;
-            const bool ok = hR ? (ha > d && hb > d && ea > d && eb > d) : (ha < -d && hb < -d && ea < -d && eb < -d);
-            if (ok) return true;
-        }
+    // the next cell in the rising direction reads one new source column (row):
+    // hR: column q+1 (s[2], s[w+2]); hL: column q-2 (s[-1], s[w-1]);
+    // vD: row p+1 (s[2w], s[2w+1]); vU: row p-2 (s[-w], s[-w+1])
+    if ((hR && q + 1 <= nbc - 2) || (hL && q - 1 >= 1)) {
+        const int o = hR ? 2 : -1;
+        const float e = s[o], f = s[w + o];
+        const float d = fmaxf(m4, fmaxf(fabsf(e), fabsf(f))) * 1.52587890625e-05f;
+        if (hR ? (ha > d && hb > d && e - a1 > d && f - b1 > d)
+               : (ha < -d && hb < -d && e - a0 > d && f - b0 > d)) return true;
     }
-    if (vD || vU) {
-        const int pn = vD ? p + 1 : p - 1;
-        if (pn >= 0 && pn < nbr) {
-            const int4 rn = bd.rb[pn];
-            const float *s0 = S + rn.z * w, *s1 = S + rn.w * w;
-            const float e0 = s0[cb.z], e1 = s0[cb.w], f0 = s1[cb.z], f1 = s1[cb.w];
-            const float m = fmaxf(m4, fmaxf(fmaxf(fabsf(e0), fabsf(e1)), fmaxf(fabsf(f0), fabsf(f1))));
-            const float d = m * 1.52587890625e-05f;
-            const float ea = f0 - e0, eb = f1 - e1;
-            const bool ok = vD ? (va > d && vb > d && ea > d && eb > d) : (va < -d && vb < -d && ea < -d && eb < -d);
-            if (ok) return true;
-        }
+    if ((vD && p + 1 <= nbr - 2) || (vU && p - 1 >= 1)) {
+        const int o = vD ? 2 * w : -w;
+        const float e = s[o], f = s[o + 1];
+        const float d = fmaxf(m4, fmaxf(fabsf(e), fabsf(f))) * 1.52587890625e-05f;
+        if (vD ? (va > d && vb > d && e - b0 > d && f - b1 > d)
+               : (va < -d && vb < -d && e - a0 > d && f - a1 > d)) return true;
     }
     return false;
 }
@@ -351,7 +360,7 @@ __device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands 
 // Exact value of output pixel (y, x); -inf off the grid (paf.py:87-93 pads).
 __device__ __forceinline__ float exact_value(const UpCornerArgs &a, const float *S, int y, int x)
 {
-    return up_val(S, a.w, ax_load(a.rows, y, a.H), ax_load(a.cols, x, a.W));
+    return up_val(S, a.w, ax_load(a.rrec, y, a.H), ax_load(a.crec, x, a.W));
 }
 
 // ---- mbarrier + 1-D bulk copy (TMA) helpers
@@ -388,17 +397,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 
 // Shared-memory layout of one CTA (byte offsets).
 struct CornerLayout {
-    int plane_floats;    // h*w rounded up to 128 (padding = -inf)
-    int n_hw;            // hot-bitmap words per plane
-    size_t planes, bars, rb, cb, rt, ct, hot, list, cand, total;
+    int plane_floats;    // h*w rounded up to 4 (padding = -inf)
+    size_t planes, bars, rb, cb, rt, ct, hot, list, cand, surv, total;
 };
 
 __host__ __device__ inline CornerLayout corner_layout(int h, int w, int nbr, int nbc, int nst)
 {
     CornerLayout L;
     const int hw = h * w;
-    L.plane_floats = (hw + 127) & ~127;
-    L.n_hw = L.plane_floats >> 5;
+    L.plane_floats = (hw + 3) & ~3;                   // 16-byte stages for the bulk copies
     size_t o = 0;
     L.planes = o; o += (size_t)nst * L.plane_floats * sizeof(float);
     L.bars = o;   o += (size_t)nst * 8;
@@ -407,9 +414,10 @@ __host__ __device__ inline CornerLayout corner_layout(int h, int w, int nbr, int
     L.cb = o;     o += (size_t)nbc * sizeof(int4);
     L.rt = o;     o += (size_t)nbr * sizeof(BandT);
     L.ct = o;     o += (size_t)nbc * sizeof(BandT);
-    L.hot = o;    o += (size_t)(L.n_hw + 4) * sizeof(uint32_t);
-    L.list = o;   o += (size_t)kCornerList * sizeof(uint32_t);
+    L.hot = o;    o += (size_t)(h + 2) * ((w + 31) >> 5) * sizeof(uint32_t);   // row-aligned hot words
+    L.list = o;   o += (size_t)kCornerList * sizeof(uint16_t);
     L.cand = o;   o += (size_t)kCornerCands * sizeof(uint32_t);
+    L.surv = o;   o += (size_t)kCornerSurv * sizeof(uint32_t);
     L.total = (o + 15) & ~(size_t)15;
     return L;
 }
@@ -429,32 +437,30 @@ __device__ __forceinline__ void fill_band(const AxisTab &tab, const double *dt, 
     T.pad = 0.f;
 }
 
-// Hot bits of source row r, columns [32j, 32j+32), from the
-// linear hot bitmap (bits beyond the row masked off).
-__device__ __forceinline__ uint32_t row_word(const uint32_t *hot, int h, int w, int r, int j)
+// Hot cells of band row p, columns [32j, 32j + 32): band p reads source rows
+// p-1 and p, cell q source columns q-1 and q, so with M = hot(p-1) | hot(p)
+// (row-aligned words; guard rows -1 and h are zero) the cell word is
+// M | M << 1 plus bit 31 of the previous word.  Source bits stop at column
+// w-1, so cell bits stop at q = w (band count w + 1) by themselves.
+__device__ __forceinline__ uint32_t cell_word(const uint32_t *R, int nws, int p, int j)
 {
-    const int c0 = j << 5;
-    if (r < 0 || r >= h || c0 >= w) return 0u;
-    const int o = r * w + c0;
-    uint32_t v = __funnelshift_r(hot[o >> 5], hot[(o >> 5) + 1], o & 31);
-    const int rem = w - c0;
-    if (rem < 32) v &= (1u << rem) - 1u;
-    return v;
+    const uint32_t *r0 = R + p * nws, *r1 = r0 + nws;    // rows p-1, p (guard-offset by one row)
+    const uint32_t m = j < nws ? (r0[j] | r1[j]) : 0u;
+    const uint32_t cin = j > 0 ? (r0[j - 1] | r1[j - 1]) >> 31 : 0u;
+    return m | (m << 1) | cin;
 }
 
 // Slow path for a plane whose hot cells or candidates overflowed the shared
 // lists: forget its peaks and exactly test every pixel of every hot cell.
 __device__ __noinline__ void redo_plane(const UpCornerArgs &a, const Bands &bd, const float *S,
-                                        const uint32_t *hot, int plane)
+                                        const uint32_t *R, int plane, int *npk)
 {
-    if (threadIdx.x == 0) a.counts[plane] = 0;
+    if (threadIdx.x == 0) *npk = 0;
     __syncthreads();
-    const int h = a.h, w = a.w, nwc = (w + 32) >> 5;
-    for (int t = threadIdx.x; t < (h + 1) * nwc; t += kCornerThreads) {
+    const int nws = (a.w + 31) >> 5, nwc = (a.w + 32) >> 5;
+    for (int t = threadIdx.x; t < a.nbr * nwc; t += kCornerThreads) {
         const int p = t / nwc, j = t - p * nwc;
-        const uint32_t m = row_word(hot, h, w, p - 1, j) | row_word(hot, h, w, p, j);
-        uint32_t c = m | (m << 1);
-        if (j) c |= (row_word(hot, h, w, p - 1, j - 1) | row_word(hot, h, w, p, j - 1)) >> 31;
+        uint32_t c = cell_word(R, nws, p, j);
         while (c) {
             const int q = (j << 5) + __ffs(c) - 1;
             c &= c - 1u;
@@ -462,13 +468,17 @@ __device__ __noinline__ void redo_plane(const UpCornerArgs &a, const Bands &bd, 
             for (int y = rb.x; y <= rb.y; ++y)
                 for (int x = cb.x; x <= cb.y; ++x) {
                     float v;
-                    if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
+                    if (exact_peak(a, S, y, x, v)) emit_peak_c(npk, a.peaks, plane, a.cap, v, y, x);
                 }
         }
     }
 }
 
-__global__ void __launch_bounds__(kCornerThreads, 5)
+#ifndef PF_CORNER_MINB
+#define PF_CORNER_MINB 8
+#endif
+template <int NWS>   // hot words per source row, (w + 31) / 32: fixed so phase A is straight-line code
+__global__ void __launch_bounds__(kCornerThreads, PF_CORNER_MINB)
 k_nms_up_corner(const UpCornerArgs a)
 {
     extern __shared__ __align__(128) unsigned char smc[];
@@ -482,9 +492,10 @@ k_nms_up_corner(const UpCornerArgs a)
     BandT *RT = reinterpret_cast<BandT *>(smc + L.rt);
     BandT *CT = reinterpret_cast<BandT *>(smc + L.ct);
     uint32_t *hot = reinterpret_cast<uint32_t *>(smc + L.hot);
-    uint32_t *list = reinterpret_cast<uint32_t *>(smc + L.list);
+    uint16_t *list = reinterpret_cast<uint16_t *>(smc + L.list);   // (p << 8) | q
     uint32_t *cand = reinterpret_cast<uint32_t *>(smc + L.cand);
-    __shared__ int n_hot, n_cand;
+    uint32_t *surv = reinterpret_cast<uint32_t *>(smc + L.surv);
+    __shared__ int n_hot, n_cand, n_surv, n_pk;
     const CandList cl{cand, &n_cand, kCornerCands};
     const Bands bd{RB, CB, RT, CT};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -498,10 +509,18 @@ k_nms_up_corner(const UpCornerArgs a)
     }
     for (int s = 0; s < nst; ++s)
         for (int e = hw + threadIdx.x; e < L.plane_floats; e += kCornerThreads) planes[s * L.plane_floats + e] = -INFINITY;
-    for (int e = L.n_hw + threadIdx.x; e < L.n_hw + 4; e += kCornerThreads) hot[e] = 0u;
+    constexpr int nws = NWS;                         // hot words per source row
+    const int nwc = (w + 32) >> 5;                   // cell words per band row (nbc = w + 1)
+    const float inv_nwc = 1.0f / (float)nwc;
+    for (int e = threadIdx.x; e < nws; e += kCornerThreads) {
+        hot[e] = 0u;                                 // guard row -1
+        hot[(h + 1) * nws + e] = 0u;                 // guard row h
+    }
     if (threadIdx.x == 0) {
         n_hot = 0;
         n_cand = 0;
+        n_surv = 0;
+        n_pk = 0;
         if (a.bulk) {
             for (int s = 0; s < nst; ++s) mbar_init(bars + s, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -517,13 +536,22 @@ k_nms_up_corner(const UpCornerArgs a)
     }
     __syncthreads();
 
+#ifdef PF_CORNER_PROF
+    unsigned long long acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long t0 = clock64(), t1;
+#define PROF_MARK(k) do { if (threadIdx.x == 0) { t1 = clock64(); acc[k] += t1 - t0; t0 = t1; } } while (0)
+#else
+#define PROF_MARK(k) do { } while (0)
+#endif
     int it = 0;
     for (long long pl = blockIdx.x; pl < P; pl += gridDim.x, ++it) {
         const int stage = it % nst;
         float *S = planes + stage * L.plane_floats;
         const int plane = (int)pl;
+        PROF_MARK(7);
         if (a.bulk) {
             mbar_wait(bars + stage, (uint32_t)(it / nst) & 1u);
+            PROF_MARK(10);
         } else {
             const long long b = pl / a.K, k = pl - b * a.K;
             const float *src = a.conf + ((size_t)b * a.C + k) * (size_t)hw;
@@ -531,79 +559,86 @@ k_nms_up_corner(const UpCornerArgs a)
             __syncthreads();
         }
 
-        // ---- (A) hot-source bitmap: 8 lanes x float4 = one 32-bit word
-        {
-            const float4 *s4 = reinterpret_cast<const float4 *>(S);
-            const int n4 = L.plane_floats >> 2;            // multiple of 32: warp-uniform trip count
-            for (int e = threadIdx.x; e < n4; e += kCornerThreads) {
-                const float4 v = s4[e];
-                uint32_t nib = uint32_t(v.x >= a.thr) | (uint32_t(v.y >= a.thr) << 1) |
-                               (uint32_t(v.z >= a.thr) << 2) | (uint32_t(v.w >= a.thr) << 3);
-                nib <<= 4 * (lane & 7);
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
-                if ((lane & 7) == 0) hot[e >> 3] = nib;
+        // ---- (A) row-aligned hot words: warp per source row, lane = column,
+        // one ballot per 32 columns (rows offset by the zero guard row)
+        for (int r = warp; r < h; r += kCornerThreads / kWarp) {
+            const float *row = S + r * w;
+            float v[NWS];
+#pragma unroll
+            for (int j = 0; j < NWS; ++j) {
+                const int c = (j << 5) + lane;
+                v[j] = (j < NWS - 1 || c < w) ? row[c] : -INFINITY;
             }
+            uint32_t mine = 0u;
+#pragma unroll
+            for (int j = 0; j < NWS; ++j) {
+                const uint32_t word = __ballot_sync(0xffffffffu, v[j] >= a.thr);
+                if (lane == j) mine = word;
+            }
+            if (lane < nws) hot[(r + 1) * nws + lane] = mine;
         }
+        PROF_MARK(0);
         __syncthreads();
+        PROF_MARK(1);
 
-        // ---- (B) hot cells of canonical bands: C_p = M_p | M_p << 1 (+ carry)
-        {
-            const int nwc = (w + 32) >> 5;                  // words per band row (nbc = w + 1 bits)
-            const int ntask = (h + 1) * nwc;
-            for (int t = threadIdx.x; t < ntask; t += kCornerThreads) {
-                const int p = t / nwc, j = t - p * nwc;
-                const uint32_t m = row_word(hot, h, w, p - 1, j) | row_word(hot, h, w, p, j);
-                uint32_t c = m | (m << 1);
-                if (j) c |= (row_word(hot, h, w, p - 1, j - 1) | row_word(hot, h, w, p, j - 1)) >> 31;
-                if (c) {
-                    int slot = atomicAdd(&n_hot, __popc(c));
-                    while (c) {
-                        const int q = (j << 5) + __ffs(c) - 1;
-                        c &= c - 1u;
-                        if (slot < kCornerList) list[slot] = (uint32_t(p) << 16) | uint32_t(q);   // beyond: slow path
-                        ++slot;
-                    }
+        // ---- (B) hot cells, one (band row, 32 cells) word per task
+        for (int t = threadIdx.x; t < nbr * nwc; t += kCornerThreads) {
+            const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;   // exact for t < 2^16
+            uint32_t c = cell_word(hot, nws, p, j);
+            if (c) {
+                int slot = atomicAdd(&n_hot, __popc(c));
+                while (c) {
+                    const int q = (j << 5) + __ffs(c) - 1;
+                    c &= c - 1u;
+                    if (slot < kCornerList) list[slot] = uint16_t((p << 8) | q);   // beyond: slow path
+                    ++slot;
                 }
             }
         }
+        PROF_MARK(2);
         __syncthreads();
+        PROF_MARK(3);
 
-        // ---- (C1) lane = hot cell.  Each warp owns a contiguous slice of the
-        // hot list: the chain pre-filter runs on every cell and compacts the
-        // survivors in place at the front of the slice (warp-synchronous: a
-        // write index never passes the read index), then the survivors are
-        // classified; normal cells push their surviving corner, partial cells
-        // their candidate pixels.
+        // ---- (C1) lane = hot cell (interleaved over the warps): the chain
+        // pre-filter on every cell, survivors appended to the CTA survivor
+        // list (warp-aggregated), then the survivors are classified spread
+        // over all warps (survivor i -> warp i % 4): normal cells push their
+        // surviving corner, partial cells their candidate pixels.
         {
             const int nh = min(n_hot, kCornerList);
-            const int chunk = (nh + 3) >> 2;
-            const int lo = warp * chunk, hi = min(nh, lo + chunk);
-            int ns = hi - lo;
-            if (a.chain) {
-                ns = 0;
-                for (int base = lo; base < hi; base += kWarp) {
-                    const int idx = base + lane;
-                    uint32_t cell = 0u;
-                    bool keep = false;
-                    if (idx < hi) {
-                        cell = list[idx];
-                        keep = !chain_pruned(bd, S, w, nbr, nbc, int(cell >> 16), int(cell & 0xffffu));
-                    }
-                    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-                    __syncwarp();
-                    if (keep) list[lo + ns + __popc(bal & ((1u << lane) - 1u))] = cell;
-                    ns += __popc(bal);
+            for (int base = warp * kWarp; base < nh; base += kCornerThreads) {
+                const int idx = base + lane;
+                uint32_t cell = 0u;
+                bool keep = false;
+                if (idx < nh) {
+                    const uint32_t pq = list[idx];
+                    cell = ((pq >> 8) << 16) | (pq & 0xffu);
+                    keep = !(a.chain && chain_pruned(S, w, nbr, nbc, int(cell >> 16), int(cell & 0xffffu)));
                 }
-                __syncwarp();
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                if (bal) {
+                    int at = 0;
+                    if (lane == 0) at = atomicAdd(&n_surv, __popc(bal));
+                    at = __shfl_sync(0xffffffffu, at, 0);
+                    const int slot = at + __popc(bal & ((1u << lane) - 1u));
+                    if (keep && slot < kCornerSurv) surv[slot] = cell;          // beyond: slow path
+                }
             }
-            for (int idx = lo + lane; idx < lo + ns; idx += kWarp) {
-                const uint32_t cell = list[idx];
+        }
+        PROF_MARK(8);
+        __syncthreads();
+        PROF_MARK(9);
+        {
+            const int ns = min(n_surv, kCornerSurv);
+            const int nw = kCornerThreads / kWarp;
+            for (int i = warp + nw * lane; i < ns; i += kCornerThreads) {
+                const uint32_t cell = surv[i];
                 process_cell(a, bd, cl, S, plane, int(cell >> 16), int(cell & 0xffffu));
             }
         }
+        PROF_MARK(4);
         __syncthreads();
+        PROF_MARK(5);
 
         // ---- (C2) the exact 3x3 test, 9 lanes per candidate (one pixel each),
         // three candidates per warp, gathered by shuffles
@@ -630,18 +665,29 @@ k_nms_up_corner(const UpCornerArgs a)
                     // paf.py:95-99: earlier neighbours strictly, later ones non-strictly
                     if (v >= a.thr && v > nv[0] && v > nv[1] && v > nv[2] && v > nv[3] && v >= nv[5] &&
                         v >= nv[6] && v >= nv[7] && v >= nv[8])
-                        emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
+                        emit_peak_c(&n_pk, a.peaks, plane, a.cap, v, y, x);
                 }
             }
         }
         __syncthreads();
-        if (n_hot > kCornerList || n_cand > kCornerCands) {    // CTA-uniform: a list overflowed
-            redo_plane(a, bd, S, hot, plane);
+        PROF_MARK(6);
+#ifdef PF_CORNER_PROF
+        if (threadIdx.x == 0) {
+            atomicAdd(g_corner_prof + 13, (unsigned long long)n_hot);
+            atomicAdd(g_corner_prof + 14, (unsigned long long)n_surv);
+            atomicAdd(g_corner_prof + 15, (unsigned long long)n_cand);
+        }
+#endif
+        if (n_hot > kCornerList || n_surv > kCornerSurv || n_cand > kCornerCands) {   // CTA-uniform: a list overflowed
+            redo_plane(a, bd, S, hot, plane, &n_pk);
         }
         __syncthreads();                                     // stage + list free again
         if (threadIdx.x == 0) {
+            a.counts[plane] = n_pk;                          // the plane's peaks are complete
             n_hot = 0;
             n_cand = 0;
+            n_surv = 0;
+            n_pk = 0;
             const long long nx = pl + (long long)nst * gridDim.x;
             if (a.bulk && nx < P) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -650,461 +696,12 @@ k_nms_up_corner(const UpCornerArgs a)
             }
         }
     }
-}
-
-// ---------------------------------------------------------------------------
-// k_nms_up_corner_w — the same exact algorithm, reorganised so that the four
-// warps of a CTA never wait for each other inside a plane.  Warp w owns the
-// band rows [w*R, (w+1)*R) of the plane in the stage buffer and runs, on its
-// own, the whole chain for them:
-//   hot rows    — ballot(S[r][32j + lane] >= thr): one row-aligned hot word
-//                 per (source row, 32 columns), carried in registers from one
-//                 band row to the next (band p reads source rows p-1, p);
-//   hot cells   — C = M | M << 1 (+ carry), M = hot(p-1) | hot(p): lane q of
-//                 word j is cell (p, 32j + q); compacted into a per-warp list;
-//   chain prune — on full lanes, survivors compacted in place (chain_pruned);
-//   classify    — survivors only (process_cell) -> per-warp candidate list;
-//   exact test  — 9 lanes per candidate, as in k_nms_up_corner.
-// The only CTA barrier per plane is the one that frees the stage buffer.
-constexpr int kWList = 256;      // hot cells per warp before a flush
-constexpr int kWCand = 128;      // candidate pixels per warp per plane
-constexpr int kMaxRowWords = 8;  // w <= 255
-
-struct CornerWLayout {
-    int plane_floats;
-    size_t planes, bars, rb, cb, rt, ct, list, cand, total;
-};
-
-__host__ __device__ inline CornerWLayout corner_w_layout(int h, int w, int nbr, int nbc, int nst)
-{
-    CornerWLayout L;
-    L.plane_floats = (h * w + 127) & ~127;
-    size_t o = 0;
-    L.planes = o; o += (size_t)nst * L.plane_floats * sizeof(float);
-    L.bars = o;   o += (size_t)nst * 8;
-    o = (o + 15) & ~(size_t)15;
-    L.rb = o;     o += (size_t)nbr * sizeof(int4);
-    L.cb = o;     o += (size_t)nbc * sizeof(int4);
-    L.rt = o;     o += (size_t)nbr * sizeof(BandT);
-    L.ct = o;     o += (size_t)nbc * sizeof(BandT);
-    L.list = o;   o += (size_t)(kCornerThreads / kWarp) * kWList * sizeof(uint32_t);
-    L.cand = o;   o += (size_t)(kCornerThreads / kWarp) * kWCand * sizeof(uint32_t);
-    L.total = (o + 15) & ~(size_t)15;
-    return L;
-}
-
-// Hot word of source row r, columns [32j, 32j + 32) (warp-uniform result).
-__device__ __forceinline__ uint32_t hot_word(const float *S, int h, int w, int r, int j, int lane, float thr)
-{
-    const int c = (j << 5) + lane;
-    const bool hot = r >= 0 && r < h && c < w && S[r * w + c] >= thr;
-    return __ballot_sync(0xffffffffu, hot);
-}
-
-// Prune the warp's hot list (full lanes, in place) and classify the survivors.
-__device__ __forceinline__ void flush_cells(const UpCornerArgs &a, const Bands &bd, const CandList &cl,
-                                            const float *S, int plane, uint32_t *list, int nl, int lane)
-{
-    int ns = nl;
-    if (a.chain) {
-        ns = 0;
-        for (int base = 0; base < nl; base += kWarp) {
-            const int idx = base + lane;
-            uint32_t cell = 0u;
-            bool keep = false;
-            if (idx < nl) {
-                cell = list[idx];
-                keep = !chain_pruned(bd, S, a.w, a.nbr, a.nbc, int(cell >> 16), int(cell & 0xffffu));
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) list[ns + __popc(bal & ((1u << lane) - 1u))] = cell;
-            ns += __popc(bal);
-        }
-        __syncwarp();
-    }
-    for (int idx = lane; idx < ns; idx += kWarp) {
-        const uint32_t cell = list[idx];
-        process_cell(a, bd, cl, S, plane, int(cell >> 16), int(cell & 0xffffu));
-    }
-    __syncwarp();
-}
-
-// Slow path (a per-warp candidate list overflowed): exact test of every
-// pixel of every hot cell of the plane, straight from the sources.
-__device__ __noinline__ void redo_plane_w(const UpCornerArgs &a, const Bands &bd, const float *S, int plane)
-{
-    if (threadIdx.x == 0) a.counts[plane] = 0;
-    __syncthreads();
-    for (int t = threadIdx.x; t < a.nbr * a.nbc; t += kCornerThreads) {
-        const int p = t / a.nbc, q = t - p * a.nbc;
-        const int4 rb = bd.rb[p], cb = bd.cb[q];
-        const CellF c = cellf(S, a.w, rb, cb);
-        if (!(c.a0 >= a.thr || c.a1 >= a.thr || c.b0 >= a.thr || c.b1 >= a.thr)) continue;
-        for (int y = rb.x; y <= rb.y; ++y)
-            for (int x = cb.x; x <= cb.y; ++x) {
-                float v;
-                if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
-            }
-    }
-}
-
-__global__ void __launch_bounds__(kCornerThreads, 5)
-k_nms_up_corner_w(const UpCornerArgs a)
-{
-    extern __shared__ __align__(128) unsigned char smc[];
-    const int h = a.h, w = a.w, hw = h * w;
-    const int nbr = a.nbr, nbc = a.nbc, nst = a.nst;
-    const CornerWLayout L = corner_w_layout(h, w, nbr, nbc, nst);
-    float *planes = reinterpret_cast<float *>(smc + L.planes);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smc + L.bars);
-    int4 *RB = reinterpret_cast<int4 *>(smc + L.rb);
-    int4 *CB = reinterpret_cast<int4 *>(smc + L.cb);
-    BandT *RT = reinterpret_cast<BandT *>(smc + L.rt);
-    BandT *CT = reinterpret_cast<BandT *>(smc + L.ct);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t *list = reinterpret_cast<uint32_t *>(smc + L.list) + warp * kWList;
-    uint32_t *cand = reinterpret_cast<uint32_t *>(smc + L.cand) + warp * kWCand;
-    __shared__ int n_cand[kCornerThreads / kWarp];
-    __shared__ int overflow;
-    const CandList cl{cand, &n_cand[warp], kWCand};
-    const Bands bd{RB, CB, RT, CT};
-    const int P = a.B * a.K;
-    const uint32_t plane_bytes = (uint32_t)hw * 4u;
-    const int nws = (w + 31) >> 5;                 // source-row words
-    const int nwc = (nbc + 31) >> 5;               // band-row cell words
-    const int rpw = (nbr + 3) >> 2;                // band rows per warp
-    const int p_lo = warp * rpw, p_hi = min(nbr, p_lo + rpw);
-
-    for (int b = threadIdx.x; b < nbr + nbc; b += kCornerThreads) {
-        if (b < nbr) fill_band(a.rows, a.rdt, a.rband, b, RB[b], RT[b]);
-        else fill_band(a.cols, a.cdt, a.cband, b - nbr, CB[b - nbr], CT[b - nbr]);
-    }
-    if (lane == 0) n_cand[warp] = 0;
+#ifdef PF_CORNER_PROF
     if (threadIdx.x == 0) {
-        overflow = 0;
-        if (a.bulk) {
-            for (int s = 0; s < nst; ++s) mbar_init(bars + s, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            for (int s = 0; s < nst; ++s) {
-                const int pl = blockIdx.x + s * gridDim.x;
-                if (pl < P) {
-                    const int b = pl / a.K, k = pl - b * a.K;
-                    bulk_load(planes + s * L.plane_floats, a.conf + ((size_t)b * a.C + k) * (size_t)hw, plane_bytes,
-                              bars + s);
-                }
-            }
-        }
+        for (int k = 0; k < 12; ++k) atomicAdd(g_corner_prof + k, acc[k]);
+        atomicAdd(g_corner_prof + 12, (unsigned long long)it);
     }
-    __syncthreads();
-
-    int it = 0, stage = 0;
-    for (int pl = blockIdx.x; pl < P; pl += gridDim.x, ++it) {
-        float *S = planes + stage * L.plane_floats;
-        if (a.bulk) {
-            mbar_wait(bars + stage, (uint32_t)(it / nst) & 1u);
-        } else {
-            const int b = pl / a.K, k = pl - b * a.K;
-            const float *src = a.conf + ((size_t)b * a.C + k) * (size_t)hw;
-            for (int e = threadIdx.x; e < hw; e += kCornerThreads) S[e] = __ldg(src + e);
-            __syncthreads();
-        }
-
-        // ---- hot cells of this warp's band rows -> list (flushed when full)
-        uint32_t prev[kMaxRowWords], cur[kMaxRowWords];
-#pragma unroll
-        for (int j = 0; j < kMaxRowWords; ++j)
-            prev[j] = j < nws ? hot_word(S, h, w, p_lo - 1, j, lane, a.thr) : 0u;
-        int nl = 0;
-        for (int p = p_lo; p < p_hi; ++p) {
-            uint32_t carry = 0u;
-#pragma unroll
-            for (int j = 0; j < kMaxRowWords; ++j) {
-                if (j >= nwc) break;
-                cur[j] = j < nws ? hot_word(S, h, w, p, j, lane, a.thr) : 0u;
-                const uint32_t m = prev[j] | cur[j];
-                uint32_t c = m | (m << 1) | carry;
-                carry = m >> 31;
-                if ((j << 5) + 32 > nbc) c &= (1u << (nbc - (j << 5))) - 1u;
-                if (c) {
-                    if (nl > kWList - kWarp) {
-                        flush_cells(a, bd, cl, S, pl, list, nl, lane);
-                        nl = 0;
-                    }
-                    if ((c >> lane) & 1u)
-                        list[nl + __popc(c & ((1u << lane) - 1u))] = (uint32_t(p) << 16) | uint32_t((j << 5) + lane);
-                    nl += __popc(c);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < kMaxRowWords; ++j) prev[j] = cur[j];
-        }
-        __syncwarp();
-        if (nl) flush_cells(a, bd, cl, S, pl, list, nl, lane);
-
-        // ---- exact 3x3 test of this warp's candidates: 9 lanes each
-        {
-            const int ncd = n_cand[warp];
-            const int nc = min(ncd, kWCand);
-            const int grp = lane / 9, nb = lane - grp * 9;
-            const int src = min(grp, 2) * 9;
-            for (int base = 0; base < nc; base += 3) {
-                const int ci = base + grp;
-                const bool act = grp < 3 && ci < nc;
-                int y = 0, x = 0;
-                float val = -INFINITY;
-                if (act) {
-                    const uint32_t yx = cand[ci];
-                    y = (int)(yx >> 16);
-                    x = (int)(yx & 0xffffu);
-                    val = exact_value(a, S, y + nb / 3 - 1, x + nb % 3 - 1);
-                }
-                float nv[9];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) nv[k] = __shfl_sync(0xffffffffu, val, src + k);
-                if (act && nb == 4) {
-                    const float v = nv[4];
-                    // paf.py:95-99: earlier neighbours strictly, later ones non-strictly
-                    if (v >= a.thr && v > nv[0] && v > nv[1] && v > nv[2] && v > nv[3] && v >= nv[5] &&
-                        v >= nv[6] && v >= nv[7] && v >= nv[8])
-                        emit_peak_c(a.counts, a.peaks, pl, a.cap, v, y, x);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) {
-                if (ncd > kWCand) overflow = 1;
-                n_cand[warp] = 0;
-            }
-        }
-        __syncthreads();                                     // every warp done with the stage
-        if (overflow) {                                      // CTA-uniform
-            redo_plane_w(a, bd, S, pl);
-            __syncthreads();
-            if (threadIdx.x == 0) overflow = 0;
-        }
-        if (threadIdx.x == 0) {
-            const int nx = pl + nst * gridDim.x;
-            if (a.bulk && nx < P) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const int b = nx / a.K, k = nx - b * a.K;
-                bulk_load(S, a.conf + ((size_t)b * a.C + k) * (size_t)hw, plane_bytes, bars + stage);
-            }
-        }
-        if (!a.bulk) __syncthreads();
-        stage = stage + 1 == nst ? 0 : stage + 1;
-    }
-}
-
-size_t nms_up_corner_w_smem(int h, int w, int nbr, int nbc, int nst)
-{
-    return corner_w_layout(h, w, nbr, nbc, nst).total;
-}
-
-// ---------------------------------------------------------------------------
-// k_nms_up_corner_g — warp per plane, sources read through L1/L2 instead of
-// a shared-memory copy.  A shared plane buffer (15 KB at 46x82) caps a CTA
-// design at ~5 resident CTAs per SM, and the per-plane chain (hot words ->
-// hot cells -> chain prune -> classify -> exact test) is latency bound, so
-// residency is what sets the speed.  Here a warp needs ~2 KB of shared
-// memory, 32 warps stay resident per SM, and every warp runs its planes
-// start to finish with warp-synchronous steps only:
-//   hot words  — batches of kGwBatch row-aligned loads in flight per lane
-//                (lane = column), one ballot per (source row, 32 columns);
-//                the warp's next plane is prefetched into L2 meanwhile;
-//   hot cells  — lane = band row p: C_j = M | M << 1 (+ carry),
-//                M = hot(p-1) | hot(p); a warp scan places every lane's
-//                cells into the warp's list (flushed whenever it fills);
-//   flush      — chain_pruned on full lanes, process_cell on the survivors;
-//   exact test — 9 lanes per candidate.  A candidate-list overflow sends the
-//                plane to an exact warp-level rescan instead.
-constexpr int kGwThreads = 256;
-constexpr int kGwWarps = kGwThreads / kWarp;
-constexpr int kGwList = 256;
-constexpr int kGwCand = 64;
-constexpr int kGwBatch = 16;
-
-__host__ __device__ inline int gw_row_stride(int w)
-{
-    const int nws = (w + 31) >> 5;
-    return nws | 1;                      // odd: conflict-free lane-per-row reads
-}
-
-__host__ __device__ inline size_t gw_smem(int h, int w)
-{
-    return (size_t)kGwWarps * ((size_t)h * gw_row_stride(w) + kGwList + kGwCand) * sizeof(uint32_t);
-}
-
-__device__ __noinline__ void redo_plane_g(const UpCornerArgs &a, const Bands &bd, const float *S, int plane,
-                                          int lane)
-{
-    for (int t = lane; t < a.nbr * a.nbc; t += kWarp) {
-        const int p = t / a.nbc, q = t - p * a.nbc;
-        const int4 rb = bd.rb[p], cb = bd.cb[q];
-        const CellF c = cellf(S, a.w, rb, cb);
-        if (!(c.a0 >= a.thr || c.a1 >= a.thr || c.b0 >= a.thr || c.b1 >= a.thr)) continue;
-        for (int y = rb.x; y <= rb.y; ++y)
-            for (int x = cb.x; x <= cb.y; ++x) {
-                float v;
-                if (exact_peak(a, S, y, x, v)) emit_peak_c(a.counts, a.peaks, plane, a.cap, v, y, x);
-            }
-    }
-}
-
-__global__ void __launch_bounds__(kGwThreads, 4)
-k_nms_up_corner_g(const UpCornerArgs a)
-{
-    extern __shared__ __align__(16) uint32_t smg[];
-    const int h = a.h, w = a.w, hw = h * w;
-    const int nbr = a.nbr, nbc = a.nbc;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rs = gw_row_stride(w);
-    uint32_t *R = smg + (size_t)warp * h * rs;
-    uint32_t *list = smg + (size_t)kGwWarps * h * rs + warp * kGwList;
-    uint32_t *cand = smg + (size_t)kGwWarps * (h * rs + kGwList) + warp * kGwCand;
-    __shared__ int n_cand[kGwWarps];
-    const CandList cl{cand, &n_cand[warp], kGwCand};
-    const Bands bd{a.rband, a.cband, a.rbt, a.cbt};
-    const int P = a.B * a.K;
-    const int nws = (w + 31) >> 5;               // source-row words
-    const int nwc = (nbc + 31) >> 5;             // band-row cell words
-    const int U = h * nws;
-    const int nwarps = gridDim.x * kGwWarps;
-    if (lane == 0) n_cand[warp] = 0;
-    __syncwarp();
-
-    for (int pl = blockIdx.x * kGwWarps + warp; pl < P; pl += nwarps) {
-        const int fb = pl / a.K, k = pl - fb * a.K;
-        const float *S = a.conf + ((size_t)fb * a.C + k) * (size_t)hw;
-        {
-            const int nx = pl + nwarps;          // this warp's next plane -> L2
-            if (nx < P) {
-                const int nb = nx / a.K, nk = nx - nb * a.K;
-                const char *Sn = reinterpret_cast<const char *>(a.conf + ((size_t)nb * a.C + nk) * (size_t)hw);
-                for (int o = lane * 128; o < hw * 4; o += kWarp * 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(Sn + o));
-            }
-        }
-
-        // ---- hot words R[r][j] (bit = column 32j + lane >= thr)
-        {
-            int r = 0, j = 0;
-            for (int u0 = 0; u0 < U; u0 += kGwBatch) {
-                float v[kGwBatch];
-                int rr = r, jj = j;
-#pragma unroll
-                for (int i = 0; i < kGwBatch; ++i) {
-                    const int col = (jj << 5) + lane;
-                    v[i] = (u0 + i < U && col < w) ? __ldg(S + rr * w + col) : -INFINITY;
-                    if (++jj == nws) { jj = 0; ++rr; }
-                }
-                uint32_t mine = 0u;
-#pragma unroll
-                for (int i = 0; i < kGwBatch; ++i) {
-                    const uint32_t word = __ballot_sync(0xffffffffu, v[i] >= a.thr);
-                    if (lane == i) mine = word;
-                }
-                const int u = u0 + lane;
-                if (lane < kGwBatch && u < U) {
-                    const int ur = u / nws;
-                    R[ur * rs + (u - ur * nws)] = mine;
-                }
-                r = rr; j = jj;
-            }
-        }
-        __syncwarp();
-
-        // ---- hot cells: lane = band row, warp scan into the list
-        int nl = 0;
-        for (int pg = 0; pg < nbr; pg += kWarp) {
-            const int p = pg + lane;
-            uint32_t cw[kMaxRowWords];
-            int cnt = 0;
-            uint32_t carry = 0u;
-#pragma unroll
-            for (int jw = 0; jw < kMaxRowWords; ++jw) {
-                uint32_t c = 0u;
-                if (jw < nwc && p < nbr) {
-                    uint32_t m = 0u;
-                    if (jw < nws) {
-                        if (p >= 1) m |= R[(p - 1) * rs + jw];
-                        if (p < h) m |= R[p * rs + jw];
-                    }
-                    c = m | (m << 1) | carry;
-                    carry = m >> 31;
-                    const int left = nbc - (jw << 5);
-                    if (left < 32) c &= (1u << left) - 1u;
-                }
-                cw[jw] = c;
-                cnt += __popc(c);
-            }
-            int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < kWarp; d <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += t;
-            }
-            const int total = __shfl_sync(0xffffffffu, incl, kWarp - 1);
-            if (total == 0) continue;
-            const int excl = incl - cnt;
-            int w0 = 0;
-            while (true) {
-                const int room = kGwList - nl;
-                int idx = excl;
-#pragma unroll
-                for (int jw = 0; jw < kMaxRowWords; ++jw) {
-                    uint32_t c = cw[jw];
-                    while (c) {
-                        const int bit = __ffs(c) - 1;
-                        c &= c - 1u;
-                        if (idx >= w0 && idx < w0 + room)
-                            list[nl + idx - w0] = (uint32_t(p) << 16) | uint32_t((jw << 5) + bit);
-                        ++idx;
-                    }
-                }
-                const int wrote = min(total - w0, room);
-                nl += wrote;
-                w0 += wrote;
-                __syncwarp();
-                if (w0 >= total) break;
-                flush_cells(a, bd, cl, S, pl, list, nl, lane);
-                nl = 0;
-            }
-        }
-        if (nl) flush_cells(a, bd, cl, S, pl, list, nl, lane);
-
-        // ---- exact 3x3 test of the candidates, 9 lanes each
-        const int ncd = n_cand[warp];
-        __syncwarp();
-        if (lane == 0) n_cand[warp] = 0;
-        if (ncd > kGwCand) {
-            redo_plane_g(a, bd, S, pl, lane);    // nothing of this plane was emitted yet
-        } else {
-            const int grp = lane / 9, nb = lane - grp * 9;
-            const int src = min(grp, 2) * 9;
-            for (int base = 0; base < ncd; base += 3) {
-                const int ci = base + grp;
-                const bool act = grp < 3 && ci < ncd;
-                int y = 0, x = 0;
-                float val = -INFINITY;
-                if (act) {
-                    const uint32_t yx = cand[ci];
-                    y = (int)(yx >> 16);
-                    x = (int)(yx & 0xffffu);
-                    val = exact_value(a, S, y + nb / 3 - 1, x + nb % 3 - 1);
-                }
-                float nv[9];
-#pragma unroll
-                for (int kk = 0; kk < 9; ++kk) nv[kk] = __shfl_sync(0xffffffffu, val, src + kk);
-                if (act && nb == 4) {
-                    const float v = nv[4];
-                    // paf.py:95-99: earlier neighbours strictly, later ones non-strictly
-                    if (v >= a.thr && v > nv[0] && v > nv[1] && v > nv[2] && v > nv[3] && v >= nv[5] &&
-                        v >= nv[6] && v >= nv[7] && v >= nv[8])
-                        emit_peak_c(a.counts, a.peaks, pl, a.cap, v, y, x);
-                }
-            }
-        }
-        __syncwarp();
-    }
+#endif
 }
 
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst)
@@ -1117,54 +714,66 @@ cudaError_t launch_nms_up_corner(const UpCornerArgs &a_in, cudaStream_t s)
     UpCornerArgs a = a_in;
     const long long P = (long long)a.B * a.K;
     if (P == 0) return cudaSuccess;
-    if (a.variant == 1 && a.w <= 32 * kMaxRowWords && a.nbc <= 32 * kMaxRowWords && P < (1ll << 30)) {
-        int dev = 0, sms = 0, occ = 0;
-        const size_t smem = gw_smem(a.h, a.w);
-        cudaError_t e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nms_up_corner_g, kGwThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) return cudaErrorInvalidConfiguration;
-        const long long grid = std::min<long long>((P + kGwWarps - 1) / kGwWarps, (long long)occ * sms);
-        k_nms_up_corner_g<<<(unsigned)grid, kGwThreads, smem, s>>>(a);
-        return cudaGetLastError();
-    }
-    const bool wk = a.warp_rows && a.w <= 32 * kMaxRowWords && a.nbc <= 32 * kMaxRowWords;
-    const size_t smem = wk ? nms_up_corner_w_smem(a.h, a.w, a.nbr, a.nbc, a.nst)
-                           : nms_up_corner_smem(a.h, a.w, a.nbr, a.nbc, a.nst);
+    const size_t smem = nms_up_corner_smem(a.h, a.w, a.nbr, a.nbc, a.nst);
     int dev = 0, sms = 0, occ = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
-        e = wk ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nms_up_corner_w, kCornerThreads, smem)
-               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nms_up_corner, kCornerThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nms_up_corner<3>, kCornerThreads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     // bulk copies need 16-byte aligned, 16-byte multiple planes
     a.bulk = ((size_t)a.h * a.w * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(a.conf) & 15) == 0;
     const long long grid = std::min<long long>(P, (long long)occ * sms);
-    if (wk) k_nms_up_corner_w<<<(unsigned)grid, kCornerThreads, smem, s>>>(a);
-    else k_nms_up_corner<<<(unsigned)grid, kCornerThreads, smem, s>>>(a);
+    switch ((a.w + 31) >> 5) {
+    case 1: k_nms_up_corner<1><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    case 2: k_nms_up_corner<2><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    case 3: k_nms_up_corner<3><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    case 4: k_nms_up_corner<4><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    case 5: k_nms_up_corner<5><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    case 6: k_nms_up_corner<6><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    case 7: k_nms_up_corner<7><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    default: k_nms_up_corner<8><<<(unsigned)grid, kCornerThreads, smem, s>>>(a); break;
+    }
     return cudaGetLastError();
 }
 
-cudaError_t configure_corner_kernels(int max_smem)
+template <int NWS>
+static cudaError_t configure_corner(int max_smem)
 {
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, k_nms_up_corner);
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_nms_up_corner<NWS>);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_nms_up_corner, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 max_smem - (int)fa.sharedSizeBytes);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_nms_up_corner_g);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_nms_up_corner_g, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 max_smem - (int)fa.sharedSizeBytes);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_nms_up_corner_w);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_nms_up_corner_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(k_nms_up_corner<NWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem - (int)fa.sharedSizeBytes);
     return e;
 }
 
+cudaError_t configure_corner_kernels(int max_smem)
+{
+    cudaError_t e = configure_corner<1>(max_smem);
+    if (e == cudaSuccess) e = configure_corner<2>(max_smem);
+    if (e == cudaSuccess) e = configure_corner<3>(max_smem);
+    if (e == cudaSuccess) e = configure_corner<4>(max_smem);
+    if (e == cudaSuccess) e = configure_corner<5>(max_smem);
+    if (e == cudaSuccess) e = configure_corner<6>(max_smem);
+    if (e == cudaSuccess) e = configure_corner<7>(max_smem);
+    if (e == cudaSuccess) e = configure_corner<8>(max_smem);
+    return e;
+}
+
 }  // namespace pf
+
+#ifdef PF_CORNER_PROF
+// development builds only: read (and reset) the per-phase cycle counters
+extern "C" int pf_corner_prof_read(unsigned long long *out, int reset)
+{
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, pf::g_corner_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 4;
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(pf::g_corner_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

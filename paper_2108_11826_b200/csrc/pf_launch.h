@@ -6,6 +6,14 @@
 
 namespace pf {
 
+// One output coordinate of operators.bilinear_resize packed for a single
+// 16-byte load: i0 | i1 << 16, t (1 - t is recomputed: the host's omt is the
+// same single rounded subtraction).
+struct __align__(16) AxisRec {
+    int32_t i01;
+    int32_t pad;
+    double t;
+};
 // pf_nms.cu
 struct UpArgs {
     const float *conf;
@@ -40,8 +48,8 @@ struct UpWinArgs {
 };
 size_t nms_up_win_smem(int h, int w, int H, int threads);
 
-// Per band, fp32 copies of the axis weights the corner kernels' classification
-// uses (built on the host for k_nms_up_corner_g, in-kernel for the others).
+// Per band, fp32 copies of the axis weights the corner kernel's classification
+// uses (filled in-kernel from the axis tables).
 struct BandT {
     float omt_f, t_f, omt_l, t_l;   // (1 - t), t at the band's first and last output
     float s_l, s_f, dt, pad;        // t step into the last output, out of the first; min step
@@ -65,12 +73,13 @@ struct UpCornerArgs {
     int nst;                             // plane stages in shared memory
     int bulk;                            // set by the launcher: planes fetched by cp.async.bulk
     int chain;                           // chain pre-filter allowed (output t steps >= 2^-5)
-    int warp_rows;                       // k_nms_up_corner_w (warp-autonomous band rows)
-    int variant;                         // 0: CTA per plane (smem stages), 1: warp per plane (global)
-    const BandT *rbt, *cbt;              // per band fp32 weights (variant 1)
+    const AxisRec *rrec, *crec;          // packed per-output axis records
 };
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
-constexpr int kCornerStages = 2;
+#ifndef PF_CORNER_STAGES
+#define PF_CORNER_STAGES 1
+#endif
+constexpr int kCornerStages = PF_CORNER_STAGES;
 cudaError_t launch_nms_up_corner(const UpCornerArgs &a, cudaStream_t s);
 cudaError_t configure_corner_kernels(int max_smem);
 cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s);
@@ -81,14 +90,6 @@ cudaError_t launch_nms_up(const UpArgs &a, int B, size_t smem, cudaStream_t s);
 cudaError_t configure_nms_kernels(int max_smem);
 
 // pf_parse.cu
-// One output coordinate of operators.bilinear_resize packed for a single
-// 16-byte load: i0 | i1 << 16, t (1 - t is recomputed: the host's omt is the
-// same single rounded subtraction).
-struct __align__(16) AxisRec {
-    int32_t i01;
-    int32_t pad;
-    double t;
-};
 struct ParseArgs {
     Topo topo;
     const float *paf;

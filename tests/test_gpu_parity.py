@@ -354,9 +354,7 @@ def test_corner_chain_prefilter_is_exact(topo, up):
         params = pf.ParserParams(upsample=up, conf_threshold=thr)
         e1 = pf.PafParser(topo, debug=True)
         runs = []
-        for layout, no_chain in ((2, 0), (2, 1), (1, 0), (0, 1), (0, 0)):
-            # 2: warp per plane (default), 1: warp band rows, 0: CTA phases
-            e1.ctx.set_option(pf._native.PF_OPT_CORNER_WARP_ROWS, layout)
+        for no_chain in (0, 1):
             e1.ctx.set_option(pf._native.PF_OPT_NO_CHAIN, no_chain)
             e1.parse_arrays(conf, paf, 48, params)      # stride divisible by every tested factor
             runs.append([e1.peaks(f) for f in range(3)])
