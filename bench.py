@@ -43,9 +43,8 @@ CONF_FRAME_BYTES = (K_PARTS + 1) * PLANE * 4        # 286,672
 PAF_FRAME_BYTES = 2 * N_LIMBS * PLANE * 4           # 573,344
 # SURVEY.md §8(d) algorithmic bytes per frame
 BYTES_FUSED_UN = K_PARTS * PLANE * 4                # 271,584: read low-res part maps once
-BYTES_UPSAMPLE = (K_PARTS + 1) * PLANE * 4 + (K_PARTS + 1) * PLANE * 64 * 4   # read low + write full (19 ch materialised)
+BYTES_UPSAMPLE = K_PARTS * PLANE * 4 + K_PARTS * PLANE * 64 * 4   # 17,652,960: read low + write full (18 part ch)
 BYTES_NMS_FULL = K_PARTS * PLANE * 64 * 4           # 17,381,376: read full-res part maps
-BYTES_PARSE = PAF_FRAME_BYTES                       # PAF planes the line integral samples
 
 
 def ncu_traffic(kernel: str, frames_per_launch: float):
@@ -63,6 +62,21 @@ def ncu_traffic(kernel: str, frames_per_launch: float):
         for name, val in d.items():
             if name != "frames_per_launch" and name.split("<")[0].startswith(kernel):
                 best = (val / d["frames_per_launch"]) * frames_per_launch
+    return best
+
+
+def paf_in_place_bytes():
+    """PCIe read bytes per frame of the in-place (zero-copy) PAF reads of
+    k_parse_frames, from the committed ncu capture (profiles/*_e2e_pcie.json)."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_e2e_pcie.json"))):
+        try:
+            with open(path) as f:
+                best = (float(json.load(f)["paf_read_in_place_bytes_per_frame"]), os.path.basename(path))
+        except Exception:
+            continue
     return best
 
 
@@ -274,7 +288,13 @@ def run_b200(args, rank, world, local_rank):
     e2e_s = time.perf_counter() - t0
     e2e_s = max_over_ranks(e2e_s)
     e2e_value = world * E * e2e_steps / e2e_s
-    h2d = E * (K_PARTS * PLANE * 4 + PAF_FRAME_BYTES)     # background plane not shipped
+    # conf: K of K+1 planes copied (the background plane is never read);
+    # PAF: read in place from pinned host memory by k_parse_frames, so only
+    # the sampled cells cross PCIe (ncu pcie__read_bytes, committed profile)
+    paf_rd = paf_in_place_bytes()
+    h2d_conf = E * K_PARTS * PLANE * 4
+    h2d_paf = E * paf_rd[0] if paf_rd else E * PAF_FRAME_BYTES
+    h2d = int(h2d_conf + h2d_paf)
     d2h = E * 8 + 32 + r.total_humans * (8 + 4 + K_PARTS * (8 + 8 + 4 + 4))
 
     # ---- unfused Mode U stages (materialised x8 maps through HBM) ----
@@ -307,17 +327,25 @@ def run_b200(args, rank, world, local_rank):
     chunk = 1024
     launches_per_step = {name: n / args.steps for name, (ms, n) in ktimes.items()}
     per_frame_bytes = {"k_nms_up": BYTES_FUSED_UN, "k_nms_up_win": BYTES_FUSED_UN,
-                       "k_nms_up_corner": BYTES_FUSED_UN, "k_nms_plane": BYTES_FUSED_UN,
-                       "k_parse_frames": BYTES_PARSE}
+                       "k_nms_up_corner": BYTES_FUSED_UN, "k_nms_plane": BYTES_FUSED_UN}
     for name, (ms, n) in ktimes.items():
         frames_per_launch = F / launches_per_step[name]
         per_launch = ms / n
-        b = per_frame_bytes.get(name, 0) * frames_per_launch
         stages[name] = {"ms_per_launch": per_launch, "launches": n,
                         "frames_per_launch": frames_per_launch,
-                        "share_of_step": ms / max(elapsed_ms, 1e-9),
-                        "bytes_per_launch": b,
-                        "achieved_gbs": b / (per_launch / 1e3) / 1e9 if b else None}
+                        "us_per_frame": per_launch * 1e3 / frames_per_launch,
+                        "share_of_step": ms / max(elapsed_ms, 1e-9)}
+        if name in per_frame_bytes:
+            b = per_frame_bytes[name] * frames_per_launch
+            stages[name].update({"bytes_per_launch": b, "bytes_kind": "algorithmic",
+                                 "achieved_gbs": b / (per_launch / 1e3) / 1e9})
+        else:
+            # latency-bound gather (the line integral reads only the sampled PAF
+            # cells): report its measured DRAM traffic, not a roofline
+            t = ncu_traffic(name, frames_per_launch)
+            stages[name].update({"bytes_per_launch": t, "bytes_kind": "ncu dram read+write",
+                                 "achieved_gbs": t / (per_launch / 1e3) / 1e9 if t else None,
+                                 "bound": "latency (gather + serial assembly)"})
     dominant = max(ktimes.items(), key=lambda kv: kv[1][0])[0] if ktimes else None
     roof = None
     if dominant:
@@ -359,7 +387,11 @@ def run_b200(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "frames_per_step": E, "steps": e2e_steps,
                     "h2d_gbs": h2d * e2e_steps * world / e2e_s / 1e9,
-                    "path": "pf_parse_host (pinned host maps -> H2D -> kernels -> D2H humans)"},
+                    "h2d_conf_copied": h2d_conf, "h2d_paf_read_in_place": int(h2d_paf),
+                    "h2d_paf_source": (f"ncu pcie__read_bytes of k_parse_frames, profiles/{paf_rd[1]}"
+                                       if paf_rd else "whole PAF (no capture committed)"),
+                    "path": "pf_parse_host (pinned host maps: conf planes H2D by copy engine, PAF read "
+                            "in place over PCIe by the parse kernel -> kernels -> D2H humans)"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

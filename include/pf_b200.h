@@ -161,6 +161,8 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_GENERIC_FUSED 4   /* use the shared-memory tile kernel for Mode U */
 #define PF_OPT_WIN_VARIANT 5     /* Mode U 3x3 kernel: 4 corner-pruned (default), 3/2/1 strip kernels */
 #define PF_OPT_NO_CHAIN 6        /* corner kernel: disable the chain pre-filter (A/B parity checks) */
+#define PF_OPT_PAF_ZERO_COPY 8   /* pf_parse_host (default 1): a pinned host PAF is read in place by the
+                                    parse kernel, so only the sampled cells cross PCIe; 0: copy it whole */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch

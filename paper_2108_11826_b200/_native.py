@@ -24,6 +24,7 @@ PF_MAX_KEYPOINTS, PF_MAX_LIMBS = 32, 64
 PF_OPT_DEBUG, PF_OPT_TIMING, PF_OPT_MATERIALISE, PF_OPT_GENERIC_FUSED = 1, 2, 3, 4
 PF_OPT_WIN_VARIANT = 5
 PF_OPT_NO_CHAIN = 6
+PF_OPT_PAF_ZERO_COPY = 8
 PF_N_KERNELS = 9
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)

@@ -173,6 +173,7 @@ struct pf_ctx {
     int generic_fused = 0;
     int win_variant = 4;
     int no_chain = 0;
+    int paf_zero_copy = 1;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double kernel_ms[PF_N_KERNELS] = {0};
@@ -518,16 +519,20 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         CU(launch_nms_up(a, n, smem, s));
     } else {
         // materialised: resize (if up > 1) -> blur (if sigma > 0) -> NMS
-        const size_t frame_full = (size_t)C * H * W;
+        // materialised maps hold the K part channels only ([n][K][H][W]);
+        // the background channel is never read (paf.py:300)
+        const size_t frame_full = (size_t)K * H * W;
         int rc = ensure_full(ctx, (size_t)n * frame_full);
         if (rc) return rc;
         const float *nms_src = conf;
+        int nms_C = C;
         long long src_frame = (long long)C * h * w;
         if (up > 1) {
             KernelTimer kt(ctx, kResize);
-            CU(launch_resize_planes(conf, (long long)n * C, h, w, ctx->d_full, H, W, rows->dev(),
-                                    cols->dev(), ctx->sms, s));
+            CU(launch_resize_planes(conf, (long long)C * h * w, K, (long long)n * K, h, w, ctx->d_full, H, W,
+                                    rows->d_rec, cols->d_rec, s));
             nms_src = ctx->d_full;
+            nms_C = K;
             src_frame = (long long)frame_full;
         }
         if (blur) {
@@ -537,9 +542,10 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             CU(launch_blur(nms_src, src_frame, ctx->d_tmp, ctx->d_full, (long long)frame_full, n, K,
                            H, W, taps, ctx->sms, s));
             nms_src = ctx->d_full;
+            nms_C = K;
         }
         KernelTimer kt(ctx, kNmsPlane);
-        CU(launch_nms_plane(nms_src, n, C, K, H, W, thr, half, ctx->caps.max_peaks_per_part,
+        CU(launch_nms_plane(nms_src, n, nms_C, K, H, W, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
     }
 
@@ -901,6 +907,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_GENERIC_FUSED: ctx->generic_fused = value ? 1 : 0; return PF_OK;
     case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 4) ? value : 4; return PF_OK;
     case PF_OPT_NO_CHAIN: ctx->no_chain = value ? 1 : 0; return PF_OK;
+    case PF_OPT_PAF_ZERO_COPY: ctx->paf_zero_copy = value ? 1 : 0; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }
@@ -1064,7 +1071,21 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     rc = prepare_axes(ctx, grid_h, grid_w, p, &rows, &cols);
     if (rc) return rc;
     int chunk = chunk_for(ctx, p, grid_h, grid_w);
-    if (chunk > 256) chunk = 256;   // copy/compute overlap granularity
+#ifndef PF_HOST_CHUNK
+#define PF_HOST_CHUNK 256
+#endif
+    if (chunk > PF_HOST_CHUNK) chunk = PF_HOST_CHUNK;   // copy/compute overlap granularity
+    // PF_OPT_PAF_ZERO_COPY: a pinned (mapped) host PAF is read in place by
+    // k_parse_frames over PCIe -- only the sampled cells cross the link
+    // instead of the whole 2L-channel field.
+    const float *paf_dev = nullptr;
+    if (ctx->paf_zero_copy && L > 0) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, paf) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer != nullptr)
+            paf_dev = static_cast<const float *>(pa.devicePointer);
+        cudaGetLastError();
+    }
     rc = ensure_nms_ws(ctx, chunk, K);
     if (rc) return rc;
     const size_t plane = (size_t)grid_h * grid_w;
@@ -1090,12 +1111,13 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
         CU(cudaMemcpy2DAsync(dconf, conf_frame * sizeof(float), conf + (size_t)f0 * conf_frame,
                              conf_frame * sizeof(float), (size_t)K * plane * sizeof(float), n,
                              cudaMemcpyHostToDevice, ctx->copy_stream));
-        if (L > 0)
+        if (L > 0 && !paf_dev)
             CU(cudaMemcpyAsync(dpaf, paf + (size_t)f0 * paf_frame, (size_t)n * paf_frame * sizeof(float),
                                cudaMemcpyHostToDevice, ctx->copy_stream));
         CU(cudaEventRecord(ctx->ev_copied[sl], ctx->copy_stream));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[sl], 0));
-        rc = run_chunk(ctx, dconf, dpaf, n, f0, grid_h, grid_w, stride, p, rows, cols, pool);
+        rc = run_chunk(ctx, dconf, paf_dev ? paf_dev + (size_t)f0 * paf_frame : dpaf, n, f0, grid_h, grid_w,
+                       stride, p, rows, cols, pool);
         if (rc) return rc;
         CU(cudaEventRecord(ctx->ev_free[sl], ctx->stream));
     }
@@ -1222,8 +1244,8 @@ int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int 
     rc = get_axis(ctx, in_w, out_w, &c);
     if (rc) return rc;
     KernelTimer kt(ctx, kResize);
-    CU(launch_resize_planes(src, n_planes, in_h, in_w, dst, out_h, out_w, r->dev(), c->dev(), ctx->sms,
-                            ctx->stream));
+    CU(launch_resize_planes(src, (long long)in_h * in_w, 1, n_planes, in_h, in_w, dst, out_h, out_w, r->d_rec,
+                            c->d_rec, ctx->stream));
     return PF_OK;
 }
 

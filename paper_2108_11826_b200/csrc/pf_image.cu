@@ -63,36 +63,62 @@ k_preprocess(const Tin *__restrict__ src, int h, int w, float *__restrict__ dst,
     }
 }
 
-// operators.py:102-107 (2-D branch) applied per plane: [P][h][w] -> [P][H][W].
-// Each thread produces 4 consecutive outputs of one row (float4 store when
-// W % 4 == 0).
-__global__ void __launch_bounds__(256)
-k_resize_planes(const float *__restrict__ src, int h, int w, float *__restrict__ dst,
-                int H, int W, AxisTab rows, AxisTab cols, long long total_quads, int quads_per_row)
+// operators.py:102-107 (2-D branch) applied per plane: [P][h][w] -> [P][H][W]
+// (source plane p at (p / K) * src_frame + (p % K) * h * w, so the part
+// channels can be taken out of a [K+1]-channel tensor).  HBM-write bound: a
+// thread owns 4 adjacent output columns of a band of kResizeRows output
+// rows; its column records are loaded once, and the row interpolants
+// top = a*(1-tx) + b*tx, bot = c*(1-tx) + d*tx are recomputed only when the
+// source row pair changes (8 output rows share one at x8), so an output costs
+// 2 DMUL + 1 DADD + 1 F2F and a 16-byte store.  Same op order as bilerp().
+constexpr int kResizeRows = 32;
+constexpr int kResizeThreads = 128;
+
+__global__ void __launch_bounds__(kResizeThreads)
+k_resize_planes(const float *__restrict__ src, long long src_frame, int K, int h, int w,
+                float *__restrict__ dst, int H, int W, const AxisRec *__restrict__ rrec,
+                const AxisRec *__restrict__ crec, int n_row_blocks)
 {
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_quads;
-         q += (long long)gridDim.x * blockDim.x) {
-        const long long row_id = q / quads_per_row;          // plane * H + y
-        const int x0 = int(q - row_id * quads_per_row) * 4;
-        const long long plane = row_id / H;
-        const int y = int(row_id - plane * H);
-        const float *s = src + plane * (long long)h * w;
-        const int i0 = __ldg(rows.i0 + y), i1 = __ldg(rows.i1 + y);
-        const double ty = __ldg(rows.t + y), omty = __ldg(rows.omt + y);
-        const float *r0 = s + (size_t)i0 * w, *r1 = s + (size_t)i1 * w;
+    const int x0 = (blockIdx.x * kResizeThreads + threadIdx.x) * 4;
+    if (x0 >= W) return;
+    const long long plane = blockIdx.y / n_row_blocks;
+    const int y_lo = (int)(blockIdx.y - plane * n_row_blocks) * kResizeRows;
+    const int y_hi = min(H, y_lo + kResizeRows);
+    const float *s = src + (plane / K) * src_frame + (plane % K) * (long long)h * w;
+    float *d = dst + plane * (long long)H * W;
+    int j0[4], j1[4];
+    double tx[4], omtx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int4 r = __ldg(reinterpret_cast<const int4 *>(crec + min(x0 + k, W - 1)));
+        j0[k] = r.x & 0xffff;
+        j1[k] = r.x >> 16;
+        tx[k] = __hiloint2double(r.w, r.z);
+        omtx[k] = __dsub_rn(1.0, tx[k]);
+    }
+    int cur = -1;
+    double top[4], bot[4];
+    const bool vec = (W & 3) == 0 && x0 + 3 < W;
+    for (int y = y_lo; y < y_hi; ++y) {
+        const int4 r = __ldg(reinterpret_cast<const int4 *>(rrec + y));
+        if (r.x != cur) {
+            cur = r.x;
+            const float *r0 = s + (size_t)(r.x & 0xffff) * w, *r1 = s + (size_t)(r.x >> 16) * w;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                top[k] = dadd(dmul((double)__ldg(r0 + j0[k]), omtx[k]), dmul((double)__ldg(r0 + j1[k]), tx[k]));
+                bot[k] = dadd(dmul((double)__ldg(r1 + j0[k]), omtx[k]), dmul((double)__ldg(r1 + j1[k]), tx[k]));
+            }
+        }
+        const double ty = __hiloint2double(r.w, r.z), omty = __dsub_rn(1.0, ty);
         float out[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int x = min(x0 + k, W - 1);
-            const int j0 = __ldg(cols.i0 + x), j1 = __ldg(cols.i1 + x);
-            out[k] = bilerp(__ldg(r0 + j0), __ldg(r0 + j1), __ldg(r1 + j0), __ldg(r1 + j1),
-                            __ldg(cols.t + x), __ldg(cols.omt + x), ty, omty);
-        }
-        float *d = dst + row_id * W + x0;
-        if ((W & 3) == 0) {
-            *reinterpret_cast<float4 *>(d) = make_float4(out[0], out[1], out[2], out[3]);
+        for (int k = 0; k < 4; ++k) out[k] = __double2float_rn(dadd(dmul(top[k], omty), dmul(bot[k], ty)));
+        float *o = d + (size_t)y * W + x0;
+        if (vec) {
+            __stcs(reinterpret_cast<float4 *>(o), make_float4(out[0], out[1], out[2], out[3]));
         } else {
-            for (int k = 0; k < 4 && x0 + k < W; ++k) d[k] = out[k];
+            for (int k = 0; k < 4 && x0 + k < W; ++k) o[k] = out[k];
         }
     }
 }
@@ -170,14 +196,24 @@ cudaError_t launch_preprocess(const void *src, int src_is_f32, int B, int h, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_resize_planes(const float *src, long long P, int h, int w, float *dst, int H, int W,
-                                 AxisTab rows, AxisTab cols, int sms, cudaStream_t s)
+cudaError_t launch_resize_planes(const float *src, long long src_frame, int K, long long P, int h, int w,
+                                 float *dst, int H, int W, const AxisRec *rrec, const AxisRec *crec,
+                                 cudaStream_t s)
 {
-    const int qpr = (W + 3) / 4;
-    const long long total = P * H * qpr;
-    if (total == 0) return cudaSuccess;
-    k_resize_planes<<<grid_for(total, 256, sms), 256, 0, s>>>(src, h, w, dst, H, W, rows, cols, total, qpr);
-    return cudaGetLastError();
+    if (P == 0 || H == 0 || W == 0) return cudaSuccess;
+    const int nrb = (H + kResizeRows - 1) / kResizeRows;
+    const unsigned gx = (unsigned)(((W + 3) / 4 + kResizeThreads - 1) / kResizeThreads);
+    // grid.y <= 65535: launch whole frames (K planes) at a time
+    long long per = (65535 / nrb) / K * K;
+    if (per < K) return cudaErrorInvalidConfiguration;
+    for (long long p0 = 0; p0 < P; p0 += per) {      // P is a multiple of K
+        const long long n = P - p0 < per ? P - p0 : per;
+        k_resize_planes<<<dim3(gx, (unsigned)(n * nrb)), kResizeThreads, 0, s>>>(
+            src + (p0 / K) * src_frame, src_frame, K, h, w, dst + p0 * (long long)H * W, H, W, rrec, crec, nrb);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_blur(const float *src, long long src_frame, float *tmp, float *dst,

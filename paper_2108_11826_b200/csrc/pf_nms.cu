@@ -55,15 +55,47 @@ k_nms_plane(const float *__restrict__ conf, int C, int K, int H, int W, float th
     const float *p = conf + ((size_t)b * C + k) * (size_t)H * W;
     const int HW = H * W;
     if ((HW & 3) == 0 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        // HBM-read bound: kNmsUnroll 16-byte loads in flight per thread, the
+        // (rare) cells >= thr then look at their neighbours through L1
         const float4 *p4 = reinterpret_cast<const float4 *>(p);
-        for (int e4 = threadIdx.x; e4 < (HW >> 2); e4 += blockDim.x) {
-            const float4 v4 = __ldg(p4 + e4);
-            const float vs[4] = {v4.x, v4.y, v4.z, v4.w};
+        const int n4 = HW >> 2;
+        constexpr int kNmsUnroll = 4;
+        const int lane = threadIdx.x & 31;
+        // warp-uniform trip count (the row-neighbour shuffles need every lane)
+        for (int bw = threadIdx.x - lane; bw < n4; bw += kNmsUnroll * blockDim.x) {
+            const int b4 = bw + lane;
+            float4 v4[kNmsUnroll];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (!(vs[q] >= thr)) continue;
-                const int e = e4 * 4 + q, i = e / W, j = e - i * W;
-                if (plane_is_peak(p, H, W, i, j, vs[q], half)) emit_peak(counts, peaks, plane, cap, vs[q], i, j);
+            for (int u = 0; u < kNmsUnroll; ++u) {
+                const int e4 = b4 + u * blockDim.x;
+                v4[u] = e4 < n4 ? __ldg(p4 + e4) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            }
+#pragma unroll
+            for (int u = 0; u < kNmsUnroll; ++u) {
+                const float vs[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+                const int e4 = b4 + u * blockDim.x;
+                // 3x3 window: the row neighbours come from registers (the
+                // adjacent lanes hold the adjacent float4s) and must not beat
+                // the centre (paf.py:95-99: left strictly, right non-strictly)
+                // before the other six neighbours are read
+                const float lft = __shfl_up_sync(0xffffffffu, vs[3], 1);
+                const float rgt = __shfl_down_sync(0xffffffffu, vs[0], 1);
+                if (!(vs[0] >= thr || vs[1] >= thr || vs[2] >= thr || vs[3] >= thr)) continue;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (!(vs[q] >= thr)) continue;
+                    const int e = e4 * 4 + q, i = e / W, j = e - i * W;
+                    if (half == 1) {
+                        // flat neighbours e -/+ 1 are the row neighbours unless j is
+                        // at a row end (then the reference pads -inf); lane 0's left
+                        // and lane 31's right float4 are not in this warp: unknown
+                        const bool have_l = j == 0 || q > 0 || lane > 0, have_r = j == W - 1 || q < 3 || lane < 31;
+                        const float l = j == 0 ? -INFINITY : (q > 0 ? vs[q - 1] : lft);
+                        const float r = j == W - 1 ? -INFINITY : (q < 3 ? vs[q + 1] : rgt);
+                        if ((have_l && !(vs[q] > l)) || (have_r && !(vs[q] >= r))) continue;
+                    }
+                    if (plane_is_peak(p, H, W, i, j, vs[q], half)) emit_peak(counts, peaks, plane, cap, vs[q], i, j);
+                }
             }
         }
     } else {

@@ -270,6 +270,35 @@ def test_device_tensor_path(topo):
     e.close()
 
 
+@pytest.mark.parametrize("up", [1, 8])
+def test_pinned_paf_read_in_place(topo, up):
+    """pf_parse_host with pinned host maps: the PAF read in place over PCIe
+    (PF_OPT_PAF_ZERO_COPY, default) gives the copied path's results and the
+    oracle's, on procedural and crowded frames across several host chunks."""
+    scenes = [pf.procedural_scene(12, s, 656, 368, SP) for s in range(5)] + [pf.crowd_scene(4, 0)]
+    conf, paf = render(scenes, topo)
+    reps = 60                                          # 360 frames: two internal host chunks
+    pc = pf._native.PinnedArray((len(scenes) * reps,) + conf.shape[1:])
+    pp = pf._native.PinnedArray((len(scenes) * reps,) + paf.shape[1:])
+    pc.array[:] = np.concatenate([conf] * reps)
+    pp.array[:] = np.concatenate([paf] * reps)
+    params = pf.ParserParams(upsample=up)
+    e = pf.PafParser(topo)
+    got = e.parse_arrays(pc.array, pp.array, 8, params)
+    in_place = [pf.pose_record(f, got.poses(f), topo) for f in range(len(scenes) * reps)]
+    e.ctx.set_option(pf._native.PF_OPT_PAF_ZERO_COPY, 0)
+    got = e.parse_arrays(pc.array, pp.array, 8, params)
+    copied = [pf.pose_record(f, got.poses(f), topo) for f in range(len(scenes) * reps)]
+    e.close()
+    assert in_place == copied
+    for f in range(len(scenes)):
+        want = oracle_run(conf[f], paf[f], topo, params)
+        assert in_place[f] == record_of(want.humans, topo, f)
+        assert in_place[f + len(scenes) * (reps - 1)].split(",", 1)[1] == in_place[f].split(",", 1)[1]
+    pc.free()
+    pp.free()
+
+
 def test_empty_inputs(eng, topo):
     assert pf.parse_batch([], topo, pf.ParserParams()) == []
     zero = pf.render_feature_maps(pf.GroundTruthScene((), 64, 64), topo, SP)
