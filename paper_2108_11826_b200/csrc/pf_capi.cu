@@ -713,8 +713,8 @@ int chunk_for(pf_ctx *ctx, const pf_params *p, int h, int w)
     const bool materialise = p->blur_sigma > 0.0 ||
                              (p->upsample > 1 && (p->nms_window / 2 > kMaxFusedHalf || ctx->materialise));
     if (materialise) {
-        // bound the full-resolution workspace to ~2 GiB
-        const size_t per = (size_t)(ctx->topo.K + 1) * h * w * p->upsample * p->upsample * sizeof(float);
+        // bound the full-resolution workspace ([chunk][K][H][W]) to ~2 GiB
+        const size_t per = (size_t)ctx->topo.K * h * w * p->upsample * p->upsample * sizeof(float);
         size_t lim = per ? ((size_t)2 << 30) / per : chunk;
         if (lim < 1) lim = 1;
         if ((size_t)chunk > lim) chunk = (int)lim;
