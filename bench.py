@@ -101,6 +101,77 @@ def make_inputs(n_distinct: int, seed: int):
     return topo, conf, paf
 
 
+def other_configs(dev, gpu):
+    """BASELINE.json configs 1-4 (the parity configs) timed on the device
+    with CUDA events, inputs resident: frames/s and the kernel split.  Not
+    part of the headline; run after the timed region (rank 0, N=1)."""
+    import torch
+
+    import paper_2108_11826_b200 as pf
+
+    topo = pf.load_topology("coco18")
+    sp = pf.SynthParams()
+    out = {}
+
+    def timed(name, conf, paf, params, reps):
+        eng = pf.PafParser(topo, device=gpu)
+        c = torch.from_numpy(conf).to(dev)
+        q = torch.from_numpy(paf).to(dev)
+        for _ in range(2):
+            eng.parse_tensors(c, q, STRIDE, params)
+            eng.results()          # automatic capacities grow (and replay) here
+        eng.set_timing(True)
+        eng.kernel_times(reset=True)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        s0.record()
+        for _ in range(reps):
+            eng.parse_tensors(c, q, STRIDE, params)
+        s1.record()
+        torch.cuda.synchronize(dev)
+        ms = s0.elapsed_time(s1) / reps
+        kt = eng.kernel_times(reset=True)
+        n = conf.shape[0]
+        out[name] = {"frames": n, "ms_per_call": ms, "frames_per_s": n / (ms / 1e3),
+                     "humans": int(eng.results().total_humans),
+                     "kernels_ms": {k: v[0] / reps for k, v in kt.items()}}
+        eng.close()
+
+    scene = pf.procedural_scene(0, 1, 656, 368, sp)
+    conf, paf = pf.synth.render_batch([scene], topo, sp)
+    timed("C1 1 frame 3 people, Mode R", conf, paf, pf.ParserParams(upsample=1), 50)
+    timed("C1 1 frame 3 people, Mode U", conf, paf, pf.ParserParams(upsample=8), 50)
+    scenes = [pf.procedural_scene(7, s, 656, 368, sp) for s in range(64)]
+    conf, paf = pf.synth.render_batch(scenes, topo, sp)
+    timed("C2 64 frames 1-5 people, Mode U", conf, paf, pf.ParserParams(upsample=8), 20)
+    scenes = [pf.crowd_scene(42, s) for s in range(256)]
+    conf, paf = pf.synth.render_batch(scenes, topo, sp)
+    timed("C3 256 crowded frames (40 people), Mode R", conf, paf, pf.ParserParams(upsample=1), 5)
+    timed("C3 256 crowded frames (40 people), Mode U", conf, paf, pf.ParserParams(upsample=8), 5)
+    scenes = [pf.GroundTruthScene(pf.crowd_scene(9, s, 1920, 1080, 6, (300.0, 500.0)).humans, 1920, 1080)
+              for s in range(32)]
+    conf, paf = pf.synth.render_batch(scenes, topo, sp)
+    timed("C4 32 frames 1080x1920 (135x240 maps, 6 people), Mode U", conf, paf, pf.ParserParams(upsample=8), 5)
+    # C4 pre-processing: u8 1080x1920 frames -> f32 CHW (same size: layout + /255)
+    frames = torch.randint(0, 256, (32, 1080, 1920, 3), dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        pf.preprocess_batch(frames, 1080, 1920, device=gpu)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    s0.record()
+    for _ in range(10):
+        pf.preprocess_batch(frames, 1080, 1920, device=gpu)
+    s1.record()
+    torch.cuda.synchronize(dev)
+    ms = s0.elapsed_time(s1) / 10
+    nbytes = 32 * (1080 * 1920 * 3 + 3 * 1080 * 1920 * 4)
+    out["C4 pre-processing 32 u8 frames 1080x1920 -> f32 CHW"] = {
+        "frames": 32, "ms_per_call": ms, "frames_per_s": 32 / (ms / 1e3),
+        "achieved_gbs": nbytes / (ms / 1e3) / 1e9, "bytes_per_frame": nbytes // 32,
+        "note": "includes a torch.empty of the output per call"}
+    return out
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi sampled every 200 ms while the timed region runs."""
@@ -398,6 +469,8 @@ def run_b200(args, rank, world, local_rank):
             "clocks": clk,
             "stages": stages,
         }
+        if world == 1 and not args.no_configs:
+            line["configs"] = other_configs(dev, gpu)
         print(json.dumps(line), flush=True)
     eng.close()
 
@@ -418,6 +491,7 @@ def main():
                     help="ncu dram bytes per launch of the dominant kernel (profiles/)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config (C1-C4) timings")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         ap.error("steps >= 1, warmup >= 0")

@@ -129,6 +129,7 @@ struct pf_ctx {
     int *d_counts = nullptr;
     uint2 *d_peaks = nullptr;
     void *d_spill = nullptr;     // candidate spill slab for crowded frames
+    uint32_t *d_corner_spill = nullptr;   // k_nms_up_corner candidate overflow (per resident CTA)
     size_t ws_frames = 0;
     int ws_K = 0;
     int ws_cap_part = 0, ws_cap_cands = 0;
@@ -474,6 +475,9 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.nst = kCornerStages;
         a.chain = rows->min_step >= 0.03125 && cols->min_step >= 0.03125 && !ctx->no_chain;
         a.rrec = rows->d_rec; a.crec = cols->d_rec;
+        if (!ctx->d_corner_spill)   // persistent grid <= 16 resident CTAs per SM
+            CU(dev_alloc(&ctx->d_corner_spill, nms_up_corner_spill_entries(ctx->sms * 16)));
+        a.cand_spill = ctx->d_corner_spill;
         KernelTimer kt(ctx, kNmsUpCorner);
         CU(launch_nms_up_corner(a, s));
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
@@ -810,7 +814,8 @@ void pf_destroy(pf_ctx *ctx)
     void *dev[] = {ctx->d_counts, ctx->d_peaks, ctx->d_spill, ctx->d_frame_first, ctx->d_frame_count,
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
-                   ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd};
+                   ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
+                   ctx->d_corner_spill};
     for (void *p : dev) cudaFree(p);
     void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
                     ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};

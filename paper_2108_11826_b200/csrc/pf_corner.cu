@@ -67,6 +67,7 @@ constexpr int kCornerThreads = PF_CORNER_THREADS;
 constexpr int kCornerCands = 512;    // candidate pixels per plane kept in shared memory
 constexpr int kCornerList = 1024;    // hot cells per plane kept in shared memory
 constexpr int kCornerSurv = 256;     // chain survivors per plane kept in shared memory
+constexpr int kCornerSpill = 4096;   // candidates per CTA beyond the shared list (global slab)
 
 
 // One CTA owns a plane, so its peak count lives in shared memory (no global
@@ -238,12 +239,16 @@ struct CandList {
     uint32_t *c;
     int *n;
     int cap;
+    uint32_t *spill;     // this CTA's global overflow slab (crowded planes)
+    int spill_cap;
 };
 
 __device__ __forceinline__ void push_cand(const CandList &cl, int y, int x)
 {
     const int slot = atomicAdd(cl.n, 1);
-    if (slot < cl.cap) cl.c[slot] = (uint32_t(y) << 16) | uint32_t(x);   // beyond: plane redone (slow path)
+    const uint32_t yx = (uint32_t(y) << 16) | uint32_t(x);
+    if (slot < cl.cap) cl.c[slot] = yx;
+    else if (slot < cl.cap + cl.spill_cap) cl.spill[slot - cl.cap] = yx;   // beyond: plane redone (slow path)
 }
 
 // Candidate pixels of a partial cell.  Rows restricted to the boundary rows
@@ -496,7 +501,8 @@ k_nms_up_corner(const UpCornerArgs a)
     uint32_t *cand = reinterpret_cast<uint32_t *>(smc + L.cand);
     uint32_t *surv = reinterpret_cast<uint32_t *>(smc + L.surv);
     __shared__ int n_hot, n_cand, n_surv, n_pk;
-    const CandList cl{cand, &n_cand, kCornerCands};
+    const CandList cl{cand, &n_cand, kCornerCands, a.cand_spill + (size_t)blockIdx.x * kCornerSpill,
+                      a.cand_spill ? kCornerSpill : 0};
     const Bands bd{RB, CB, RT, CT};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long P = (long long)a.B * a.K;
@@ -604,7 +610,19 @@ k_nms_up_corner(const UpCornerArgs a)
         // list (warp-aggregated), then the survivors are classified spread
         // over all warps (survivor i -> warp i % 4): normal cells push their
         // surviving corner, partial cells their candidate pixels.
-        {
+        if (n_hot > kCornerList) {
+            // crowded plane (the hot list overflowed): no lists, each thread
+            // walks the hot cells of its (band row, 32 cells) words itself
+            for (int t = threadIdx.x; t < nbr * nwc; t += kCornerThreads) {
+                const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;
+                uint32_t c = cell_word(hot, nws, p, j);
+                while (c) {
+                    const int q = (j << 5) + __ffs(c) - 1;
+                    c &= c - 1u;
+                    if (!(a.chain && chain_pruned(S, w, nbr, nbc, p, q))) process_cell(a, bd, cl, S, plane, p, q);
+                }
+            }
+        } else {
             const int nh = min(n_hot, kCornerList);
             for (int base = warp * kWarp; base < nh; base += kCornerThreads) {
                 const int idx = base + lane;
@@ -628,12 +646,23 @@ k_nms_up_corner(const UpCornerArgs a)
         PROF_MARK(8);
         __syncthreads();
         PROF_MARK(9);
-        {
-            const int ns = min(n_surv, kCornerSurv);
+        if (n_hot > kCornerList) {
+            // done above
+        } else if (n_surv <= kCornerSurv) {
+            const int ns = n_surv;
             const int nw = kCornerThreads / kWarp;
             for (int i = warp + nw * lane; i < ns; i += kCornerThreads) {
                 const uint32_t cell = surv[i];
                 process_cell(a, bd, cl, S, plane, int(cell >> 16), int(cell & 0xffffu));
+            }
+        } else if (n_surv > kCornerSurv) {
+            // the survivor list overflowed: classify every surviving hot cell
+            // straight from the hot words (the hot list itself was complete)
+            const int nh = n_hot;
+            for (int i = threadIdx.x; i < nh; i += kCornerThreads) {
+                const uint32_t pq = list[i];
+                const int p = int(pq >> 8), q = int(pq & 0xffu);
+                if (!(a.chain && chain_pruned(S, w, nbr, nbc, p, q))) process_cell(a, bd, cl, S, plane, p, q);
             }
         }
         PROF_MARK(4);
@@ -643,7 +672,7 @@ k_nms_up_corner(const UpCornerArgs a)
         // ---- (C2) the exact 3x3 test, 9 lanes per candidate (one pixel each),
         // three candidates per warp, gathered by shuffles
         {
-            const int nc = min(n_cand, kCornerCands);
+            const int nc = min(n_cand, kCornerCands + cl.spill_cap);
             const int grp = lane / 9, nb = lane - grp * 9;
             const int src = min(grp, 2) * 9;
             for (int base = warp * 3; base < nc; base += 3 * (kCornerThreads / kWarp)) {
@@ -652,7 +681,7 @@ k_nms_up_corner(const UpCornerArgs a)
                 int y = 0, x = 0;
                 float val = -INFINITY;
                 if (act) {
-                    const uint32_t yx = cand[ci];
+                    const uint32_t yx = ci < kCornerCands ? cand[ci] : __ldcg(cl.spill + (ci - kCornerCands));
                     y = (int)(yx >> 16);
                     x = (int)(yx & 0xffffu);
                     val = exact_value(a, S, y + nb / 3 - 1, x + nb % 3 - 1);
@@ -678,7 +707,7 @@ k_nms_up_corner(const UpCornerArgs a)
             atomicAdd(g_corner_prof + 15, (unsigned long long)n_cand);
         }
 #endif
-        if (n_hot > kCornerList || n_surv > kCornerSurv || n_cand > kCornerCands) {   // CTA-uniform: a list overflowed
+        if (n_cand > kCornerCands + cl.spill_cap) {          // CTA-uniform: the candidate lists overflowed
             redo_plane(a, bd, S, hot, plane, &n_pk);
         }
         __syncthreads();                                     // stage + list free again
@@ -702,6 +731,11 @@ k_nms_up_corner(const UpCornerArgs a)
         atomicAdd(g_corner_prof + 12, (unsigned long long)it);
     }
 #endif
+}
+
+size_t nms_up_corner_spill_entries(int max_ctas)
+{
+    return (size_t)max_ctas * kCornerSpill;
 }
 
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst)

@@ -74,7 +74,9 @@ struct UpCornerArgs {
     int bulk;                            // set by the launcher: planes fetched by cp.async.bulk
     int chain;                           // chain pre-filter allowed (output t steps >= 2^-5)
     const AxisRec *rrec, *crec;          // packed per-output axis records
+    uint32_t *cand_spill;                // [grid][kCornerSpill] candidate overflow slab (or null)
 };
+size_t nms_up_corner_spill_entries(int max_ctas);
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
 #ifndef PF_CORNER_STAGES
 #define PF_CORNER_STAGES 1
