@@ -1200,18 +1200,19 @@ static int preprocess_impl(pf_ctx *ctx, const void *src, int is_f32, int batch, 
     if (!src || !dst) return fail(ctx, PF_ERR_CONTRACT, "null image pointer");
     int rc = set_device(ctx);
     if (rc) return rc;
-    AxisTab rt{}, ct{};
+    const AxisRec *rt = nullptr, *ct = nullptr;
     if (h != out_h || w != out_w) {
+        if (h > 65535 || w > 65535) return fail(ctx, PF_ERR_CONTRACT, "source extents exceed 65535");
         AxisCache *r, *c;
         rc = get_axis(ctx, h, out_h, &r);
         if (rc) return rc;
         rc = get_axis(ctx, w, out_w, &c);
         if (rc) return rc;
-        rt = r->dev();
-        ct = c->dev();
+        rt = r->d_rec;
+        ct = c->d_rec;
     }
     KernelTimer kt(ctx, kPreprocess);
-    CU(launch_preprocess(src, is_f32, batch, h, w, dst, out_h, out_w, rt, ct, ctx->sms, ctx->stream));
+    CU(launch_preprocess(src, is_f32, batch, h, w, dst, out_h, out_w, rt, ct, ctx->stream));
     return PF_OK;
 }
 

@@ -26,41 +26,86 @@ struct PixelLoad<float> {
     __device__ float operator()(const float *p) const { return __ldg(p); }
 };
 
+// Same size (operators.py:123-124: layout only): 4 pixels per thread, one
+// 12-byte (u8) or 48-byte (f32) load, one 16-byte store per channel plane.
 template <typename Tin>
 __global__ void __launch_bounds__(256)
-k_preprocess(const Tin *__restrict__ src, int h, int w, float *__restrict__ dst,
-             int H, int W, AxisTab rows, AxisTab cols, int same, long long total)
+k_preprocess_same(const Tin *__restrict__ src, int hw, float *__restrict__ dst, int vec)
 {
     __shared__ float lut[256];
-    for (int u = threadIdx.x; u < 256; u += blockDim.x) lut[u] = __fdiv_rn((float)u, 255.0f);
-    __syncthreads();
-    PixelLoad<Tin> ld;
-    if constexpr (sizeof(Tin) == 1) ld.lut = lut;
-    const long long HW = (long long)H * W;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const long long bb = e / HW;
-        const int rem = int(e - bb * HW);
-        const int y = rem / W, x = rem - y * W;
-        const Tin *s = src + bb * (long long)h * w * 3;
-        float *d = dst + bb * 3 * HW + rem;
-        if (same) {
-            const Tin *px = s + ((size_t)y * w + x) * 3;
-            d[0] = ld(px);
-            d[HW] = ld(px + 1);
-            d[2 * HW] = ld(px + 2);
-        } else {
-            const int i0 = __ldg(rows.i0 + y), i1 = __ldg(rows.i1 + y);
-            const int j0 = __ldg(cols.i0 + x), j1 = __ldg(cols.i1 + x);
-            const double ty = __ldg(rows.t + y), omty = __ldg(rows.omt + y);
-            const double tx = __ldg(cols.t + x), omtx = __ldg(cols.omt + x);
-            const Tin *p00 = s + ((size_t)i0 * w + j0) * 3, *p01 = s + ((size_t)i0 * w + j1) * 3;
-            const Tin *p10 = s + ((size_t)i1 * w + j0) * 3, *p11 = s + ((size_t)i1 * w + j1) * 3;
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                d[c * HW] = bilerp(ld(p00 + c), ld(p01 + c), ld(p10 + c), ld(p11 + c), tx, omtx, ty, omty);
-        }
+    if constexpr (sizeof(Tin) == 1) {
+        for (int u = threadIdx.x; u < 256; u += blockDim.x) lut[u] = __fdiv_rn((float)u, 255.0f);
+        __syncthreads();
     }
+    const long long b = blockIdx.y;
+    const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (p0 >= hw) return;
+    const Tin *s = src + b * (long long)hw * 3 + (long long)p0 * 3;
+    float *d = dst + b * 3LL * hw + p0;
+    float v[12];
+    if (vec) {
+        if constexpr (sizeof(Tin) == 1) {
+            const uint32_t *s4 = reinterpret_cast<const uint32_t *>(s);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const uint32_t wd = __ldg(s4 + k);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[4 * k + q] = lut[(wd >> (8 * q)) & 0xffu];
+            }
+        } else {
+            const float4 *s4 = reinterpret_cast<const float4 *>(s);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float4 f = __ldg(s4 + k);
+                v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            __stcs(reinterpret_cast<float4 *>(d + (long long)c * hw),
+                   make_float4(v[c], v[3 + c], v[6 + c], v[9 + c]));
+    } else {
+        for (int q = 0; q < 4 && p0 + q < hw; ++q)
+            for (int c = 0; c < 3; ++c) {
+                const Tin x = s[3 * q + c];
+                d[(long long)c * hw + q] = sizeof(Tin) == 1 ? lut[(int)x] : (float)x;
+            }
+    }
+}
+
+// Resize (operators.py:97-101, 3-D branch): thread per output pixel, packed
+// axis records, fp64 bilinear per channel rounded once to fp32.
+template <typename Tin>
+__global__ void __launch_bounds__(128)
+k_preprocess_resize(const Tin *__restrict__ src, int h, int w, float *__restrict__ dst, int H, int W,
+                    const AxisRec *__restrict__ rrec, const AxisRec *__restrict__ crec)
+{
+    __shared__ float lut[256];
+    if constexpr (sizeof(Tin) == 1) {
+        for (int u = threadIdx.x; u < 256; u += blockDim.x) lut[u] = __fdiv_rn((float)u, 255.0f);
+        __syncthreads();
+    }
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const long long b = blockIdx.z;
+    if (x >= W) return;
+    const int4 ry = __ldg(reinterpret_cast<const int4 *>(rrec + y));
+    const int4 rx = __ldg(reinterpret_cast<const int4 *>(crec + x));
+    const int i0 = ry.x & 0xffff, i1 = ry.x >> 16, j0 = rx.x & 0xffff, j1 = rx.x >> 16;
+    const double ty = __hiloint2double(ry.w, ry.z), tx = __hiloint2double(rx.w, rx.z);
+    const double omty = __dsub_rn(1.0, ty), omtx = __dsub_rn(1.0, tx);
+    const Tin *s = src + b * (long long)h * w * 3;
+    const Tin *p00 = s + ((size_t)i0 * w + j0) * 3, *p01 = s + ((size_t)i0 * w + j1) * 3;
+    const Tin *p10 = s + ((size_t)i1 * w + j0) * 3, *p11 = s + ((size_t)i1 * w + j1) * 3;
+    auto ld = [&](const Tin *q) -> float {
+        if constexpr (sizeof(Tin) == 1) return lut[*q];
+        else return __ldg(q);
+    };
+    const long long HW = (long long)H * W;
+    float *d = dst + b * 3 * HW + (long long)y * W + x;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        d[c * HW] = bilerp(ld(p00 + c), ld(p01 + c), ld(p10 + c), ld(p11 + c), tx, omtx, ty, omty);
 }
 
 // operators.py:102-107 (2-D branch) applied per plane: [P][h][w] -> [P][H][W]
@@ -182,18 +227,38 @@ static unsigned grid_for(long long total, int threads, int sms)
 }
 
 cudaError_t launch_preprocess(const void *src, int src_is_f32, int B, int h, int w, float *dst,
-                              int H, int W, AxisTab rows, AxisTab cols, int sms, cudaStream_t s)
+                              int H, int W, const AxisRec *rrec, const AxisRec *crec, cudaStream_t s)
 {
-    const long long total = (long long)B * H * W;
-    if (total == 0) return cudaSuccess;
-    const int same = (h == H && w == W);
-    if (src_is_f32)
-        k_preprocess<float><<<grid_for(total, 256, sms), 256, 0, s>>>(
-            static_cast<const float *>(src), h, w, dst, H, W, rows, cols, same, total);
-    else
-        k_preprocess<uint8_t><<<grid_for(total, 256, sms), 256, 0, s>>>(
-            static_cast<const uint8_t *>(src), h, w, dst, H, W, rows, cols, same, total);
-    return cudaGetLastError();
+    if ((long long)B * H * W == 0) return cudaSuccess;
+    for (int b0 = 0; b0 < B; b0 += 65535) {           // grid.y / grid.z <= 65535
+        const int nb = B - b0 < 65535 ? B - b0 : 65535;
+        if (h == H && w == W) {
+            const int hw = h * w;
+            const dim3 grid((unsigned)((hw / 4 + 256) / 256), (unsigned)nb);
+            // 16-byte vectors need hw % 4 == 0 and aligned bases
+            const int vec = (hw & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+                            (reinterpret_cast<uintptr_t>(src) & (src_is_f32 ? 15 : 3)) == 0;
+            if (src_is_f32)
+                k_preprocess_same<float><<<grid, 256, 0, s>>>(static_cast<const float *>(src) + (size_t)b0 * hw * 3,
+                                                             hw, dst + (size_t)b0 * 3 * hw, vec);
+            else
+                k_preprocess_same<uint8_t><<<grid, 256, 0, s>>>(static_cast<const uint8_t *>(src) + (size_t)b0 * hw * 3,
+                                                               hw, dst + (size_t)b0 * 3 * hw, vec);
+        } else {
+            if (H > 65535) return cudaErrorInvalidConfiguration;
+            const dim3 grid((unsigned)((W + 127) / 128), (unsigned)H, (unsigned)nb);
+            const size_t so = (size_t)b0 * h * w * 3, dof = (size_t)b0 * 3 * H * W;
+            if (src_is_f32)
+                k_preprocess_resize<float><<<grid, 128, 0, s>>>(static_cast<const float *>(src) + so, h, w, dst + dof,
+                                                               H, W, rrec, crec);
+            else
+                k_preprocess_resize<uint8_t><<<grid, 128, 0, s>>>(static_cast<const uint8_t *>(src) + so, h, w,
+                                                                 dst + dof, H, W, rrec, crec);
+        }
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_resize_planes(const float *src, long long src_frame, int K, long long P, int h, int w,

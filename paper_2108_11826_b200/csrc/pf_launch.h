@@ -143,7 +143,7 @@ cudaError_t configure_parse_kernels(int max_smem);
 constexpr int kMaxBlurRadius = 64;
 struct BlurTaps { double w[2 * kMaxBlurRadius + 1]; int r; };
 cudaError_t launch_preprocess(const void *src, int src_is_f32, int B, int h, int w, float *dst,
-                              int H, int W, AxisTab rows, AxisTab cols, int sms, cudaStream_t s);
+                              int H, int W, const AxisRec *rrec, const AxisRec *crec, cudaStream_t s);
 cudaError_t launch_resize_planes(const float *src, long long src_frame, int K, long long P, int h, int w,
                                  float *dst, int H, int W, const AxisRec *rrec, const AxisRec *crec,
                                  cudaStream_t s);
