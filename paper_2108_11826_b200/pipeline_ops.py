@@ -30,7 +30,7 @@ import numpy as np
 from . import _native
 from .core import Frame, HumanPose, SkeletonTopology, TensorF32
 from .errors import ContractError
-from .parser import ParserParams, _params_of, default_parser, parse, parse_batch
+from .parser import ParserParams, _params_of, _stack_maps, default_parser, parse, parse_batch
 
 
 @dataclass(frozen=True)
@@ -178,23 +178,38 @@ def _is_packet(item) -> bool:
 
 
 def make_batched_postprocess(topo: SkeletonTopology, params, batch_max: int = 256,
-                             device: int = 0) -> OperatorSpec:
+                             device: int = 0, devices: Optional[Sequence[int]] = None) -> OperatorSpec:
     """Batched GPU post-processing stage.
 
     ``runner(ctx, in_ch, out_ch)`` follows the reference batching operator
     (scheduler.py:108-136): block for one item, drain what is queued up to
     ``batch_max`` without waiting, parse the batch in one GPU call, emit in
     ascending ``seq_id``.  ``fn`` is the per-item form for sequential runs.
-    Outputs are identical for every batch composition (parse is pure).
+    With ``devices`` (more than one entry) a drained batch is cut into
+    contiguous shards parsed concurrently on those GPUs (``MultiDeviceParser``)
+    and merged back in ``seq_id`` order.  Outputs are identical for every
+    batch composition and device count (parse is pure).
     """
     params = _params_of(params)
     if batch_max < 1:
         raise ContractError("batch_max must be >= 1")
+    multi = None
+    if devices is not None and len(devices) > 1:
+        from .sharding import MultiDeviceParser
+
+        multi = MultiDeviceParser(topo, devices)
 
     def run_batch(batch: Sequence[Packet]) -> List[Packet]:
         batch = sorted(batch, key=lambda p: p.seq_id)
         maps = [p.payload[1] for p in batch]
-        poses = parse_batch(maps, topo, params, device=device)
+        if multi is None:
+            poses = parse_batch(maps, topo, params, device=device)
+        else:
+            params.validate()
+            for m in maps:
+                m.validate(topo)
+            conf, paf, stride = _stack_maps(maps, topo)
+            poses = multi.parse_arrays(conf, paf, stride, params).all_poses()
         return [Packet(p.seq_id, p.ingest_ns, (p.payload[0], hp)) for p, hp in zip(batch, poses)]
 
     def runner(ctx, in_ch, out_ch):

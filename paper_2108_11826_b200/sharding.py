@@ -98,3 +98,72 @@ def parse_shard(conf: np.ndarray, paf: np.ndarray, stride: int, topo, params, ra
         for i, poses in zip(range(b0, b1), parse_fn(conf[b0:b1], paf[b0:b1])):
             out.append((seq_base + i, pose_record(seq_base + i, poses, topo)))
     return out
+
+
+class MultiDeviceParser:
+    """In-process frame sharding over several GPUs.
+
+    One worker thread and one ``pf_ctx`` per entry of ``devices`` (contexts are
+    not reentrant, so each stays on its own thread); a batch is cut into
+    contiguous shards (``shard_bounds``), the shards run concurrently, and the
+    results come back in frame order.  No maps move between GPUs and there is
+    no collective: ``parse`` is pure per frame (paf.py:292-305).  The same
+    device may appear more than once (two contexts on one GPU).
+    """
+
+    def __init__(self, topo, devices: Sequence[int], caps: Optional[dict] = None):
+        from concurrent.futures import ThreadPoolExecutor
+
+        if not devices:
+            raise ValueError("MultiDeviceParser needs at least one device")
+        self.topo = topo
+        self.devices = [int(d) for d in devices]
+        self._caps = caps
+        self._pools = [ThreadPoolExecutor(max_workers=1) for _ in self.devices]
+        self._engines = [None] * len(self.devices)
+
+    def _engine(self, i: int):
+        if self._engines[i] is None:
+            from .parser import PafParser
+
+            self._engines[i] = PafParser(self.topo, device=self.devices[i], caps=self._caps)
+        return self._engines[i]
+
+    def parse_arrays(self, conf: np.ndarray, paf: np.ndarray, stride: int, params) -> "ShardedResult":
+        n, world = conf.shape[0], len(self.devices)
+
+        def work(i: int):
+            lo, hi = shard_bounds(n, i, world)
+            if hi == lo:
+                return lo, None
+            return lo, self._engine(i).parse_arrays(conf[lo:hi], paf[lo:hi], stride, params)
+
+        futures = [self._pools[i].submit(work, i) for i in range(world)]
+        return ShardedResult(n, [f.result() for f in futures])
+
+    def close(self) -> None:
+        for i, pool in enumerate(self._pools):
+            if self._engines[i] is not None:
+                pool.submit(self._engines[i].close).result()
+                self._engines[i] = None
+            pool.shutdown()
+
+
+class ShardedResult:
+    """Frame-ordered view over the per-device ``BatchResult`` shards."""
+
+    def __init__(self, n_frames: int, shards):
+        self.n_frames = n_frames
+        self._shards = [(lo, r) for lo, r in shards if r is not None]
+        self.total_humans = sum(int(r.total_humans) for _, r in self._shards)
+
+    def poses(self, frame: int):
+        if not 0 <= frame < self.n_frames:
+            raise IndexError(frame)
+        for lo, r in reversed(self._shards):
+            if frame >= lo:
+                return r.poses(frame - lo)
+        raise IndexError(frame)
+
+    def all_poses(self):
+        return [self.poses(f) for f in range(self.n_frames)]

@@ -117,3 +117,28 @@ def test_batched_postprocess_operator(topo):
     assert ch.closed and [p.seq_id for p in ctx.out] == list(range(5))
     assert [pf.pose_record(p.seq_id, p.payload[1], topo) for p in ctx.out] == \
            [pf.pose_record(i, x, topo) for i, x in enumerate(b)]
+
+
+def test_multi_device_parser_and_operator(topo):
+    """In-process sharding: contiguous shards on several
+    contexts (two on this one GPU, plus an empty shard) give the single-context
+    results in frame order; the batched operator with ``devices`` likewise."""
+    sp = pf.SynthParams()
+    scenes = [pf.procedural_scene(21, s, 656, 368, sp) for s in range(7)] + [pf.crowd_scene(6, 0)]
+    conf, paf = pf.synth.render_batch(scenes, topo, sp)
+    params = pf.ParserParams(upsample=8)
+    single = pf.PafParser(topo).parse_arrays(conf, paf, 8, params)
+    want = [pf.pose_record(f, single.poses(f), topo) for f in range(len(scenes))]
+    for devices in ([0, 0], [0, 0, 0]):
+        multi = pf.MultiDeviceParser(topo, devices)
+        got = multi.parse_arrays(conf, paf, 8, params)
+        assert got.total_humans == single.total_humans
+        assert [pf.pose_record(f, p, topo) for f, p in enumerate(got.all_poses())] == want
+        one = multi.parse_arrays(conf[:1], paf[:1], 8, params)     # shards 1 and 2 empty
+        assert pf.pose_record(0, one.poses(0), topo) == want[0]
+        multi.close()
+    maps = [pf.render_feature_maps(s, topo, sp) for s in scenes[:5]]
+    op = pf.make_batched_postprocess(topo, params, batch_max=4, devices=[0, 0])
+    pkts = [pf.Packet(s, 0, (None, m)) for s, m in enumerate(maps)]
+    got = [pf.pose_record(p.seq_id, op.fn(p).payload[1], topo) for p in pkts]
+    assert got == want[:5]
