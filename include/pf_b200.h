@@ -202,6 +202,20 @@ void pf_host_free(void *p);
 /* Kernel launches issued by this context since creation (evidence counter). */
 int64_t pf_launch_count(const pf_ctx *ctx);
 
+/* poses.jsonl for a batch (replaces a Python loop over
+ * poseflow/operators.py:293-310 pose_record): one line per frame, seq ids
+ * seq_base + f, byte-identical to json.dumps(..., separators=(",", ":")) with
+ * CPython float repr.  Inputs are the pf_results SoA arrays (host) and the K
+ * keypoint names.  Writes the lines to out if cap is large enough and returns
+ * their byte length (call with out = NULL to size the buffer); -1 on bad
+ * arguments.  Host-only: needs no device. */
+long long pf_format_records(int n_frames, int n_keypoints, const int32_t *frame_first, const int32_t *frame_count,
+                            const double *human_score, const double *kp_x, const double *kp_y,
+                            const float *kp_score, const int32_t *kp_peak, const char *const *part_names,
+                            long long seq_base, char *out, long long cap);
+/* One double formatted as CPython repr() (NUL-terminated); length or -1. */
+int pf_format_float(double v, char *out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,11 @@ class BatchResult:
     def all_poses(self) -> List[List[HumanPose]]:
         return [self.poses(f) for f in range(self.n_frames)]
 
+    def records(self, topo: SkeletonTopology, seq_base: int = 0) -> List[str]:
+        """``pose_record(seq_base + f, poses(f), topo)`` for every frame, built
+        natively from the SoA arrays (byte-identical; no HumanPose objects)."""
+        return format_records(self, topo, seq_base)
+
 
 class PafParser:
     """A GPU parsing engine bound to one device (one ``pf_ctx``).
@@ -304,3 +309,30 @@ def parse_arrays(conf: np.ndarray, paf: np.ndarray, stride: int, topo: SkeletonT
                  params, device: Optional[int] = None) -> BatchResult:
     """Batched host arrays -> SoA ``BatchResult`` (no per-human objects)."""
     return default_parser(topo, device).parse_arrays(conf, paf, stride, params)
+
+
+def format_records(res: "BatchResult", topo: SkeletonTopology, seq_base: int = 0) -> List[str]:
+    """poses.jsonl lines of a batch (operators.py:293-310) via pf_format_records."""
+    import ctypes
+
+    lib = _native.load_library()
+    names = [n.encode() for n in topo.keypoint_names]
+    name_arr = (ctypes.c_char_p * len(names))(*names)
+    k = res.n_keypoints
+
+    def p(a):
+        return a.ctypes.data_as(ctypes.c_void_p) if a.size else None
+
+    xs = np.ascontiguousarray(res.kp_x).reshape(-1)
+    ys = np.ascontiguousarray(res.kp_y).reshape(-1)
+    ks = np.ascontiguousarray(res.kp_score).reshape(-1)
+    kp = np.ascontiguousarray(res.kp_peak).reshape(-1)
+    args = (res.n_frames, k, p(res.frame_first), p(res.frame_count), p(res.human_score), p(xs), p(ys), p(ks),
+            p(kp), ctypes.cast(name_arr, ctypes.c_void_p), int(seq_base))
+    n = lib.pf_format_records(*args, None, 0)
+    if n < 0:
+        raise ContractError("pf_format_records: bad arguments")
+    buf = ctypes.create_string_buffer(int(n) + 1)
+    lib.pf_format_records(*args, ctypes.cast(buf, ctypes.c_void_p), n)
+    text = buf.raw[:n].decode()
+    return text.split("\n")[:-1] if text else []

@@ -266,6 +266,8 @@ def test_device_tensor_path(topo):
     dev = e.results()
     assert [pf.pose_record(f, host.poses(f), topo) for f in range(6)] == \
            [pf.pose_record(f, dev.poses(f), topo) for f in range(6)]
+    # native poses.jsonl of the whole batch == per-frame pose_record
+    assert dev.records(topo, 40) == [pf.pose_record(40 + f, dev.poses(f), topo) for f in range(6)]
     assert e.launch_count() >= 4
     e.close()
 
