@@ -484,7 +484,7 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--frames", type=int, default=8192, help="frames per GPU per step")
     ap.add_argument("--distinct", type=int, default=256, help="distinct rendered frames")
-    ap.add_argument("--e2e-frames", type=int, default=2048)
+    ap.add_argument("--e2e-frames", type=int, default=8192, help="frames per e2e step (default: the device step)")
     ap.add_argument("--unfused-frames", type=int, default=256)
     ap.add_argument("--mode", choices=("U", "R"), default="U")
     ap.add_argument("--traffic", type=float, default=None,
