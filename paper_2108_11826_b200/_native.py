@@ -25,7 +25,8 @@ PF_OPT_DEBUG, PF_OPT_TIMING, PF_OPT_MATERIALISE, PF_OPT_GENERIC_FUSED = 1, 2, 3,
 PF_OPT_WIN_VARIANT = 5
 PF_OPT_NO_CHAIN = 6
 PF_OPT_PAF_ZERO_COPY = 8
-PF_N_KERNELS = 9
+PF_OPT_CORNER_SPLIT = 9
+PF_N_KERNELS = 10
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (

@@ -23,6 +23,10 @@
 
 using namespace pf;
 
+#ifndef PF_CORNER_SPLIT_DEFAULT
+#define PF_CORNER_SPLIT_DEFAULT 1
+#endif
+
 namespace {
 
 struct AxisCache {
@@ -130,6 +134,10 @@ struct pf_ctx {
     uint2 *d_peaks = nullptr;
     void *d_spill = nullptr;     // candidate spill slab for crowded frames
     uint32_t *d_corner_spill = nullptr;   // k_nms_up_corner candidate overflow (per resident CTA)
+    uint32_t *d_surv = nullptr;           // split corner path: survivors per plane
+    int *d_surv_n = nullptr;
+    size_t surv_planes = 0;
+    int corner_split = PF_CORNER_SPLIT_DEFAULT;
     size_t ws_frames = 0;
     int ws_K = 0;
     int ws_cap_part = 0, ws_cap_cands = 0;
@@ -220,10 +228,11 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
     } while (0)
 
 enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
-                kNmsUpWin, kNmsUpCorner };
+                kNmsUpWin, kNmsUpCorner, kCornerFinish };
 const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
                                           "k_resize_planes", "k_blur_rows", "k_blur_cols",
-                                          "k_preprocess", "k_nms_up_win", "k_nms_up_corner"};
+                                          "k_preprocess", "k_nms_up_win", "k_nms_up_corner",
+                                          "k_corner_finish"};
 
 cudaEvent_t take_event(pf_ctx *ctx)
 {
@@ -478,8 +487,27 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         if (!ctx->d_corner_spill)   // persistent grid <= 16 resident CTAs per SM
             CU(dev_alloc(&ctx->d_corner_spill, nms_up_corner_spill_entries(ctx->sms * 16)));
         a.cand_spill = ctx->d_corner_spill;
-        KernelTimer kt(ctx, kNmsUpCorner);
-        CU(launch_nms_up_corner(a, s));
+        if (ctx->corner_split) {
+            const size_t planes = (size_t)n * K;
+            if (planes > ctx->surv_planes) {
+                cudaFree(ctx->d_surv);
+                cudaFree(ctx->d_surv_n);
+                ctx->d_surv = nullptr; ctx->d_surv_n = nullptr; ctx->surv_planes = 0;
+                CU(dev_alloc(&ctx->d_surv, planes * corner_surv_entries_per_plane()));
+                CU(dev_alloc(&ctx->d_surv_n, planes));
+                ctx->surv_planes = planes;
+            }
+            a.surv_out = ctx->d_surv;
+            a.surv_n = ctx->d_surv_n;
+        }
+        {
+            KernelTimer kt(ctx, kNmsUpCorner);
+            CU(launch_nms_up_corner(a, s));
+        }
+        if (ctx->corner_split) {
+            KernelTimer kt(ctx, kCornerFinish);
+            CU(launch_corner_finish(a, s));
+        }
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
                nms_up_win_smem(h, w, H, 128) <= 96 * 1024) {
         UpWinArgs a{};
@@ -815,7 +843,7 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
-                   ctx->d_corner_spill};
+                   ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n};
     for (void *p : dev) cudaFree(p);
     void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
                     ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};
@@ -913,6 +941,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 4) ? value : 4; return PF_OK;
     case PF_OPT_NO_CHAIN: ctx->no_chain = value ? 1 : 0; return PF_OK;
     case PF_OPT_PAF_ZERO_COPY: ctx->paf_zero_copy = value ? 1 : 0; return PF_OK;
+    case PF_OPT_CORNER_SPLIT: ctx->corner_split = value ? 1 : 0; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }

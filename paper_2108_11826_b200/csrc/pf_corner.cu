@@ -128,6 +128,23 @@ __device__ __noinline__ bool exact_peak(const UpCornerArgs &a, const float *S, i
     return v >= up_val(S, a.w, yp, xp);
 }
 
+// The same predicate without early exits: all nine values are gathered at
+// once (one load round trip), for gather-latency-bound callers.
+__device__ __forceinline__ bool exact_peak_all(const UpCornerArgs &a, const float *S, int y, int x, float &v)
+{
+    const Ax ys[3] = {ax_load(a.rrec, y - 1, a.H), ax_load(a.rrec, y, a.H), ax_load(a.rrec, y + 1, a.H)};
+    const Ax xs[3] = {ax_load(a.crec, x - 1, a.W), ax_load(a.crec, x, a.W), ax_load(a.crec, x + 1, a.W)};
+    float n[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) n[3 * r + c] = up_val(S, a.w, ys[r], xs[c]);
+    v = n[4];
+    // paf.py:95-99: earlier neighbours strictly, later ones non-strictly
+    return v >= a.thr && v > n[0] && v > n[1] && v > n[2] && v > n[3] && v >= n[5] && v >= n[6] && v >= n[7] &&
+           v >= n[8];
+}
+
 struct CellF {
     float a0, a1, b0, b1;    // S[r0][c0], S[r0][c1], S[r1][c0], S[r1][c1]
 };
@@ -241,6 +258,7 @@ struct CandList {
     int cap;
     uint32_t *spill;     // this CTA's global overflow slab (crowded planes)
     int spill_cap;
+    __device__ void operator()(int y, int x) const;   // candidate sink: push_cand
 };
 
 __device__ __forceinline__ void push_cand(const CandList &cl, int y, int x)
@@ -250,13 +268,15 @@ __device__ __forceinline__ void push_cand(const CandList &cl, int y, int x)
     if (slot < cl.cap) cl.c[slot] = yx;
     else if (slot < cl.cap + cl.spill_cap) cl.spill[slot - cl.cap] = yx;   // beyond: plane redone (slow path)
 }
+__device__ __forceinline__ void CandList::operator()(int y, int x) const { push_cand(*this, y, x); }
 
 // Candidate pixels of a partial cell.  Rows restricted to the boundary rows
 // when v_ok, columns to the boundary columns when h_ok; further, a row whose
 // own slope clears the noise bound is strictly monotone inside the cell, so
 // only its rising-end column can be "> left and >= right" (and likewise a
 // monotone column keeps only its rising-end row).
-__device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands &bd, const CandList &cl,
+template <typename Sink>
+__device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands &bd, const Sink &cl,
                                               const float *S, int plane, int p, int q, unsigned ok)
 {
     const int4 rb = bd.rb[p], cb = bd.cb[q];
@@ -283,7 +303,7 @@ __device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands
                 const float e = sl_v(c, (float)__dsub_rn(1.0, tx), (float)tx);
                 if (fabsf(e) * rdt > n && y != (e > 0.f ? rb.y : rb.x)) continue;
             }
-            push_cand(cl, y, x);
+            cl(y, x);
         }
     }
 }
@@ -341,7 +361,8 @@ __device__ __forceinline__ bool chain_pruned(const float *S, int w, int nbr, int
 
 // One hot cell: classify; a normal cell pushes its surviving corner, a partial
 // cell its candidate pixels.
-__device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands &bd, const CandList &cl,
+template <typename Sink>
+__device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands &bd, const Sink &cl,
                                              const float *S, int plane, int pr, int q)
 {
     const int4 rb = bd.rb[pr], cb = bd.cb[q];
@@ -355,7 +376,7 @@ __device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands 
             if (i == 1 && rb.x == rb.y) continue;     // a 1-row band's pixel is visited once
             if (j == 1 && cb.x == cb.y) continue;
             if (!corner_cross_ok(bd, S, a.w, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
-            push_cand(cl, i ? rb.x : rb.y, j ? cb.x : cb.y);
+            cl(i ? rb.x : rb.y, j ? cb.x : cb.y);
         }
     } else {
         partial_cands(a, bd, cl, S, plane, pr, q, ok);
@@ -646,7 +667,13 @@ k_nms_up_corner(const UpCornerArgs a)
         PROF_MARK(8);
         __syncthreads();
         PROF_MARK(9);
-        if (n_hot > kCornerList) {
+        // split mode: hand the survivors to k_corner_finish (no shared plane
+        // needed there) unless this plane took a crowded path
+        const bool handed = a.surv_out && n_hot <= kCornerList && n_surv <= kCornerSurv;
+        if (handed) {
+            for (int i = threadIdx.x; i < n_surv; i += kCornerThreads)
+                a.surv_out[(size_t)plane * kCornerSurv + i] = surv[i];
+        } else if (n_hot > kCornerList) {
             // done above
         } else if (n_surv <= kCornerSurv) {
             const int ns = n_surv;
@@ -671,7 +698,7 @@ k_nms_up_corner(const UpCornerArgs a)
 
         // ---- (C2) the exact 3x3 test, 9 lanes per candidate (one pixel each),
         // three candidates per warp, gathered by shuffles
-        {
+        if (!handed) {
             const int nc = min(n_cand, kCornerCands + cl.spill_cap);
             const int grp = lane / 9, nb = lane - grp * 9;
             const int src = min(grp, 2) * 9;
@@ -712,7 +739,8 @@ k_nms_up_corner(const UpCornerArgs a)
         }
         __syncthreads();                                     // stage + list free again
         if (threadIdx.x == 0) {
-            a.counts[plane] = n_pk;                          // the plane's peaks are complete
+            if (a.surv_out) a.surv_n[plane] = handed ? n_surv : -1;
+            if (!handed) a.counts[plane] = n_pk;             // handed: k_corner_finish writes it
             n_hot = 0;
             n_cand = 0;
             n_surv = 0;
@@ -732,6 +760,101 @@ k_nms_up_corner(const UpCornerArgs a)
     }
 #endif
 }
+
+// ---------------------------------------------------------------------------
+// k_corner_finish — second half of the split corner path.  k_nms_up_corner
+// (split mode) keeps only the streaming part — hot words, hot cells, chain
+// pre-filter — and hands each plane's chain survivors (≈15) over; here one
+// warp per plane classifies them (process_cell, lane per survivor) and runs
+// the exact 3x3 test lane per candidate (exact_peak_all: all nine values
+// gathered at once).  Sources are read through L1/L2 — no plane buffer — so
+// many warps stay resident to hide the gathers.  Persistent CTAs fill the
+// band tables once.  Same functions as the one-kernel path: same results; a
+// candidate overflow falls back to the exact test of every pixel of every
+// survivor cell.
+constexpr int kFinThreads = 256;
+constexpr int kFinWarps = kFinThreads / kWarp;
+constexpr int kFinCands = 96;
+
+__global__ void __launch_bounds__(kFinThreads, 4)
+k_corner_finish(const UpCornerArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smf[];
+    const int nbr = a.nbr, nbc = a.nbc;
+    int4 *RB = reinterpret_cast<int4 *>(smf);
+    int4 *CB = RB + nbr;
+    BandT *RT = reinterpret_cast<BandT *>(CB + nbc);
+    BandT *CT = RT + nbr;
+    uint32_t *candw = reinterpret_cast<uint32_t *>(CT + nbc);
+    __shared__ int n_cand[kFinWarps], n_pk[kFinWarps];
+    for (int b = threadIdx.x; b < nbr + nbc; b += kFinThreads) {
+        if (b < nbr) fill_band(a.rows, a.rdt, a.rband, b, RB[b], RT[b]);
+        else fill_band(a.cols, a.cdt, a.cband, b - nbr, CB[b - nbr], CT[b - nbr]);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Bands bd{RB, CB, RT, CT};
+    uint32_t *wc = candw + warp * kFinCands;
+    const CandList cl{wc, &n_cand[warp], kFinCands, nullptr, 0};
+    const int P = a.B * a.K;
+    for (int plane = blockIdx.x * kFinWarps + warp; plane < P; plane += gridDim.x * kFinWarps) {
+        const int ns = __ldcg(a.surv_n + plane);
+        if (ns < 0) continue;                             // k_nms_up_corner finished this plane
+        if (lane == 0) { n_cand[warp] = 0; n_pk[warp] = 0; }
+        __syncwarp();
+        const int fb = plane / a.K, k = plane - fb * a.K;
+        const float *S = a.conf + ((size_t)fb * a.C + k) * (size_t)a.h * a.w;
+        const uint32_t *sv = a.surv_out + (size_t)plane * kCornerSurv;
+        for (int i = lane; i < ns; i += kWarp) {
+            const uint32_t cell = __ldcg(sv + i);
+            process_cell(a, bd, cl, S, plane, int(cell >> 16), int(cell & 0xffffu));
+        }
+        __syncwarp();
+        const int ncd = n_cand[warp];
+        if (ncd <= kFinCands) {
+            for (int ci = lane; ci < ncd; ci += kWarp) {
+                const uint32_t yx = wc[ci];
+                const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
+                float v;
+                if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk[warp], a.peaks, plane, a.cap, v, y, x);
+            }
+        } else {
+            // candidate overflow: every pixel of every survivor cell, exactly
+            for (int i = 0; i < ns; ++i) {
+                const uint32_t cell = __ldcg(sv + i);
+                const int4 rb = bd.rb[int(cell >> 16)], cb = bd.cb[int(cell & 0xffffu)];
+                const int bw = cb.y - cb.x + 1, npx = (rb.y - rb.x + 1) * bw;
+                for (int t = lane; t < npx; t += kWarp) {
+                    const int y = rb.x + t / bw, x = cb.x + t % bw;
+                    float v;
+                    if (exact_peak(a, S, y, x, v)) emit_peak_c(&n_pk[warp], a.peaks, plane, a.cap, v, y, x);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) a.counts[plane] = n_pk[warp];
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s)
+{
+    const long long P = (long long)a.B * a.K;
+    if (P == 0) return cudaSuccess;
+    const size_t smem = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) +
+                        (size_t)kFinWarps * kFinCands * sizeof(uint32_t);
+    int dev = 0, sms = 0, occ = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_corner_finish, kFinThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const long long need = (P + kFinWarps - 1) / kFinWarps;
+    k_corner_finish<<<(unsigned)std::min<long long>(need, (long long)occ * sms), kFinThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+size_t corner_surv_entries_per_plane() { return kCornerSurv; }
 
 size_t nms_up_corner_spill_entries(int max_ctas)
 {
@@ -793,6 +916,13 @@ cudaError_t configure_corner_kernels(int max_smem)
     if (e == cudaSuccess) e = configure_corner<6>(max_smem);
     if (e == cudaSuccess) e = configure_corner<7>(max_smem);
     if (e == cudaSuccess) e = configure_corner<8>(max_smem);
+    if (e == cudaSuccess) {
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, k_corner_finish);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_corner_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     max_smem - (int)fa.sharedSizeBytes);
+    }
     return e;
 }
 

@@ -75,7 +75,11 @@ struct UpCornerArgs {
     int chain;                           // chain pre-filter allowed (output t steps >= 2^-5)
     const AxisRec *rrec, *crec;          // packed per-output axis records
     uint32_t *cand_spill;                // [grid][kCornerSpill] candidate overflow slab (or null)
+    uint32_t *surv_out;                  // split mode: [B*K][kCornerSurv] chain survivors (or null)
+    int *surv_n;                         // split mode: [B*K] survivor counts, -1 = plane finished
 };
+cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s);
+size_t corner_surv_entries_per_plane();
 size_t nms_up_corner_spill_entries(int max_ctas);
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
 #ifndef PF_CORNER_STAGES

@@ -385,8 +385,10 @@ def test_corner_chain_prefilter_is_exact(topo, up):
         params = pf.ParserParams(upsample=up, conf_threshold=thr)
         e1 = pf.PafParser(topo, debug=True)
         runs = []
-        for no_chain in (0, 1):
+        for no_chain, split in ((0, 1), (1, 1), (0, 0), (1, 0)):
+            # split 1: survivors classified by k_corner_finish; 0: one kernel
             e1.ctx.set_option(pf._native.PF_OPT_NO_CHAIN, no_chain)
+            e1.ctx.set_option(pf._native.PF_OPT_CORNER_SPLIT, split)
             e1.parse_arrays(conf, paf, 48, params)      # stride divisible by every tested factor
             runs.append([e1.peaks(f) for f in range(3)])
         e1.close()
