@@ -431,6 +431,14 @@ def run_b200(args, rank, world, local_rank):
                 "bytes_per_frame": per_frame_bytes.get(dominant, 0),
                 "note": "algorithmic bytes = the low-res part maps the fused upsample+NMS must read "
                         "(SURVEY §8(d) 'fused U+N compulsory'); traffic = ncu dram read+write per launch"}
+        # the fused upsample+NMS stage is two kernels when split (streaming +
+        # survivor finish): report the stage as a whole too
+        fused = [k for k in ("k_nms_up_corner", "k_corner_finish", "k_nms_up_win", "k_nms_up") if k in stages]
+        if fused:
+            ms = sum(stages[k]["ms_per_launch"] * stages[k]["launches"] for k in fused) / args.steps
+            b = BYTES_FUSED_UN * F
+            roof["stage_upsample_nms"] = {"kernels": fused, "ms_per_step": ms, "achieved_gbs": b / (ms / 1e3) / 1e9,
+                                          "frac": b / (ms / 1e3) / 1e9 / peak_gbs}
 
     # ---- CPU baseline (rank 0, N == 1) ----
     cpu = None
