@@ -773,8 +773,15 @@ k_nms_up_corner(const UpCornerArgs a)
 // candidate overflow falls back to the exact test of every pixel of every
 // survivor cell.
 constexpr int kFinThreads = 256;
-constexpr int kFinWarps = kFinThreads / kWarp;
-constexpr int kFinCands = 96;
+#ifndef PF_FIN_GROUP
+#define PF_FIN_GROUP 32
+#endif
+constexpr int kFinGroup = PF_FIN_GROUP;              // lanes per plane (16: two planes per warp)
+constexpr int kFinGroups = kFinThreads / kFinGroup;  // planes in flight per CTA
+#ifndef PF_FIN_CANDS
+#define PF_FIN_CANDS 192
+#endif
+constexpr int kFinCands = PF_FIN_CANDS;              // candidates per plane in shared memory
 
 __global__ void __launch_bounds__(kFinThreads, 4)
 k_corner_finish(const UpCornerArgs a)
@@ -786,37 +793,39 @@ k_corner_finish(const UpCornerArgs a)
     BandT *RT = reinterpret_cast<BandT *>(CB + nbc);
     BandT *CT = RT + nbr;
     uint32_t *candw = reinterpret_cast<uint32_t *>(CT + nbc);
-    __shared__ int n_cand[kFinWarps], n_pk[kFinWarps];
+    __shared__ int n_cand[kFinGroups], n_pk[kFinGroups];
     for (int b = threadIdx.x; b < nbr + nbc; b += kFinThreads) {
         if (b < nbr) fill_band(a.rows, a.rdt, a.rband, b, RB[b], RT[b]);
         else fill_band(a.cols, a.cdt, a.cband, b - nbr, CB[b - nbr], CT[b - nbr]);
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = threadIdx.x / kFinGroup, gl = threadIdx.x % kFinGroup;
+    const unsigned gmask = kFinGroup == kWarp ? 0xffffffffu
+                                              : ((1u << kFinGroup) - 1u) << ((threadIdx.x & 31) & ~(kFinGroup - 1));
     const Bands bd{RB, CB, RT, CT};
-    uint32_t *wc = candw + warp * kFinCands;
-    const CandList cl{wc, &n_cand[warp], kFinCands, nullptr, 0};
+    uint32_t *wc = candw + grp * kFinCands;
+    const CandList cl{wc, &n_cand[grp], kFinCands, nullptr, 0};
     const int P = a.B * a.K;
-    for (int plane = blockIdx.x * kFinWarps + warp; plane < P; plane += gridDim.x * kFinWarps) {
+    for (int plane = blockIdx.x * kFinGroups + grp; plane < P; plane += gridDim.x * kFinGroups) {
         const int ns = __ldcg(a.surv_n + plane);
-        if (ns < 0) continue;                             // k_nms_up_corner finished this plane
-        if (lane == 0) { n_cand[warp] = 0; n_pk[warp] = 0; }
-        __syncwarp();
+        if (ns < 0) continue;                             // k_nms_up_corner finished this plane (group-uniform)
+        if (gl == 0) { n_cand[grp] = 0; n_pk[grp] = 0; }
+        __syncwarp(gmask);
         const int fb = plane / a.K, k = plane - fb * a.K;
         const float *S = a.conf + ((size_t)fb * a.C + k) * (size_t)a.h * a.w;
         const uint32_t *sv = a.surv_out + (size_t)plane * kCornerSurv;
-        for (int i = lane; i < ns; i += kWarp) {
+        for (int i = gl; i < ns; i += kFinGroup) {
             const uint32_t cell = __ldcg(sv + i);
             process_cell(a, bd, cl, S, plane, int(cell >> 16), int(cell & 0xffffu));
         }
-        __syncwarp();
-        const int ncd = n_cand[warp];
+        __syncwarp(gmask);
+        const int ncd = n_cand[grp];
         if (ncd <= kFinCands) {
-            for (int ci = lane; ci < ncd; ci += kWarp) {
+            for (int ci = gl; ci < ncd; ci += kFinGroup) {
                 const uint32_t yx = wc[ci];
                 const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
                 float v;
-                if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk[warp], a.peaks, plane, a.cap, v, y, x);
+                if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
             }
         } else {
             // candidate overflow: every pixel of every survivor cell, exactly
@@ -824,16 +833,16 @@ k_corner_finish(const UpCornerArgs a)
                 const uint32_t cell = __ldcg(sv + i);
                 const int4 rb = bd.rb[int(cell >> 16)], cb = bd.cb[int(cell & 0xffffu)];
                 const int bw = cb.y - cb.x + 1, npx = (rb.y - rb.x + 1) * bw;
-                for (int t = lane; t < npx; t += kWarp) {
+                for (int t = gl; t < npx; t += kFinGroup) {
                     const int y = rb.x + t / bw, x = cb.x + t % bw;
                     float v;
-                    if (exact_peak(a, S, y, x, v)) emit_peak_c(&n_pk[warp], a.peaks, plane, a.cap, v, y, x);
+                    if (exact_peak(a, S, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
                 }
             }
         }
-        __syncwarp();
-        if (lane == 0) a.counts[plane] = n_pk[warp];
-        __syncwarp();
+        __syncwarp(gmask);
+        if (gl == 0) a.counts[plane] = n_pk[grp];
+        __syncwarp(gmask);
     }
 }
 
@@ -842,14 +851,14 @@ cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s)
     const long long P = (long long)a.B * a.K;
     if (P == 0) return cudaSuccess;
     const size_t smem = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) +
-                        (size_t)kFinWarps * kFinCands * sizeof(uint32_t);
+                        (size_t)kFinGroups * kFinCands * sizeof(uint32_t);
     int dev = 0, sms = 0, occ = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_corner_finish, kFinThreads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
-    const long long need = (P + kFinWarps - 1) / kFinWarps;
+    const long long need = (P + kFinGroups - 1) / kFinGroups;
     k_corner_finish<<<(unsigned)std::min<long long>(need, (long long)occ * sms), kFinThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
