@@ -136,6 +136,7 @@ struct pf_ctx {
     uint32_t *d_corner_spill = nullptr;   // k_nms_up_corner candidate overflow (per resident CTA)
     uint32_t *d_surv = nullptr;           // split corner path: survivors per plane
     int *d_surv_n = nullptr;
+    int *d_crowd = nullptr;                 // crowded plane list + its counter (last slot)
     size_t surv_planes = 0;
     int corner_split = PF_CORNER_SPLIT_DEFAULT;
     size_t ws_frames = 0;
@@ -492,20 +493,26 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             if (planes > ctx->surv_planes) {
                 cudaFree(ctx->d_surv);
                 cudaFree(ctx->d_surv_n);
-                ctx->d_surv = nullptr; ctx->d_surv_n = nullptr; ctx->surv_planes = 0;
+                cudaFree(ctx->d_crowd);
+                ctx->d_surv = nullptr; ctx->d_surv_n = nullptr; ctx->d_crowd = nullptr; ctx->surv_planes = 0;
                 CU(dev_alloc(&ctx->d_surv, planes * corner_surv_entries_per_plane()));
                 CU(dev_alloc(&ctx->d_surv_n, planes));
+                CU(dev_alloc(&ctx->d_crowd, planes + 1));
                 ctx->surv_planes = planes;
             }
             a.surv_out = ctx->d_surv;
             a.surv_n = ctx->d_surv_n;
+            a.crowd_list = ctx->d_crowd;
+            a.crowd_n = ctx->d_crowd + ctx->surv_planes;
+            CU(cudaMemsetAsync(a.crowd_n, 0, sizeof(int), s));
         }
         {
             KernelTimer kt(ctx, kNmsUpCorner);
-            CU(launch_nms_up_corner(a, s));
+            if (ctx->corner_split) CU(launch_nms_up_scan(a, s));     // streaming half
+            else CU(launch_nms_up_corner(a, s));                      // one-kernel path
         }
         if (ctx->corner_split) {
-            KernelTimer kt(ctx, kCornerFinish);
+            KernelTimer kt(ctx, kCornerFinish, 2);   // k_corner_finish + k_corner_crowded
             CU(launch_corner_finish(a, s));
         }
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
@@ -843,7 +850,7 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
-                   ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n};
+                   ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd};
     for (void *p : dev) cudaFree(p);
     void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
                     ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};

@@ -762,6 +762,222 @@ k_nms_up_corner(const UpCornerArgs a)
 }
 
 // ---------------------------------------------------------------------------
+// k_nms_up_scan — the streaming half of the split path, on its own: no band
+// tables, no candidate lists, no classification code, so it needs ~19 KB of
+// shared memory and few registers and keeps more planes in flight per SM.
+// Per plane: (A) row-aligned hot words, (B) the hot-cell list, (C) the chain
+// pre-filter with survivors written straight to HBM (a hot-list overflow
+// walks the hot words instead); a plane with more than kCornerSurv survivors
+// is marked crowded (surv_n = -2) and k_corner_crowded walks it from the
+// sources.
+constexpr int kScanThreads = 128;
+constexpr int kScanCrowd = 64;       // more survivors than this: k_corner_crowded (CTA per plane)
+#ifndef PF_SCAN_MINB
+#define PF_SCAN_MINB 10
+#endif
+#ifndef PF_SCAN_STAGES
+#define PF_SCAN_STAGES 1
+#endif
+
+struct ScanLayout {
+    int plane_floats;
+    size_t planes, bars, hot, list, total;
+};
+
+__host__ __device__ inline ScanLayout scan_layout(int h, int w, int nst)
+{
+    ScanLayout L;
+    L.plane_floats = (h * w + 3) & ~3;
+    size_t o = 0;
+    L.planes = o; o += (size_t)nst * L.plane_floats * sizeof(float);
+    L.bars = o;   o += (size_t)nst * 8;
+    o = (o + 15) & ~(size_t)15;
+    L.hot = o;    o += (size_t)(h + 2) * ((w + 31) >> 5) * sizeof(uint32_t);
+    L.list = o;   o += (size_t)kCornerList * sizeof(uint16_t);
+    L.total = (o + 15) & ~(size_t)15;
+    return L;
+}
+
+template <int NWS>
+__global__ void __launch_bounds__(kScanThreads, PF_SCAN_MINB)
+k_nms_up_scan(const UpCornerArgs a)
+{
+    extern __shared__ __align__(128) unsigned char smc[];
+    const int h = a.h, w = a.w, hw = h * w;
+    const int nbr = a.nbr, nbc = a.nbc, nst = a.nst;
+    const ScanLayout L = scan_layout(h, w, nst);
+    float *planes = reinterpret_cast<float *>(smc + L.planes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smc + L.bars);
+    uint32_t *hot = reinterpret_cast<uint32_t *>(smc + L.hot);
+    uint16_t *list = reinterpret_cast<uint16_t *>(smc + L.list);   // (p << 8) | q
+    __shared__ int n_hot, n_surv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = a.B * a.K;
+    const uint32_t plane_bytes = (uint32_t)hw * 4u;
+    constexpr int nws = NWS;
+    const int nwc = (w + 32) >> 5;
+    const float inv_nwc = 1.0f / (float)nwc;
+
+    for (int e = threadIdx.x; e < nws; e += kScanThreads) {
+        hot[e] = 0u;
+        hot[(h + 1) * nws + e] = 0u;
+    }
+    if (threadIdx.x == 0) {
+        n_hot = 0;
+        n_surv = 0;
+        if (a.bulk) {
+            for (int s = 0; s < nst; ++s) mbar_init(bars + s, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int s = 0; s < nst; ++s) {
+                const int pl = blockIdx.x + s * gridDim.x;
+                if (pl < P) {
+                    const int b = pl / a.K, k = pl - b * a.K;
+                    bulk_load(planes + s * L.plane_floats, a.conf + ((size_t)b * a.C + k) * (size_t)hw, plane_bytes,
+                              bars + s);
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    int it = 0, stage = 0;
+    for (int pl = blockIdx.x; pl < P; pl += gridDim.x, ++it) {
+        float *S = planes + stage * L.plane_floats;
+        if (a.bulk) {
+            mbar_wait(bars + stage, (uint32_t)(it / nst) & 1u);
+        } else {
+            const int b = pl / a.K, k = pl - b * a.K;
+            const float *src = a.conf + ((size_t)b * a.C + k) * (size_t)hw;
+            for (int e = threadIdx.x; e < hw; e += kScanThreads) S[e] = __ldg(src + e);
+            __syncthreads();
+        }
+        // (A) row-aligned hot words
+        for (int r = warp; r < h; r += kScanThreads / kWarp) {
+            const float *row = S + r * w;
+            float v[NWS];
+#pragma unroll
+            for (int j = 0; j < NWS; ++j) {
+                const int c = (j << 5) + lane;
+                v[j] = (j < NWS - 1 || c < w) ? row[c] : -INFINITY;
+            }
+            uint32_t mine = 0u;
+#pragma unroll
+            for (int j = 0; j < NWS; ++j) {
+                const uint32_t word = __ballot_sync(0xffffffffu, v[j] >= a.thr);
+                if (lane == j) mine = word;
+            }
+            if (lane < nws) hot[(r + 1) * nws + lane] = mine;
+        }
+        __syncthreads();
+        // (B) hot cells
+        for (int t = threadIdx.x; t < nbr * nwc; t += kScanThreads) {
+            const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;   // exact for t < 2^16
+            uint32_t c = cell_word(hot, nws, p, j);
+            if (c) {
+                int slot = atomicAdd(&n_hot, __popc(c));
+                while (c) {
+                    const int q = (j << 5) + __ffs(c) - 1;
+                    c &= c - 1u;
+                    if (slot < kCornerList) list[slot] = uint16_t((p << 8) | q);
+                    ++slot;
+                }
+            }
+        }
+        __syncthreads();
+        // (C) chain pre-filter; survivors straight to HBM
+        const int nh = n_hot;
+        uint32_t *sv = a.surv_out + (size_t)pl * kCornerSurv;
+        if (nh <= kCornerList) {
+            for (int base = warp * kWarp; base < nh; base += kScanThreads) {
+                const int idx = base + lane;
+                uint32_t cell = 0u;
+                bool keep = false;
+                if (idx < nh) {
+                    const uint32_t pq = list[idx];
+                    cell = ((pq >> 8) << 16) | (pq & 0xffu);
+                    keep = !(a.chain && chain_pruned(S, w, nbr, nbc, int(cell >> 16), int(cell & 0xffffu)));
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                if (bal) {
+                    int at = 0;
+                    if (lane == 0) at = atomicAdd(&n_surv, __popc(bal));
+                    at = __shfl_sync(0xffffffffu, at, 0);
+                    const int slot = at + __popc(bal & ((1u << lane) - 1u));
+                    if (keep && slot < kCornerSurv) sv[slot] = cell;
+                }
+            }
+        } else {
+            // the hot list overflowed (crowded plane): each thread walks the
+            // hot cells of its (band row, 32 cells) words itself
+            for (int t = threadIdx.x; t < nbr * nwc; t += kScanThreads) {
+                const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;
+                uint32_t c = cell_word(hot, nws, p, j);
+                while (c) {
+                    const int q = (j << 5) + __ffs(c) - 1;
+                    c &= c - 1u;
+                    if (!(a.chain && chain_pruned(S, w, nbr, nbc, p, q))) {
+                        const int slot = atomicAdd(&n_surv, 1);
+                        if (slot < kCornerSurv) sv[slot] = (uint32_t(p) << 16) | uint32_t(q);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (n_surv > kScanCrowd) {                           // crowded: a whole CTA finishes it
+                a.surv_n[pl] = int(0x80000000u | uint32_t(min(n_surv, 0x3fffffff)));   // < 0 for k_corner_finish
+                a.crowd_list[atomicAdd(a.crowd_n, 1)] = pl;
+            } else {
+                a.surv_n[pl] = n_surv;
+            }
+            n_hot = 0;
+            n_surv = 0;
+            const int nx = pl + nst * gridDim.x;
+            if (a.bulk && nx < P) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const int b = nx / a.K, k = nx - b * a.K;
+                bulk_load(S, a.conf + ((size_t)b * a.C + k) * (size_t)hw, plane_bytes, bars + stage);
+            }
+        }
+        if (!a.bulk) __syncthreads();
+        stage = stage + 1 == nst ? 0 : stage + 1;
+    }
+}
+
+size_t nms_up_scan_smem(int h, int w, int nst)
+{
+    return scan_layout(h, w, nst).total;
+}
+
+cudaError_t launch_nms_up_scan(const UpCornerArgs &a_in, cudaStream_t s)
+{
+    UpCornerArgs a = a_in;
+    const long long P = (long long)a.B * a.K;
+    if (P == 0) return cudaSuccess;
+    a.nst = PF_SCAN_STAGES;
+    const size_t smem = nms_up_scan_smem(a.h, a.w, a.nst);
+    int dev = 0, sms = 0, occ = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nms_up_scan<3>, kScanThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    a.bulk = ((size_t)a.h * a.w * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(a.conf) & 15) == 0;
+    const long long grid = std::min<long long>(P, (long long)occ * sms);
+    switch ((a.w + 31) >> 5) {
+    case 1: k_nms_up_scan<1><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    case 2: k_nms_up_scan<2><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    case 3: k_nms_up_scan<3><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    case 4: k_nms_up_scan<4><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    case 5: k_nms_up_scan<5><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    case 6: k_nms_up_scan<6><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    case 7: k_nms_up_scan<7><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    default: k_nms_up_scan<8><<<(unsigned)grid, kScanThreads, smem, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // k_corner_finish — second half of the split corner path.  k_nms_up_corner
 // (split mode) keeps only the streaming part — hot words, hot cells, chain
 // pre-filter — and hands each plane's chain survivors (≈15) over; here one
@@ -782,6 +998,32 @@ constexpr int kFinGroups = kFinThreads / kFinGroup;  // planes in flight per CTA
 #define PF_FIN_CANDS 192
 #endif
 constexpr int kFinCands = PF_FIN_CANDS;              // candidates per plane in shared memory
+
+__device__ __noinline__ void classify_inline(const UpCornerArgs &a, const Bands &bd, const float *S, int plane,
+                                            int *npk, int p, int q);
+
+// Candidate sink that runs the exact test on the spot (candidate-list overflows).
+struct InlineSink {
+    const UpCornerArgs *a;
+    const float *S;
+    int plane;
+    int *npk;
+    __device__ void operator()(int y, int x) const
+    {
+        float v;
+        if (exact_peak_all(*a, S, y, x, v)) emit_peak_c(npk, a->peaks, plane, a->cap, v, y, x);
+    }
+};
+
+// process_cell with the on-the-spot sink, kept out of line so the common
+// path's register allocation does not pay for it
+__device__ __noinline__ void classify_inline(const UpCornerArgs &a, const Bands &bd, const float *S, int plane,
+                                            int *npk, int p, int q)
+{
+    const InlineSink sink{&a, S, plane, npk};
+    process_cell(a, bd, sink, S, plane, p, q);
+}
+
 
 __global__ void __launch_bounds__(kFinThreads, 4)
 k_corner_finish(const UpCornerArgs a)
@@ -808,7 +1050,7 @@ k_corner_finish(const UpCornerArgs a)
     const int P = a.B * a.K;
     for (int plane = blockIdx.x * kFinGroups + grp; plane < P; plane += gridDim.x * kFinGroups) {
         const int ns = __ldcg(a.surv_n + plane);
-        if (ns < 0) continue;                             // k_nms_up_corner finished this plane (group-uniform)
+        if (ns < 0) continue;   // -1: k_nms_up_corner finished it; -2: crowded (k_corner_crowded); group-uniform
         if (gl == 0) { n_cand[grp] = 0; n_pk[grp] = 0; }
         __syncwarp(gmask);
         const int fb = plane / a.K, k = plane - fb * a.K;
@@ -828,21 +1070,92 @@ k_corner_finish(const UpCornerArgs a)
                 if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
             }
         } else {
-            // candidate overflow: every pixel of every survivor cell, exactly
-            for (int i = 0; i < ns; ++i) {
+            // candidate overflow: classify again and test each candidate on
+            // the spot (nothing was emitted yet)
+            for (int i = gl; i < ns; i += kFinGroup) {
                 const uint32_t cell = __ldcg(sv + i);
-                const int4 rb = bd.rb[int(cell >> 16)], cb = bd.cb[int(cell & 0xffffu)];
-                const int bw = cb.y - cb.x + 1, npx = (rb.y - rb.x + 1) * bw;
-                for (int t = gl; t < npx; t += kFinGroup) {
-                    const int y = rb.x + t / bw, x = cb.x + t % bw;
-                    float v;
-                    if (exact_peak(a, S, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
-                }
+                classify_inline(a, bd, S, plane, &n_pk[grp], int(cell >> 16), int(cell & 0xffffu));
             }
         }
         __syncwarp(gmask);
         if (gl == 0) a.counts[plane] = n_pk[grp];
         __syncwarp(gmask);
+    }
+}
+
+// Crowded planes of the split path (more than kScanCrowd survivors, or the
+// survivor list overflowed): k_nms_up_scan appends them to a compact list;
+// here a whole CTA takes one such plane — survivors (from the list, or from a
+// walk of the hot cells when the list overflowed) classified across all
+// threads, candidates collected in shared memory and tested lane by lane.
+constexpr int kCrowdCands = 2048;
+
+__global__ void __launch_bounds__(kFinThreads, 3)
+k_corner_crowded(const UpCornerArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smf[];
+    const int nbr = a.nbr, nbc = a.nbc;
+    int4 *RB = reinterpret_cast<int4 *>(smf);
+    int4 *CB = RB + nbr;
+    BandT *RT = reinterpret_cast<BandT *>(CB + nbc);
+    BandT *CT = RT + nbr;
+    uint32_t *cand = reinterpret_cast<uint32_t *>(CT + nbc);
+    __shared__ int n_cand, n_pk;
+    const int nlist = min(*a.crowd_n, a.B * a.K);
+    if ((int)blockIdx.x >= nlist) return;                 // the usual case: nothing crowded
+    for (int b = threadIdx.x; b < nbr + nbc; b += kFinThreads) {
+        if (b < nbr) fill_band(a.rows, a.rdt, a.rband, b, RB[b], RT[b]);
+        else fill_band(a.cols, a.cdt, a.cband, b - nbr, CB[b - nbr], CT[b - nbr]);
+    }
+    const Bands bd{RB, CB, RT, CT};
+    const CandList cl{cand, &n_cand, kCrowdCands, nullptr, 0};
+    for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
+        const int plane = __ldcg(a.crowd_list + li);
+        if (threadIdx.x == 0) { n_cand = 0; n_pk = 0; }
+        __syncthreads();
+        const int fb = plane / a.K, k = plane - fb * a.K;
+        const float *S = a.conf + ((size_t)fb * a.C + k) * (size_t)a.h * a.w;
+        const int ns = __ldcg(a.surv_n + plane) & 0x3fffffff;     // survivors found by k_nms_up_scan
+        const bool listed = ns <= kCornerSurv;
+        const uint32_t *sv = a.surv_out + (size_t)plane * kCornerSurv;
+        const int nwc = (nbc + 31) >> 5;
+        // pass 0: candidates into shared memory; pass 1 (overflow): inline tests
+        for (int pass = 0; pass < 2; ++pass) {
+            if (listed) {
+                for (int i = threadIdx.x; i < ns; i += kFinThreads) {
+                    const uint32_t cell = __ldcg(sv + i);
+                    if (pass == 0) process_cell(a, bd, cl, S, plane, int(cell >> 16), int(cell & 0xffffu));
+                    else classify_inline(a, bd, S, plane, &n_pk, int(cell >> 16), int(cell & 0xffffu));
+                }
+            } else {
+                for (int t = threadIdx.x; t < nbr * 32 * nwc; t += kFinThreads) {
+                    const int pj = t >> 5, bit = t & 31;
+                    const int p = pj / nwc, j = pj - p * nwc, q = (j << 5) + bit;
+                    if (q >= nbc) continue;
+                    const CellF c = cellf(S, a.w, bd.rb[p], bd.cb[q]);
+                    if (!(c.a0 >= a.thr || c.a1 >= a.thr || c.b0 >= a.thr || c.b1 >= a.thr)) continue;
+                    if (a.chain && chain_pruned(S, a.w, nbr, nbc, p, q)) continue;
+                    if (pass == 0) process_cell(a, bd, cl, S, plane, p, q);
+                    else classify_inline(a, bd, S, plane, &n_pk, p, q);
+                }
+            }
+            __syncthreads();
+            if (pass == 0) {
+                const int nc = n_cand;
+                if (nc <= kCrowdCands) {
+                    for (int ci = threadIdx.x; ci < nc; ci += kFinThreads) {
+                        const uint32_t yx = cand[ci];
+                        const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
+                        float v;
+                        if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk, a.peaks, plane, a.cap, v, y, x);
+                    }
+                    break;                                 // CTA-uniform
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) a.counts[plane] = n_pk;
+        __syncthreads();
     }
 }
 
@@ -858,8 +1171,12 @@ cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s)
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_corner_finish, kFinThreads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
-    const long long need = (P + kFinGroups - 1) / kFinGroups;
+    const long long need = (P * (kCornerSurv / kFinGroup) + kFinGroups - 1) / kFinGroups;
     k_corner_finish<<<(unsigned)std::min<long long>(need, (long long)occ * sms), kFinThreads, smem, s>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem_c = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) + kCrowdCands * sizeof(uint32_t);
+    k_corner_crowded<<<(unsigned)std::min<long long>(P, (long long)sms * 3), kFinThreads, smem_c, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -915,6 +1232,17 @@ static cudaError_t configure_corner(int max_smem)
     return e;
 }
 
+template <int NWS>
+static cudaError_t configure_scan(int max_smem)
+{
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_nms_up_scan<NWS>);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_nms_up_scan<NWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem - (int)fa.sharedSizeBytes);
+    return e;
+}
+
 cudaError_t configure_corner_kernels(int max_smem)
 {
     cudaError_t e = configure_corner<1>(max_smem);
@@ -925,6 +1253,21 @@ cudaError_t configure_corner_kernels(int max_smem)
     if (e == cudaSuccess) e = configure_corner<6>(max_smem);
     if (e == cudaSuccess) e = configure_corner<7>(max_smem);
     if (e == cudaSuccess) e = configure_corner<8>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<1>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<2>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<3>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<4>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<5>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<6>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<7>(max_smem);
+    if (e == cudaSuccess) e = configure_scan<8>(max_smem);
+    if (e == cudaSuccess) {
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, k_corner_crowded);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_corner_crowded, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     max_smem - (int)fa.sharedSizeBytes);
+    }
     if (e == cudaSuccess) {
         cudaFuncAttributes fa;
         e = cudaFuncGetAttributes(&fa, k_corner_finish);

@@ -76,9 +76,12 @@ struct UpCornerArgs {
     const AxisRec *rrec, *crec;          // packed per-output axis records
     uint32_t *cand_spill;                // [grid][kCornerSpill] candidate overflow slab (or null)
     uint32_t *surv_out;                  // split mode: [B*K][kCornerSurv] chain survivors (or null)
-    int *surv_n;                         // split mode: [B*K] survivor counts, -1 = plane finished
+    int *surv_n;                         // split mode: [B*K] survivor counts, -1 = plane finished,
+                                         //   sign bit = crowded (low bits: survivors)
+    int *crowd_list, *crowd_n;           // split mode: crowded planes (compact) and their count
 };
 cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s);
+cudaError_t launch_nms_up_scan(const UpCornerArgs &a, cudaStream_t s);
 size_t corner_surv_entries_per_plane();
 size_t nms_up_corner_spill_entries(int max_ctas);
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
