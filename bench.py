@@ -398,7 +398,8 @@ def run_b200(args, rank, world, local_rank):
     chunk = 1024
     launches_per_step = {name: n / args.steps for name, (ms, n) in ktimes.items()}
     per_frame_bytes = {"k_nms_up": BYTES_FUSED_UN, "k_nms_up_win": BYTES_FUSED_UN,
-                       "k_nms_up_corner": BYTES_FUSED_UN, "k_nms_plane": BYTES_FUSED_UN}
+                       "k_nms_up_corner": BYTES_FUSED_UN, "k_nms_up_scan": BYTES_FUSED_UN,
+                       "k_nms_plane": BYTES_FUSED_UN}
     for name, (ms, n) in ktimes.items():
         frames_per_launch = F / launches_per_step[name]
         per_launch = ms / n
@@ -433,7 +434,9 @@ def run_b200(args, rank, world, local_rank):
                         "(SURVEY §8(d) 'fused U+N compulsory'); traffic = ncu dram read+write per launch"}
         # the fused upsample+NMS stage is two kernels when split (streaming +
         # survivor finish): report the stage as a whole too
-        fused = [k for k in ("k_nms_up_corner", "k_corner_finish", "k_nms_up_win", "k_nms_up") if k in stages]
+        fused = [k for k in ("k_nms_up_scan", "k_nms_up_corner", "k_corner_finish", "k_corner_crowded", "k_nms_up_win",
+                             "k_nms_up")
+                 if k in stages]
         if fused:
             ms = sum(stages[k]["ms_per_launch"] * stages[k]["launches"] for k in fused) / args.steps
             b = BYTES_FUSED_UN * F

@@ -168,7 +168,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch
  * counts accumulated since the last reset; ids index pf_kernel_name(). */
-#define PF_N_KERNELS 10
+#define PF_N_KERNELS 12
 const char *pf_kernel_name(int id);
 int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset);
 int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,

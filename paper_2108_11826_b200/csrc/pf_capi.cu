@@ -229,11 +229,11 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
     } while (0)
 
 enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
-                kNmsUpWin, kNmsUpCorner, kCornerFinish };
+                kNmsUpWin, kNmsUpCorner, kCornerFinish, kCornerCrowded, kNmsUpScan };
 const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
                                           "k_resize_planes", "k_blur_rows", "k_blur_cols",
                                           "k_preprocess", "k_nms_up_win", "k_nms_up_corner",
-                                          "k_corner_finish"};
+                                          "k_corner_finish", "k_corner_crowded", "k_nms_up_scan"};
 
 cudaEvent_t take_event(pf_ctx *ctx)
 {
@@ -506,14 +506,20 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             a.crowd_n = ctx->d_crowd + ctx->surv_planes;
             CU(cudaMemsetAsync(a.crowd_n, 0, sizeof(int), s));
         }
-        {
-            KernelTimer kt(ctx, kNmsUpCorner);
-            if (ctx->corner_split) CU(launch_nms_up_scan(a, s));     // streaming half
-            else CU(launch_nms_up_corner(a, s));                      // one-kernel path
+        if (ctx->corner_split) {
+            KernelTimer kt(ctx, kNmsUpScan);                          // streaming half
+            CU(launch_nms_up_scan(a, s));
+        } else {
+            KernelTimer kt(ctx, kNmsUpCorner);                        // one-kernel path
+            CU(launch_nms_up_corner(a, s));
         }
         if (ctx->corner_split) {
-            KernelTimer kt(ctx, kCornerFinish, 2);   // k_corner_finish + k_corner_crowded
-            CU(launch_corner_finish(a, s));
+            {
+                KernelTimer kt(ctx, kCornerFinish);
+                CU(launch_corner_finish(a, s));
+            }
+            KernelTimer kt(ctx, kCornerCrowded);
+            CU(launch_corner_crowded(a, s));
         }
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
                nms_up_win_smem(h, w, H, 128) <= 96 * 1024) {

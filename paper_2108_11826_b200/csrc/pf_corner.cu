@@ -1173,7 +1173,16 @@ cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s)
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const long long need = (P * (kCornerSurv / kFinGroup) + kFinGroups - 1) / kFinGroups;
     k_corner_finish<<<(unsigned)std::min<long long>(need, (long long)occ * sms), kFinThreads, smem, s>>>(a);
-    e = cudaGetLastError();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_corner_crowded(const UpCornerArgs &a, cudaStream_t s)
+{
+    const long long P = (long long)a.B * a.K;
+    if (P == 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
     const size_t smem_c = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) + kCrowdCands * sizeof(uint32_t);
     k_corner_crowded<<<(unsigned)std::min<long long>(P, (long long)sms * 3), kFinThreads, smem_c, s>>>(a);

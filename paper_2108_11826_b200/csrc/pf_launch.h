@@ -81,6 +81,7 @@ struct UpCornerArgs {
     int *crowd_list, *crowd_n;           // split mode: crowded planes (compact) and their count
 };
 cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s);
+cudaError_t launch_corner_crowded(const UpCornerArgs &a, cudaStream_t s);
 cudaError_t launch_nms_up_scan(const UpCornerArgs &a, cudaStream_t s);
 size_t corner_surv_entries_per_plane();
 size_t nms_up_corner_spill_entries(int max_ctas);
