@@ -162,13 +162,14 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_WIN_VARIANT 5     /* Mode U 3x3 kernel: 4 corner-pruned (default), 3/2/1 strip kernels */
 #define PF_OPT_NO_CHAIN 6        /* corner kernel: disable the chain pre-filter (A/B parity checks) */
 #define PF_OPT_CORNER_SPLIT 9    /* Mode U 3x3: survivors classified by a second kernel (default 1) */
+#define PF_OPT_PARSE_SPLIT 10    /* line integral over all frames' pairs in its own kernel (default 1) */
 #define PF_OPT_PAF_ZERO_COPY 8   /* pf_parse_host (default 1): a pinned host PAF is read in place by the
                                     parse kernel, so only the sampled cells cross PCIe; 0: copy it whole */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch
  * counts accumulated since the last reset; ids index pf_kernel_name(). */
-#define PF_N_KERNELS 12
+#define PF_N_KERNELS 14
 const char *pf_kernel_name(int id);
 int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset);
 int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,

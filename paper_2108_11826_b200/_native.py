@@ -26,7 +26,8 @@ PF_OPT_WIN_VARIANT = 5
 PF_OPT_NO_CHAIN = 6
 PF_OPT_PAF_ZERO_COPY = 8
 PF_OPT_CORNER_SPLIT = 9
-PF_N_KERNELS = 12
+PF_OPT_PARSE_SPLIT = 10
+PF_N_KERNELS = 14
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (

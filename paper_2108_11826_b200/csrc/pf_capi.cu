@@ -26,6 +26,9 @@ using namespace pf;
 #ifndef PF_CORNER_SPLIT_DEFAULT
 #define PF_CORNER_SPLIT_DEFAULT 1
 #endif
+#ifndef PF_PARSE_SPLIT_DEFAULT
+#define PF_PARSE_SPLIT_DEFAULT 1
+#endif
 
 namespace {
 
@@ -139,6 +142,13 @@ struct pf_ctx {
     int *d_crowd = nullptr;                 // crowded plane list + its counter (last slot)
     size_t surv_planes = 0;
     int corner_split = PF_CORNER_SPLIT_DEFAULT;
+    int parse_split = PF_PARSE_SPLIT_DEFAULT;
+    uint32_t *d_pk_cell = nullptr;          // split parse staging (ensure_split_ws)
+    float *d_pk_score = nullptr;
+    int *d_pk_base = nullptr, *d_pair_pp = nullptr, *d_npairs = nullptr, *d_pair_base = nullptr, *d_cand_n = nullptr;
+    int2 *d_ferr = nullptr;
+    size_t split_frames = 0;
+    int split_cap_frame = 0;
     size_t ws_frames = 0;
     int ws_K = 0;
     int ws_cap_part = 0, ws_cap_cands = 0;
@@ -229,11 +239,12 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
     } while (0)
 
 enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
-                kNmsUpWin, kNmsUpCorner, kCornerFinish, kCornerCrowded, kNmsUpScan };
+                kNmsUpWin, kNmsUpCorner, kCornerFinish, kCornerCrowded, kNmsUpScan, kParsePeaks, kScorePairs };
 const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
                                           "k_resize_planes", "k_blur_rows", "k_blur_cols",
                                           "k_preprocess", "k_nms_up_win", "k_nms_up_corner",
-                                          "k_corner_finish", "k_corner_crowded", "k_nms_up_scan"};
+                                          "k_corner_finish", "k_corner_crowded", "k_nms_up_scan",
+                                          "k_parse_peaks", "k_score_pairs"};
 
 cudaEvent_t take_event(pf_ctx *ctx)
 {
@@ -341,10 +352,37 @@ int ensure_nms_ws(pf_ctx *ctx, size_t frames, int K)
     CU(dev_alloc(&ctx->d_counts, f * k));
     CU(cudaMemset(ctx->d_counts, 0, f * k * sizeof(int)));
     CU(dev_alloc(&ctx->d_peaks, f * k * (size_t)ctx->caps.max_peaks_per_part));
+    // [f][cap_cands] records: the one-kernel parse uses it as the spill past the
+    // shared candidates, the split parse as the whole per-frame candidate list
     CU(dev_alloc(reinterpret_cast<char **>(&ctx->d_spill),
-                 f * cand_spill_bytes_per_frame(ctx->caps.max_candidates)));
+                 f * (size_t)ctx->caps.max_candidates * cand_record_bytes()));
     ctx->ws_frames = f;
     ctx->ws_K = k;
+    return PF_OK;
+}
+
+// Split-parse staging ([frames] x per-frame arrays), sized for the current caps.
+int ensure_split_ws(pf_ctx *ctx, size_t frames)
+{
+    if (frames <= ctx->split_frames && ctx->split_cap_frame == ctx->caps.max_peaks_per_frame) return PF_OK;
+    const size_t f = frames > ctx->split_frames ? frames : ctx->split_frames;
+    void *old[] = {ctx->d_pk_cell, ctx->d_pk_score, ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs,
+                   ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n};
+    for (void *q : old) cudaFree(q);
+    ctx->d_pk_cell = nullptr; ctx->d_pk_score = nullptr; ctx->d_pk_base = nullptr; ctx->d_pair_pp = nullptr;
+    ctx->d_npairs = nullptr; ctx->d_pair_base = nullptr; ctx->d_ferr = nullptr; ctx->d_cand_n = nullptr;
+    ctx->split_frames = 0;
+    const size_t cf = (size_t)ctx->caps.max_peaks_per_frame;
+    CU(dev_alloc(&ctx->d_pk_cell, f * cf));
+    CU(dev_alloc(&ctx->d_pk_score, f * cf));
+    CU(dev_alloc(&ctx->d_pk_base, f * (PF_MAX_KEYPOINTS + 1)));
+    CU(dev_alloc(&ctx->d_pair_pp, f * (PF_MAX_LIMBS + 1)));
+    CU(dev_alloc(&ctx->d_npairs, f + 1));            // + the pair total
+    CU(dev_alloc(&ctx->d_pair_base, f));
+    CU(dev_alloc(&ctx->d_ferr, f));
+    CU(dev_alloc(&ctx->d_cand_n, f));
+    ctx->split_frames = f;
+    ctx->split_cap_frame = ctx->caps.max_peaks_per_frame;
     return PF_OK;
 }
 
@@ -635,8 +673,26 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     a.dbg_npeaks = ctx->d_dbg_np; a.dbg_peaks = ctx->d_dbg_peaks;
     a.dbg_nconns = ctx->d_dbg_nc; a.dbg_conn_i = ctx->d_dbg_ci; a.dbg_conn_d = ctx->d_dbg_cd;
     a.cand_spill = ctx->d_spill;
-    const int threads = kParseThreads;
+    if (ctx->parse_split) {
+        int rc = ensure_split_ws(ctx, (size_t)n);
+        if (rc) return rc;
+        a.split = 1;
+        a.pk_cell = ctx->d_pk_cell; a.pk_score = ctx->d_pk_score; a.pk_base = ctx->d_pk_base;
+        a.pair_pp = ctx->d_pair_pp; a.n_pairs = ctx->d_npairs; a.pair_base = ctx->d_pair_base;
+        a.pair_total = ctx->d_npairs + ctx->split_frames;
+        a.ferr = ctx->d_ferr; a.cand_n = ctx->d_cand_n;
+        a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
+    }
+    const int threads = ctx->parse_split ? kParseFinThreads : kParseThreads;
     const size_t smem = parse_smem_bytes(a.cap_frame, a.cap_cands, a.cap_humans, K, threads / 32);
+    if (a.split) {
+        {
+            KernelTimer kt(ctx, kParsePeaks, 2);   // k_parse_peaks + k_pair_scan
+            CU(launch_parse_peaks(a, n, s));
+        }
+        KernelTimer kt(ctx, kScorePairs);
+        CU(launch_score_pairs(a, n, s));
+    }
     KernelTimer kt(ctx, kParseFrames);
     CU(launch_parse_frames(a, n, threads, smem, s));
     return PF_OK;
@@ -730,7 +786,7 @@ bool grow_cap(pf_ctx *ctx, const Status &st)
         return false;
     }
     const size_t smem = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
-                                         PF_MAX_KEYPOINTS, kParseThreads / 32) + 2048;
+                                         PF_MAX_KEYPOINTS, std::max(kParseThreads, kParseFinThreads) / 32) + 2048;
     if (smem > (size_t)ctx->max_smem) return false;
     if (c.max_peaks_per_part == ctx->caps.max_peaks_per_part && c.max_candidates == ctx->caps.max_candidates &&
         c.max_peaks_per_frame == ctx->caps.max_peaks_per_frame &&
@@ -838,7 +894,7 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
         cu(configure_parse_kernels(max_smem), "configure k_parse_frames"))
         return bail(PF_ERR_CUDA);
     const size_t need = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
-                                         PF_MAX_KEYPOINTS, kParseThreads / 32) + 2048;
+                                         PF_MAX_KEYPOINTS, std::max(kParseThreads, kParseFinThreads) / 32) + 2048;
     if (need > (size_t)max_smem) {
         fail(ctx, PF_ERR_CONFIG, "caps need %zu B of shared memory per frame CTA (> %d)", need, max_smem);
         return bail(PF_ERR_CONFIG);
@@ -856,7 +912,8 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
-                   ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd};
+                   ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_pk_cell, ctx->d_pk_score,
+                   ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n};
     for (void *p : dev) cudaFree(p);
     void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
                     ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};
@@ -955,6 +1012,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_NO_CHAIN: ctx->no_chain = value ? 1 : 0; return PF_OK;
     case PF_OPT_PAF_ZERO_COPY: ctx->paf_zero_copy = value ? 1 : 0; return PF_OK;
     case PF_OPT_CORNER_SPLIT: ctx->corner_split = value ? 1 : 0; return PF_OK;
+    case PF_OPT_PARSE_SPLIT: ctx->parse_split = value ? 1 : 0; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }

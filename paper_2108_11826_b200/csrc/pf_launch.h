@@ -132,6 +132,16 @@ struct ParseArgs {
     double ry, rx;       // h / H, w / W: operators.py:88-89 ratios (up > 1)
     const AxisRec *rrec, *crec;   // packed operators.py:86-96 axis records (up > 1)
     int good_need;       // least n_good with fl(n_good / n) >= good_min (n + 1: none)
+    // split parse (PF_OPT_PARSE_SPLIT): per-frame HBM staging between the kernels
+    int split;
+    uint32_t *pk_cell;   // [B][cap_frame] peaks in id order
+    float *pk_score;
+    int *pk_base;        // [B][K+1] part prefix
+    int *pair_pp;        // [B][L+1] pair prefix per limb
+    int *n_pairs, *pair_base, *pair_total;   // [B], [B], scalar
+    int2 *ferr;          // [B] capacity error (what, value) from k_parse_peaks
+    struct Cand *cand_g; // [B][cap_cands] gated candidates
+    int *cand_n;         // [B]
 };
 #ifndef PF_CAND_SMEM
 #define PF_CAND_SMEM 256
@@ -141,10 +151,17 @@ constexpr int kCandSmem = PF_CAND_SMEM;   // gated candidates kept in shared mem
 #define PF_PARSE_THREADS 128
 #endif
 constexpr int kParseThreads = PF_PARSE_THREADS;   // k_parse_frames CTA size
+#ifndef PF_PARSE_FIN_THREADS
+#define PF_PARSE_FIN_THREADS 64
+#endif
+constexpr int kParseFinThreads = PF_PARSE_FIN_THREADS;   // k_parse_frames<true> (split finish) CTA size
 size_t cand_spill_bytes_per_frame(int cap_cands);
+size_t cand_record_bytes();
 enum { kCapPart = 1, kCapFrame = 2, kCapCands = 3, kCapHumans = 4, kCapPool = 5 };
 size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps);
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s);
+cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s);    // k_parse_peaks + k_pair_scan
+cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s);
 cudaError_t configure_parse_kernels(int max_smem);
 
 // pf_image.cu

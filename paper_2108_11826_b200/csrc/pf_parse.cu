@@ -103,6 +103,42 @@ __device__ __forceinline__ double finish_sample(const ParseArgs &a, const Sample
     return dadd(dmul(px, vx), dmul(py, vy));
 }
 
+// score_limb + gate of one (limb, a, b) pair (paf.py:131-165): the samples in
+// order, so the fp64 running total is the reference's `total += d`; the pair
+// is left as soon as it can no longer pass (more failing samples than
+// max_fail = n - good_need).  True if gated (good >= good_min, score > 0).
+__device__ __forceinline__ bool score_pair(const ParseArgs &a, const float *__restrict__ paf_f, int l, uint32_t ca,
+                                           uint32_t cbp, const double *t_tab, int max_fail, double &score, int &ngood)
+{
+    const int n = a.n_samples;
+    const int ai = int(ca >> 16), aj = int(ca & 0xffff);
+    const int di = int(cbp >> 16) - ai, dj = int(cbp & 0xffff) - aj;
+    if ((di | dj) == 0) return false;                     // coincident cells score (0, 0): never gated
+    const double norm = __dsqrt_rn((double)(di * di + dj * dj));
+    const double vx = __ddiv_rn((double)dj, norm);
+    const double vy = __ddiv_rn((double)di, norm);
+    const float *chx = paf_f + (size_t)a.topo.cx[l] * a.h * a.w;
+    const float *chy = paf_f + (size_t)a.topo.cy[l] * a.h * a.w;
+    const double den = (double)(n - 1);
+    double total = 0.0;
+    int nfail = 0;
+    ngood = 0;
+    for (int u = 0; u < n; ++u) {
+        // nearest cell of sample u (paf.py:139-141)
+        const double t = u < kParseTTab ? t_tab[u] : __ddiv_rn((double)u, den);
+        const int ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
+        const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
+        SampleRaw r;
+        fetch_sample(a, chx, chy, ci, cj, r);
+        const double d = finish_sample(a, r, vx, vy);
+        total = dadd(total, d);
+        if (d >= a.dot_thr) ++ngood;
+        else if (++nfail > max_fail) return false;
+    }
+    score = __ddiv_rn(total, (double)n);
+    return score > 0.0;                                   // paf.py:162 (good already passed)
+}
+
 // CPython 3.12 builtin sum() over floats starting from int 0 (Neumaier).
 __device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
 {
@@ -115,7 +151,15 @@ __device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
 #ifndef PF_PARSE_MINB
 #define PF_PARSE_MINB 8
 #endif
-__global__ void __launch_bounds__(kParseThreads, PF_PARSE_MINB)
+#ifndef PF_PARSE_FIN_MINB
+#define PF_PARSE_FIN_MINB 16
+#endif
+// SPLIT = false: the whole parse of a frame in this CTA.  SPLIT = true: peaks
+// ranked by k_parse_peaks and pairs scored by k_score_pairs (all frames'
+// pairs spread over the whole GPU); this CTA takes the frame's gated
+// candidates from HBM and runs steps 4-7 (sort, greedy, assembly, scores).
+template <bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? kParseFinThreads : kParseThreads, SPLIT ? PF_PARSE_FIN_MINB : PF_PARSE_MINB)
 k_parse_frames(const ParseArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -155,18 +199,26 @@ k_parse_frames(const ParseArgs a)
     int8_t *h_order = reinterpret_cast<int8_t *>(h_parts + a.cap_humans * K); // cap_humans*K
     int8_t *h_n = h_order + a.cap_humans * K;                                 // cap_humans
     int8_t *h_alive = h_n + a.cap_humans;                                     // cap_humans
-    const CandStore cand{cand_s, reinterpret_cast<Cand *>(a.cand_spill) +
-                                     (size_t)b * (a.cap_cands - kCandSmem)};
+    // split: the frame's candidates already sit in cand_g; entries past the
+    // shared part are used (and sorted) in place there
+    const CandStore cand{cand_s, SPLIT ? a.cand_g + (size_t)b * a.cap_cands + kCandSmem
+                                       : reinterpret_cast<Cand *>(a.cand_spill) + (size_t)b * (a.cap_cands - kCandSmem)};
 
     // ---- 1. peak counts, prefix, capacity checks; reset counters ----
     if (tid == 0) { s_err = 0; s_ncand = 0; }
-    if (tid < K) {
+    if (SPLIT) {
+        for (int k = tid; k <= K; k += nthr) s_base[k] = a.pk_base[(size_t)b * (K + 1) + k];
+        if (tid == 0) {
+            const int2 e = a.ferr[b];
+            s_err = e.x; s_errval = e.y;
+        }
+    } else if (tid < K) {
         const int c = a.counts[(size_t)b * K + tid];
         a.counts[(size_t)b * K + tid] = 0;   // ready for the next launch
         s_base[tid + 1] = c;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (!SPLIT && tid == 0) {
         s_base[0] = 0;
         int err = 0, val = 0;
         for (int k = 0; k < K; ++k) {
@@ -190,7 +242,14 @@ k_parse_frames(const ParseArgs a)
     const int P = s_base[K];
 
     // ---- 2. rank-sort each part's peaks (read straight from the NMS slab) ----
-    for (int e = tid; e < P; e += nthr) {
+    if (SPLIT) {
+        for (int e = tid; e < P; e += nthr) {
+            p_cell[e] = __ldcg(a.pk_cell + (size_t)b * a.cap_frame + e);
+            p_score[e] = __ldcg(a.pk_score + (size_t)b * a.cap_frame + e);
+            owner[e] = -1;
+        }
+    }
+    for (int e = tid; !SPLIT && e < P; e += nthr) {
         int part = 0;
         while (e >= s_base[part + 1]) ++part;
         const uint2 *slab = a.peaks + ((size_t)b * K + part) * a.cap_part;
@@ -207,7 +266,7 @@ k_parse_frames(const ParseArgs a)
         p_score[s_base[part] + rank] = vs;
         owner[e] = -1;
     }
-    if (tid == 0) {
+    if (!SPLIT && tid == 0) {
         int acc = 0;
         for (int l = 0; l < L; ++l) {
             s_pp[l] = acc;
@@ -220,7 +279,7 @@ k_parse_frames(const ParseArgs a)
     for (int l = tid; l <= L; l += nthr) s_seg[l] = 0x7fffffff;
     for (int l = tid; l < L; l += nthr) s_lcnt[l] = 0;
     __syncthreads();
-    if (a.debug) {
+    if (!SPLIT && a.debug) {
         for (int e = tid; e < P; e += nthr) {
             int part = 0;
             while (e >= s_base[part + 1]) ++part;
@@ -239,8 +298,7 @@ k_parse_frames(const ParseArgs a)
     const int n_pairs = s_pp[L];
     const int n = a.n_samples;
     const int max_fail = n - a.good_need;            // < 0: nothing can pass
-    if (max_fail >= 0) {
-        const double den = (double)(n - 1);
+    if (!SPLIT && max_fail >= 0) {
         for (int p = tid; p < n_pairs; p += nthr) {
             int l = 0;
             while (p >= s_pp[l + 1]) ++l;
@@ -250,35 +308,9 @@ k_parse_frames(const ParseArgs a)
             const int qa = local / nb;
             const int ia = s_base[pa_part] + qa;
             const int ib = s_base[pb_part] + (local - qa * nb);
-            const int ai = int(p_cell[ia] >> 16), aj = int(p_cell[ia] & 0xffff);
-            const int di = int(p_cell[ib] >> 16) - ai, dj = int(p_cell[ib] & 0xffff) - aj;
-            if ((di | dj) == 0) continue;                 // coincident cells score (0, 0): never gated
-            const double norm = __dsqrt_rn((double)(di * di + dj * dj));
-            const double vx = __ddiv_rn((double)dj, norm);
-            const double vy = __ddiv_rn((double)di, norm);
-            const float *chx = paf_f + (size_t)s_cx[l] * a.h * a.w;
-            const float *chy = paf_f + (size_t)s_cy[l] * a.h * a.w;
-            // nearest cell of sample u (paf.py:139-141)
-            auto cell_of = [&](int u, int &ci, int &cj) {
-                const double t = u < kParseTTab ? s_t[u] : __ddiv_rn((double)u, den);
-                ci = (int)floor(dadd(dadd((double)ai, dmul(t, (double)di)), 0.5));
-                cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
-            };
-            double total = 0.0;
-            int ngood = 0, nfail = 0;
-            for (int u = 0; u < n; ++u) {
-                int ci, cj;
-                cell_of(u, ci, cj);
-                SampleRaw r;
-                fetch_sample(a, chx, chy, ci, cj, r);
-                const double d = finish_sample(a, r, vx, vy);
-                total = dadd(total, d);
-                if (d >= a.dot_thr) ++ngood;
-                else if (++nfail > max_fail) break;
-            }
-            if (nfail > max_fail) continue;
-            const double score = __ddiv_rn(total, (double)n);
-            if (!(score > 0.0)) continue;                  // paf.py:162 (good already passed)
+            double score;
+            int ngood;
+            if (!score_pair(a, paf_f, l, p_cell[ia], p_cell[ib], s_t, max_fail, score, ngood)) continue;
             const int slot = atomicAdd(&s_ncand, 1);
             atomicAdd(&s_lcnt[l], 1);
             if (slot < a.cap_cands) {
@@ -289,6 +321,16 @@ k_parse_frames(const ParseArgs a)
                 cand[slot] = c;
             }
         }
+    }
+    if (SPLIT) {
+        const int ncg = __ldcg(a.cand_n + b);
+        const Cand *cg = a.cand_g + (size_t)b * a.cap_cands;
+        for (int i = tid; i < ncg && i < a.cap_cands; i += nthr) {
+            const Cand c = cg[i];
+            if (i < kCandSmem) cand_s[i] = c;
+            atomicAdd(&s_lcnt[c.lg >> 24], 1);
+        }
+        if (tid == 0) s_ncand = ncg;
     }
     __syncthreads();
     const int nc = s_ncand;
@@ -559,6 +601,182 @@ k_parse_frames(const ParseArgs a)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Split parse (PF_OPT_PARSE_SPLIT): the per-frame CTA no longer carries the
+// gather-bound line integral.
+//   k_parse_peaks  — warp per frame: peak counts, capacity checks, rank sort
+//                    of each part (paf.py:104), ids, pair prefix per limb;
+//   k_pair_scan    — exclusive scan of the frames' pair counts;
+//   k_score_pairs  — thread per (frame, limb, a, b) pair over ALL frames
+//                    (score_pair), gated candidates appended to the frame's
+//                    list in HBM (order irrelevant: the finish step sorts);
+//   k_parse_frames<true> — steps 4-7 per frame.
+constexpr int kPeakFrames = 4;       // frames (warps) per k_parse_peaks CTA
+constexpr int kScoreThreads = 256;
+
+__global__ void __launch_bounds__(kPeakFrames * kWarp)
+k_parse_peaks(const ParseArgs a, int B)
+{
+    const int K = a.topo.K, L = a.topo.L;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * kPeakFrames + warp;
+    __shared__ int s_base[kPeakFrames][PF_MAX_KEYPOINTS + 1];
+    if (b >= B) return;
+    const int gframe = a.frame_base + b;
+    int c = 0;
+    if (lane < K) {
+        c = a.counts[(size_t)b * K + lane];
+        a.counts[(size_t)b * K + lane] = 0;               // ready for the next launch
+    }
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < kWarp; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const int P = __shfl_sync(0xffffffffu, incl, K - 1);
+    const uint32_t over = __ballot_sync(0xffffffffu, lane < K && c > a.cap_part);
+    int err = 0, val = 0;
+    if (over) { err = kCapPart; val = __shfl_sync(0xffffffffu, c, __ffs(over) - 1); }
+    else if (P > a.cap_frame) { err = kCapFrame; val = P; }
+    {   // exclusive prefix: s_base[k] = incl of lane k - 1 (every lane takes part in the shuffle)
+        const int prev = __shfl_sync(0xffffffffu, incl, min(max(lane - 1, 0), 31));
+        if (lane <= K) s_base[warp][lane] = lane == 0 ? 0 : prev;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        a.ferr[b] = make_int2(err, val);
+        a.cand_n[b] = 0;
+    }
+    if (err) {
+        if (lane == 0) {
+            a.n_pairs[b] = 0;
+            if (a.debug) { a.dbg_npeaks[gframe] = 0; a.dbg_nconns[gframe] = 0; }
+        }
+        return;
+    }
+    for (int k = lane; k <= K; k += kWarp) a.pk_base[(size_t)b * (K + 1) + k] = s_base[warp][k];
+    // rank sort of each part's peaks by (score desc, cell asc) straight from the slab
+    for (int e = lane; e < P; e += kWarp) {
+        int part = 0;
+        while (e >= s_base[warp][part + 1]) ++part;
+        const uint2 *slab = a.peaks + ((size_t)b * K + part) * a.cap_part;
+        const int np = s_base[warp][part + 1] - s_base[warp][part];
+        const uint2 v = __ldg(slab + (e - s_base[warp][part]));
+        const float vs = __uint_as_float(v.x);
+        int rank = 0;
+        for (int q = 0; q < np; ++q) {
+            const uint2 u = __ldg(slab + q);
+            const float us = __uint_as_float(u.x);
+            rank += (us > vs) || (us == vs && u.y < v.y);
+        }
+        const size_t o = (size_t)b * a.cap_frame + s_base[warp][part] + rank;
+        a.pk_cell[o] = v.y;
+        a.pk_score[o] = vs;
+        if (a.debug)
+            a.dbg_peaks[(size_t)gframe * a.cap_frame + s_base[warp][part] + rank] =
+                make_int4(part, int(v.y >> 16), int(v.y & 0xffff), __float_as_int(vs));
+    }
+    if (lane == 0) {
+        if (a.debug) a.dbg_npeaks[gframe] = P;
+        int acc = 0;
+        int *pp = a.pair_pp + (size_t)b * (L + 1);
+        for (int l = 0; l < L; ++l) {
+            pp[l] = acc;
+            const int na = s_base[warp][a.topo.la[l] + 1] - s_base[warp][a.topo.la[l]];
+            const int nb = s_base[warp][a.topo.lb[l] + 1] - s_base[warp][a.topo.lb[l]];
+            acc += na * nb;
+        }
+        pp[L] = acc;
+        a.n_pairs[b] = a.n_samples - a.good_need < 0 ? 0 : acc;   // nothing can pass: no pairs to score
+    }
+}
+
+// exclusive scan of the frames' pair counts (one CTA; B is a launch chunk)
+__global__ void __launch_bounds__(1024)
+k_pair_scan(const ParseArgs a, int B)
+{
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < B; b0 += 1024) {
+        const int b = b0 + threadIdx.x;
+        const int v = b < B ? a.n_pairs[b] : 0;
+        int incl = v;
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int w = wsum[lane];
+#pragma unroll
+            for (int d = 1; d < kWarp; d <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= d) w += t;
+            }
+            wsum[lane] = w;                                // inclusive over warps
+        }
+        __syncthreads();
+        const int before = carry + (warp ? wsum[warp - 1] : 0);
+        if (b < B) a.pair_base[b] = before + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = before + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *a.pair_total = carry;
+}
+
+__global__ void __launch_bounds__(kScoreThreads)
+k_score_pairs(const ParseArgs a, int B)
+{
+    __shared__ double s_t[kParseTTab];                     // u / (n - 1), paf.py:139
+    for (int u = threadIdx.x; u < kParseTTab && u < a.n_samples; u += blockDim.x)
+        s_t[u] = __ddiv_rn((double)u, (double)(a.n_samples - 1));
+    __syncthreads();
+    const int K = a.topo.K, L = a.topo.L;
+    const int total = *a.pair_total;
+    const int max_fail = a.n_samples - a.good_need;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+        // frame: last b with pair_base[b] <= g (frames with no pairs share bases)
+        int lo = 0, hi = B - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(a.pair_base + mid) <= g) lo = mid;
+            else hi = mid - 1;
+        }
+        const int b = lo;
+        const int local0 = g - __ldg(a.pair_base + b);
+        const int *pp = a.pair_pp + (size_t)b * (L + 1);
+        int l = 0;
+        while (local0 >= __ldg(pp + l + 1)) ++l;
+        const int *base = a.pk_base + (size_t)b * (K + 1);
+        const int pa_part = a.topo.la[l], pb_part = a.topo.lb[l];
+        const int nb = __ldg(base + pb_part + 1) - __ldg(base + pb_part);
+        const int local = local0 - __ldg(pp + l);
+        const int qa = local / nb;
+        const int ia = __ldg(base + pa_part) + qa;
+        const int ib = __ldg(base + pb_part) + (local - qa * nb);
+        const uint32_t *cells = a.pk_cell + (size_t)b * a.cap_frame;
+        double score;
+        int ngood;
+        const float *paf_f = a.paf + (size_t)b * (2 * L) * a.h * a.w;
+        if (!score_pair(a, paf_f, l, __ldcg(cells + ia), __ldcg(cells + ib), s_t, max_fail, score, ngood)) continue;
+        const int slot = atomicAdd(a.cand_n + b, 1);
+        if (slot < a.cap_cands) {
+            Cand c;
+            c.score = score;
+            c.ab = (uint32_t(ia) << 16) | uint32_t(ib);
+            c.lg = (uint32_t(l) << 24) | uint32_t(ngood);
+            a.cand_g[(size_t)b * a.cap_cands + slot] = c;
+        }
+    }
+}
+
 size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps)
 {
     (void)cap_cands;
@@ -574,6 +792,8 @@ size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int
     return (s + 15) & ~size_t(15);
 }
 
+size_t cand_record_bytes() { return sizeof(Cand); }
+
 size_t cand_spill_bytes_per_frame(int cap_cands)
 {
     return cap_cands > kCandSmem ? (size_t)(cap_cands - kCandSmem) * sizeof(Cand) : 0;
@@ -582,17 +802,44 @@ size_t cand_spill_bytes_per_frame(int cap_cands)
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s)
 {
     if (B == 0) return cudaSuccess;
-    k_parse_frames<<<B, threads, smem, s>>>(a);
+    if (a.split) k_parse_frames<true><<<B, threads, smem, s>>>(a);
+    else k_parse_frames<false><<<B, threads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s)
+{
+    if (B == 0) return cudaSuccess;
+    k_parse_peaks<<<(B + kPeakFrames - 1) / kPeakFrames, kPeakFrames * kWarp, 0, s>>>(a, B);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_pair_scan<<<1, 1024, 0, s>>>(a, B);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s)
+{
+    if (B == 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    k_score_pairs<<<sms * 8, kScoreThreads, 0, s>>>(a, B);
     return cudaGetLastError();
 }
 
 cudaError_t configure_parse_kernels(int max_smem)
 {
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, k_parse_frames);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_parse_frames, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                max_smem - (int)fa.sharedSizeBytes);
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_parse_frames<false>);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_parse_frames<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_frames<true>);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_parse_frames<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem - (int)fa.sharedSizeBytes);
+    return e;
 }
 
 }  // namespace pf
