@@ -398,3 +398,28 @@ def test_corner_chain_prefilter_is_exact(topo, up):
             for f in range(3):
                 want = oracle_run(conf[f], paf[f], topo, params, 48)
                 assert with_chain[f] == want.peaks, f"frame {f}"
+
+
+@pytest.mark.parametrize("up", [1, 8])
+def test_split_paths_agree(topo, up):
+    """The split kernels (corner: scan + finish + crowded; parse: peaks + pair
+    scoring over all frames + finish) give the one-kernel paths' peaks,
+    connections and records on procedural, crowded and random frames."""
+    rng = np.random.default_rng(99)
+    scenes = [pf.procedural_scene(77, s, 656, 368, SP) for s in range(6)] + [pf.crowd_scene(11, s) for s in range(2)]
+    conf, paf = render(scenes, topo)
+    conf[5, :topo.n_keypoints] = rng.random(conf.shape[1:])[:topo.n_keypoints].astype(np.float32)   # noise part maps
+    params = pf.ParserParams(upsample=up)
+    e = pf.PafParser(topo, debug=True)
+    out = []
+    for corner_split, parse_split in ((1, 1), (0, 0), (1, 0), (0, 1)):
+        e.ctx.set_option(pf._native.PF_OPT_CORNER_SPLIT, corner_split)
+        e.ctx.set_option(pf._native.PF_OPT_PARSE_SPLIT, parse_split)
+        got = e.parse_arrays(conf, paf, 8, params)
+        out.append(([e.peaks(f) for f in range(len(scenes))], [e.connections(f) for f in range(len(scenes))],
+                    [pf.pose_record(f, got.poses(f), topo) for f in range(len(scenes))]))
+    e.close()
+    assert all(o == out[0] for o in out)
+    for f in (0, 6):
+        want = oracle_run(conf[f], paf[f], topo, params)
+        assert out[0][2][f] == record_of(want.humans, topo, f)
