@@ -27,6 +27,7 @@ PF_OPT_NO_CHAIN = 6
 PF_OPT_PAF_ZERO_COPY = 8
 PF_OPT_CORNER_SPLIT = 9
 PF_OPT_PARSE_SPLIT = 10
+PF_OPT_CONF_ZERO_COPY = 11
 PF_N_KERNELS = 14
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)

@@ -194,6 +194,7 @@ struct pf_ctx {
     int win_variant = 4;
     int no_chain = 0;
     int paf_zero_copy = 1;
+    int conf_zero_copy = 0;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double kernel_ms[PF_N_KERNELS] = {0};
@@ -1011,6 +1012,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_WIN_VARIANT: ctx->win_variant = (value >= 1 && value <= 4) ? value : 4; return PF_OK;
     case PF_OPT_NO_CHAIN: ctx->no_chain = value ? 1 : 0; return PF_OK;
     case PF_OPT_PAF_ZERO_COPY: ctx->paf_zero_copy = value ? 1 : 0; return PF_OK;
+    case PF_OPT_CONF_ZERO_COPY: ctx->conf_zero_copy = value ? 1 : 0; return PF_OK;
     case PF_OPT_CORNER_SPLIT: ctx->corner_split = value ? 1 : 0; return PF_OK;
     case PF_OPT_PARSE_SPLIT: ctx->parse_split = value ? 1 : 0; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
@@ -1183,12 +1185,19 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     // PF_OPT_PAF_ZERO_COPY: a pinned (mapped) host PAF is read in place by
     // k_parse_frames over PCIe -- only the sampled cells cross the link
     // instead of the whole 2L-channel field.
-    const float *paf_dev = nullptr;
+    const float *paf_dev = nullptr, *conf_dev = nullptr;
     if (ctx->paf_zero_copy && L > 0) {
         cudaPointerAttributes pa{};
         if (cudaPointerGetAttributes(&pa, paf) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
             pa.devicePointer != nullptr)
             paf_dev = static_cast<const float *>(pa.devicePointer);
+        cudaGetLastError();
+    }
+    if (ctx->conf_zero_copy) {        // the NMS kernels stream the planes over PCIe themselves
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, conf) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer != nullptr)
+            conf_dev = static_cast<const float *>(pa.devicePointer);
         cudaGetLastError();
     }
     rc = ensure_nms_ws(ctx, chunk, K);
@@ -1213,15 +1222,17 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
         float *dpaf = dconf + (size_t)n * conf_frame;
         CU(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_free[sl], 0));
         // the background channel (index K) is never read: copy K of K+1 planes per frame
-        CU(cudaMemcpy2DAsync(dconf, conf_frame * sizeof(float), conf + (size_t)f0 * conf_frame,
-                             conf_frame * sizeof(float), (size_t)K * plane * sizeof(float), n,
-                             cudaMemcpyHostToDevice, ctx->copy_stream));
+        if (!conf_dev)
+            CU(cudaMemcpy2DAsync(dconf, conf_frame * sizeof(float), conf + (size_t)f0 * conf_frame,
+                                 conf_frame * sizeof(float), (size_t)K * plane * sizeof(float), n,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
         if (L > 0 && !paf_dev)
             CU(cudaMemcpyAsync(dpaf, paf + (size_t)f0 * paf_frame, (size_t)n * paf_frame * sizeof(float),
                                cudaMemcpyHostToDevice, ctx->copy_stream));
         CU(cudaEventRecord(ctx->ev_copied[sl], ctx->copy_stream));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[sl], 0));
-        rc = run_chunk(ctx, dconf, paf_dev ? paf_dev + (size_t)f0 * paf_frame : dpaf, n, f0, grid_h, grid_w,
+        rc = run_chunk(ctx, conf_dev ? conf_dev + (size_t)f0 * conf_frame : dconf,
+                       paf_dev ? paf_dev + (size_t)f0 * paf_frame : dpaf, n, f0, grid_h, grid_w,
                        stride, p, rows, cols, pool);
         if (rc) return rc;
         CU(cudaEventRecord(ctx->ev_free[sl], ctx->stream));
