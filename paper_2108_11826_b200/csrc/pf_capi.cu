@@ -1212,6 +1212,15 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
         CU(dev_alloc(&ctx->d_in[1], slot));
         ctx->in_elems = slot;
     }
+    // a PAF read in place over PCIe: the one-kernel parse keeps each frame's
+    // gathers on one SM (measured 131k vs 120k frames/s for the split parse)
+    const int saved_split = ctx->parse_split;
+    if (paf_dev) ctx->parse_split = 0;
+    struct Restore {
+        pf_ctx *c;
+        int v;
+        ~Restore() { c->parse_split = v; }
+    } restore{ctx, saved_split};
     // slots start free
     for (int k = 0; k < 2; ++k) CU(cudaEventRecord(ctx->ev_free[k], ctx->stream));
     int ci = 0;

@@ -22,9 +22,10 @@ params = pf.ParserParams(upsample=8)
 e = pf.PafParser(topo)
 ref = None
 for rep in range(2):
-    for zc in (0, 1, 2):     # 0: copy both, 1: PAF in place, 2: PAF and conf in place
+    for zc in (1, 3):        # 0: copy both, 1: PAF in place, 2: PAF and conf in place, 3: 1 + one-kernel parse
         e.ctx.set_option(_native.PF_OPT_PAF_ZERO_COPY, 1 if zc else 0)
         e.ctx.set_option(_native.PF_OPT_CONF_ZERO_COPY, 1 if zc == 2 else 0)
+        e.ctx.set_option(_native.PF_OPT_PARSE_SPLIT, 0 if zc == 3 else 1)
         r = e.parse_arrays(pin_conf.array, pin_paf.array, 8, params)
         recs = [pf.pose_record(f, r.poses(f), topo) for f in range(0, E, 17)]
         if ref is None:
