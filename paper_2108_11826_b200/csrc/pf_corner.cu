@@ -844,7 +844,8 @@ k_nms_up_scan(const UpCornerArgs a)
     for (int pl = blockIdx.x; pl < P; pl += gridDim.x, ++it) {
         float *S = planes + stage * L.plane_floats;
         if (a.bulk) {
-            mbar_wait(bars + stage, (uint32_t)(it / nst) & 1u);
+            if (threadIdx.x == 0) mbar_wait(bars + stage, (uint32_t)(it / nst) & 1u);
+            __syncthreads();                               // the others sleep at the barrier
         } else {
             const int b = pl / a.K, k = pl - b * a.K;
             const float *src = a.conf + ((size_t)b * a.C + k) * (size_t)hw;
