@@ -29,6 +29,7 @@ using namespace pf;
 #ifndef PF_PARSE_SPLIT_DEFAULT
 #define PF_PARSE_SPLIT_DEFAULT 1
 #endif
+constexpr int kSplitMinFrames = 64;   // split option 1 (auto): batches of at least this many frames
 
 namespace {
 
@@ -527,7 +528,9 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         if (!ctx->d_corner_spill)   // persistent grid <= 16 resident CTAs per SM
             CU(dev_alloc(&ctx->d_corner_spill, nms_up_corner_spill_entries(ctx->sms * 16)));
         a.cand_spill = ctx->d_corner_spill;
-        if (ctx->corner_split) {
+        // split kernels pay off on batches; a few frames take the one-kernel path (fewer launches)
+        const bool csplit = ctx->corner_split == 2 || (ctx->corner_split == 1 && n >= kSplitMinFrames);
+        if (csplit) {
             const size_t planes = (size_t)n * K;
             if (planes > ctx->surv_planes) {
                 cudaFree(ctx->d_surv);
@@ -545,14 +548,14 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             a.crowd_n = ctx->d_crowd + ctx->surv_planes;
             CU(cudaMemsetAsync(a.crowd_n, 0, sizeof(int), s));
         }
-        if (ctx->corner_split) {
+        if (csplit) {
             KernelTimer kt(ctx, kNmsUpScan);                          // streaming half
             CU(launch_nms_up_scan(a, s));
         } else {
             KernelTimer kt(ctx, kNmsUpCorner);                        // one-kernel path
             CU(launch_nms_up_corner(a, s));
         }
-        if (ctx->corner_split) {
+        if (csplit) {
             {
                 KernelTimer kt(ctx, kCornerFinish);
                 CU(launch_corner_finish(a, s));
@@ -674,7 +677,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     a.dbg_npeaks = ctx->d_dbg_np; a.dbg_peaks = ctx->d_dbg_peaks;
     a.dbg_nconns = ctx->d_dbg_nc; a.dbg_conn_i = ctx->d_dbg_ci; a.dbg_conn_d = ctx->d_dbg_cd;
     a.cand_spill = ctx->d_spill;
-    if (ctx->parse_split) {
+    const bool psplit = ctx->parse_split == 2 || (ctx->parse_split == 1 && n >= kSplitMinFrames);
+    if (psplit) {
         int rc = ensure_split_ws(ctx, (size_t)n);
         if (rc) return rc;
         a.split = 1;
@@ -684,7 +688,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.ferr = ctx->d_ferr; a.cand_n = ctx->d_cand_n;
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }
-    const int threads = ctx->parse_split ? kParseFinThreads : kParseThreads;
+    const int threads = psplit ? kParseFinThreads : kParseThreads;
     const size_t smem = parse_smem_bytes(a.cap_frame, a.cap_cands, a.cap_humans, K, threads / 32);
     if (a.split) {
         {
@@ -1013,8 +1017,8 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_NO_CHAIN: ctx->no_chain = value ? 1 : 0; return PF_OK;
     case PF_OPT_PAF_ZERO_COPY: ctx->paf_zero_copy = value ? 1 : 0; return PF_OK;
     case PF_OPT_CONF_ZERO_COPY: ctx->conf_zero_copy = value ? 1 : 0; return PF_OK;
-    case PF_OPT_CORNER_SPLIT: ctx->corner_split = value ? 1 : 0; return PF_OK;
-    case PF_OPT_PARSE_SPLIT: ctx->parse_split = value ? 1 : 0; return PF_OK;
+    case PF_OPT_CORNER_SPLIT: ctx->corner_split = (value >= 0 && value <= 2) ? value : 1; return PF_OK;
+    case PF_OPT_PARSE_SPLIT: ctx->parse_split = (value >= 0 && value <= 2) ? value : 1; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }

@@ -385,8 +385,8 @@ def test_corner_chain_prefilter_is_exact(topo, up):
         params = pf.ParserParams(upsample=up, conf_threshold=thr)
         e1 = pf.PafParser(topo, debug=True)
         runs = []
-        for no_chain, split in ((0, 1), (1, 1), (0, 0), (1, 0)):
-            # split 1: survivors classified by k_corner_finish; 0: one kernel
+        for no_chain, split in ((0, 2), (1, 2), (0, 0), (1, 0)):
+            # split 2: survivors classified by k_corner_finish; 0: one kernel
             e1.ctx.set_option(pf._native.PF_OPT_NO_CHAIN, no_chain)
             e1.ctx.set_option(pf._native.PF_OPT_CORNER_SPLIT, split)
             e1.parse_arrays(conf, paf, 48, params)      # stride divisible by every tested factor
@@ -412,7 +412,7 @@ def test_split_paths_agree(topo, up):
     params = pf.ParserParams(upsample=up)
     e = pf.PafParser(topo, debug=True)
     out = []
-    for corner_split, parse_split in ((1, 1), (0, 0), (1, 0), (0, 1)):
+    for corner_split, parse_split in ((2, 2), (0, 0), (2, 0), (0, 2)):   # 2: always split
         e.ctx.set_option(pf._native.PF_OPT_CORNER_SPLIT, corner_split)
         e.ctx.set_option(pf._native.PF_OPT_PARSE_SPLIT, parse_split)
         got = e.parse_arrays(conf, paf, 8, params)
