@@ -295,13 +295,24 @@ def run_b200(args, rank, world, local_rank):
     gpu = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
-    topo, conf_h, paf_h = make_inputs(args.distinct, seed=5 + 1000 * rank)
     params = pf.ParserParams(upsample=UP if args.mode == "U" else 1)
     F = args.frames
-    # device pool: `distinct` rendered frames tiled to F frames (F * 0.86 MB > L2)
-    idx = torch.arange(F) % conf_h.shape[0]
-    conf_d = torch.from_numpy(conf_h).to(dev)[idx.to(dev)].contiguous()
-    paf_d = torch.from_numpy(paf_h).to(dev)[idx.to(dev)].contiguous()
+    if args.distinct >= F:
+        # every frame distinct: F procedural scenes rendered on the GPU
+        # (pf_render_maps, the GPU-resident producer); host copies of the
+        # first frames feed the CPU baseline
+        sp = pf.SynthParams()
+        topo = pf.load_topology("coco18")
+        scenes = [pf.procedural_scene(5 + 1000 * rank, s, GRID_W * STRIDE, GRID_H * STRIDE, sp) for s in range(F)]
+        conf_d, paf_d = pf.synth.render_batch_gpu(scenes, topo, sp, device=gpu)
+        conf_h = conf_d[:256].cpu().numpy()
+        paf_h = paf_d[:256].cpu().numpy()
+    else:
+        topo, conf_h, paf_h = make_inputs(args.distinct, seed=5 + 1000 * rank)
+        # device pool: `distinct` rendered frames tiled to F frames (F * 0.86 MB > L2)
+        idx = torch.arange(F) % conf_h.shape[0]
+        conf_d = torch.from_numpy(conf_h).to(dev)[idx.to(dev)].contiguous()
+        paf_d = torch.from_numpy(paf_h).to(dev)[idx.to(dev)].contiguous()
     eng = pf.PafParser(topo, device=gpu)
     stream = torch.cuda.current_stream(dev)
 
@@ -346,9 +357,8 @@ def run_b200(args, rank, world, local_rank):
     E = min(args.e2e_frames, F)
     pin_conf = _native.PinnedArray((E, K_PARTS + 1, GRID_H, GRID_W))
     pin_paf = _native.PinnedArray((E, 2 * N_LIMBS, GRID_H, GRID_W))
-    sel = np.arange(E) % conf_h.shape[0]
-    pin_conf.array[:] = conf_h[sel]
-    pin_paf.array[:] = paf_h[sel]
+    pin_conf.array[:] = conf_d[:E].cpu().numpy()     # the device step's frames, from host memory
+    pin_paf.array[:] = paf_d[:E].cpu().numpy()
     for _ in range(max(1, args.warmup)):
         r = eng.parse_arrays(pin_conf.array, pin_paf.array, STRIDE, params)
     barrier()
@@ -459,10 +469,10 @@ def run_b200(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
+            "dtype": "f64", "data": "synthetic (procedural scenes, rendered on the GPU by pf_render_maps)",
             "config": {"workload": "C5 stream: synthetic 368x656 frames, 46x82 COCO-18 maps "
                                    "(19 conf + 38 paf), x8 bilinear upsample (Mode U), 1-5 people",
-                       "frames_per_gpu_step": F, "distinct_frames": int(conf_h.shape[0]),
+                       "frames_per_gpu_step": F, "distinct_frames": min(F, args.distinct),
                        "mode": args.mode, "parallelism": f"frame-sharded x{world}, no collective",
                        "l2": f"inputs {F * (CONF_FRAME_BYTES + PAF_FRAME_BYTES) / 1e9:.2f} GB/GPU > L2; no flush",
                        "humans_per_step": humans_per_step},
@@ -494,7 +504,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--frames", type=int, default=8192, help="frames per GPU per step")
-    ap.add_argument("--distinct", type=int, default=256, help="distinct rendered frames")
+    ap.add_argument("--distinct", type=int, default=8192,
+                    help="distinct frames (>= --frames: all distinct, rendered on the GPU; else host-rendered, tiled)")
     ap.add_argument("--e2e-frames", type=int, default=8192, help="frames per e2e step (default: the device step)")
     ap.add_argument("--unfused-frames", type=int, default=256)
     ap.add_argument("--mode", choices=("U", "R"), default="U")

@@ -200,6 +200,17 @@ int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int 
  * 2r+1 taps (if cap allows) and returns r, or -1 for an invalid sigma. */
 int pf_gaussian_taps(double sigma, double *taps, int cap);
 
+/* Synthetic feature maps on the device (the reference synthetic backend's
+ * render_feature_maps, synth.py:93-183): kp_cells [frames][max_humans][K][2]
+ * (row, col) keypoint cells, NaN = missing; n_humans [frames]; outputs conf
+ * [frames][K+1][grid_h][grid_w] and paf [frames][2L][grid_h][grid_w], all
+ * device pointers, on the context's stream.  Input generation for tests and
+ * benchmarks (a GPU-resident producer); fp64 exp() may differ from numpy's
+ * in the last bit, so maps agree with the host renderer up to fp32 rounding
+ * boundaries. */
+int pf_render_maps(pf_ctx *ctx, const double *kp_cells, const int32_t *n_humans, int frames, int max_humans,
+                   int grid_h, int grid_w, double sigma, double halfwidth, float *conf, float *paf);
+
 /* Pinned host allocation helpers for callers without their own allocator. */
 void *pf_host_alloc(size_t bytes);
 void pf_host_free(void *p);

@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "pf_get_results", "pf_sync", "pf_set_debug", "pf_set_option", "pf_kernel_name",
     "pf_get_kernel_times", "pf_get_peaks", "pf_get_connections",
     "pf_preprocess_device", "pf_preprocess_f32_device", "pf_resize_device", "pf_host_alloc", "pf_host_free",
-    "pf_launch_count", "pf_gaussian_taps", "pf_format_records", "pf_format_float",
+    "pf_launch_count", "pf_gaussian_taps", "pf_format_records", "pf_format_float", "pf_render_maps",
 )
 
 
@@ -135,6 +135,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                           ctypes.c_longlong, vp, ctypes.c_longlong]
         lib.pf_format_records.restype = ctypes.c_longlong
         lib.pf_format_float.argtypes = [ctypes.c_double, ctypes.c_char_p, c_int]
+        lib.pf_render_maps.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, ctypes.c_double, ctypes.c_double,
+                                       vp, vp]
+        lib.pf_render_maps.restype = c_int
         lib.pf_format_float.restype = c_int
         lib.pf_gaussian_taps.argtypes = [ctypes.c_double, vp, c_int]
         del i32

@@ -1379,6 +1379,28 @@ int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int 
     return PF_OK;
 }
 
+int pf_render_maps(pf_ctx *ctx, const double *kp_cells, const int32_t *n_humans, int frames, int max_humans,
+                   int grid_h, int grid_w, double sigma, double halfwidth, float *conf, float *paf)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    if (!ctx->has_topo) return fail(ctx, PF_ERR_CONTRACT, "topology not set");
+    if (frames < 0 || max_humans < 0 || grid_h < 0 || grid_w < 0)
+        return fail(ctx, PF_ERR_CONTRACT, "negative extents");
+    if (!(sigma > 0.0) || !(halfwidth > 0.0)) return fail(ctx, PF_ERR_CONFIG, "sigma and halfwidth must be > 0");
+    if ((long long)frames * grid_h * grid_w == 0) return PF_OK;
+    if (!kp_cells || !n_humans || !conf || !paf) return fail(ctx, PF_ERR_CONTRACT, "null pointer");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    RenderArgs a{};
+    a.topo = ctx->topo;
+    a.kp = kp_cells; a.n_humans = n_humans;
+    a.F = frames; a.hmax = max_humans; a.gh = grid_h; a.gw = grid_w;
+    a.sigma = sigma; a.halfwidth = halfwidth;
+    a.conf = conf; a.paf = paf;
+    CU(launch_render_maps(a, ctx->sms, ctx->stream));
+    return PF_OK;
+}
+
 int pf_gaussian_taps(double sigma, double *taps, int cap)
 {
     if (!(sigma > 0.0) || !std::isfinite(sigma) || (int)std::ceil(3.0 * sigma) > kMaxBlurRadius) return -1;

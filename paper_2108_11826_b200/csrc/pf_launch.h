@@ -164,6 +164,17 @@ cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s);    //
 cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s);
 cudaError_t configure_parse_kernels(int max_smem);
 
+// pf_render.cu
+struct RenderArgs {
+    Topo topo;
+    const double *kp;        // [F][hmax][K][2] keypoint cells (row, col); NaN = missing
+    const int *n_humans;     // [F]
+    int F, hmax, gh, gw;
+    double sigma, halfwidth;
+    float *conf, *paf;       // [F][K+1][gh][gw], [F][2L][gh][gw]
+};
+cudaError_t launch_render_maps(const RenderArgs &a, int sms, cudaStream_t s);
+
 // pf_image.cu
 constexpr int kMaxBlurRadius = 64;
 struct BlurTaps { double w[2 * kMaxBlurRadius + 1]; int r; };

@@ -238,3 +238,50 @@ def render_batch(scenes, topo: SkeletonTopology, p: SynthParams):
     """Render scenes into stacked conf [B,K+1,H,W] and paf [B,2L,H,W] arrays."""
     maps = [render_feature_maps(s, topo, p, frame_ref=i) for i, s in enumerate(scenes)]
     return (np.stack([m.conf.array for m in maps]), np.stack([m.paf.array for m in maps]))
+
+
+def render_batch_gpu(scenes, topo: SkeletonTopology, p: SynthParams, device: int = 0):
+    """``render_batch`` on the GPU (pf_render_maps): torch
+    CUDA tensors conf [B,K+1,H,W] and paf [B,2L,H,W].  Input generation only;
+    equal to the host renderer except where fp64 exp() differs from numpy's in
+    the last bit and that decides an fp32 rounding."""
+    import ctypes
+
+    import torch
+
+    from .parser import default_parser
+
+    p.validate()
+    k = topo.n_keypoints
+    if not scenes:
+        raise ContractError("render_batch_gpu needs at least one scene")
+    w0, h0 = scenes[0].input_w, scenes[0].input_h
+    for s in scenes:
+        s.validate(k)
+        if (s.input_w, s.input_h) != (w0, h0):
+            raise ContractError("render_batch_gpu needs scenes of one size")
+    if w0 % p.stride or h0 % p.stride:
+        raise ContractError("scene extents must be divisible by the stride")
+    gh, gw = h0 // p.stride, w0 // p.stride
+    hmax = max(1, max(len(s.humans) for s in scenes))
+    kp = np.full((len(scenes), hmax, k, 2), np.nan, dtype=np.float64)
+    nh = np.zeros(len(scenes), dtype=np.int32)
+    for f, s in enumerate(scenes):
+        nh[f] = len(s.humans)
+        for hh, hum in enumerate(s.humans):
+            for part, xy in enumerate(hum.keypoints):
+                if xy is not None:
+                    kp[f, hh, part] = pixel_to_cell(xy[0], xy[1], p.stride)
+    dev = torch.device("cuda", device)
+    kp_d = torch.from_numpy(kp).to(dev)
+    nh_d = torch.from_numpy(nh).to(dev)
+    conf = torch.empty((len(scenes), k + 1, gh, gw), dtype=torch.float32, device=dev)
+    paf = torch.empty((len(scenes), 2 * topo.n_limbs, gh, gw), dtype=torch.float32, device=dev)
+    eng = default_parser(topo, device)
+    ctx = eng.ctx
+    ctx.check(ctx.lib.pf_set_stream(ctx.handle, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    ctx.check(ctx.lib.pf_render_maps(ctx.handle, ctypes.c_void_p(kp_d.data_ptr()), ctypes.c_void_p(nh_d.data_ptr()),
+                                     len(scenes), hmax, gh, gw, float(p.sigma_conf), float(p.paf_halfwidth),
+                                     ctypes.c_void_p(conf.data_ptr()), ctypes.c_void_p(paf.data_ptr())))
+    torch.cuda.synchronize(dev)
+    return conf, paf

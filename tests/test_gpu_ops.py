@@ -142,3 +142,28 @@ def test_multi_device_parser_and_operator(topo):
     pkts = [pf.Packet(s, 0, (None, m)) for s, m in enumerate(maps)]
     got = [pf.pose_record(p.seq_id, op.fn(p).payload[1], topo) for p in pkts]
     assert got == want[:5]
+
+
+def test_gpu_renderer_matches_host(topo):
+    """pf_render_maps (GPU-resident producer) against the host renderer on
+    procedural and crowded scenes: bit-identical except where fp64 exp()
+    rounds differently from numpy's (then within 1 fp32 ulp), and the parse
+    of both renderings gives the same records."""
+    sp = pf.SynthParams()
+    scenes = [pf.procedural_scene(3, s, 656, 368, sp) for s in range(6)] + [pf.crowd_scene(2, 0)]
+    conf_h, paf_h = pf.synth.render_batch(scenes, topo, sp)
+    conf_g, paf_g = pf.synth.render_batch_gpu(scenes, topo, sp)
+    conf_g, paf_g = conf_g.cpu().numpy(), paf_g.cpu().numpy()
+    assert np.array_equal(paf_g, paf_h)                      # sqrt / division only: exact
+    diff = conf_g != conf_h
+    assert diff.mean() < 1e-3
+    assert np.all(np.abs(conf_g[diff].view(np.int32) - conf_h[diff].view(np.int32)) <= 1)
+    e = pf.PafParser(topo)
+    params = pf.ParserParams(upsample=8)
+    a = e.parse_arrays(conf_h, paf_h, 8, params)
+    ra = [pf.pose_record(f, a.poses(f), topo) for f in range(len(scenes))]
+    b = e.parse_arrays(np.ascontiguousarray(conf_g), np.ascontiguousarray(paf_g), 8, params)
+    rb = [pf.pose_record(f, b.poses(f), topo) for f in range(len(scenes))]
+    e.close()
+    if not diff.any():
+        assert ra == rb
