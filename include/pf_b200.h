@@ -211,6 +211,21 @@ int pf_gaussian_taps(double sigma, double *taps, int cap);
 int pf_render_maps(pf_ctx *ctx, const double *kp_cells, const int32_t *n_humans, int frames, int max_humans,
                    int grid_h, int grid_w, double sigma, double halfwidth, float *conf, float *paf);
 
+/* Overlay rasteriser (the reference's visualize, poseflow/operators.py:173-290).
+ * Primitives in draw order per frame (later overwrite earlier): kind 0 = line
+ * (x0,y0)-(x1,y1) Bresenham-stamped with discs of radius r (thickness // 2);
+ * kind 1 = disc at (x0,y0) of radius r (r = 0: one pixel, for label glyphs).
+ * rgb is the colour as stored in the f32 image. */
+typedef struct {
+    int32_t frame, kind, x0, y0, x1, y1, r;
+    float rgb[3];
+} pf_overlay_prim;
+/* prims / prim_first ([frames + 1], frame f owns prims[prim_first[f] ..
+ * prim_first[f+1])) and img ([frames][h][w][3] f32, drawn in place) are
+ * device pointers; runs on the context's stream. */
+int pf_overlay(pf_ctx *ctx, const pf_overlay_prim *prims, const int32_t *prim_first, int n_prims, int frames,
+               int h, int w, float *img);
+
 /* Pinned host allocation helpers for callers without their own allocator. */
 void *pf_host_alloc(size_t bytes);
 void pf_host_free(void *p);

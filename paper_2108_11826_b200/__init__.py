@@ -41,6 +41,7 @@ from .pipeline_ops import (
     preprocess_batch,
     resize_planes,
 )
+from .overlay import OverlayStyle, part_color, visualize, visualize_batch
 from .sharding import MultiDeviceParser, ShardedResult
 from .skeleton import load_topology, parse_topology
 from .synth import (

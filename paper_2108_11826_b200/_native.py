@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "pf_get_kernel_times", "pf_get_peaks", "pf_get_connections",
     "pf_preprocess_device", "pf_preprocess_f32_device", "pf_resize_device", "pf_host_alloc", "pf_host_free",
     "pf_launch_count", "pf_gaussian_taps", "pf_format_records", "pf_format_float", "pf_render_maps",
+    "pf_overlay",
 )
 
 
@@ -138,6 +139,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pf_render_maps.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, ctypes.c_double, ctypes.c_double,
                                        vp, vp]
         lib.pf_render_maps.restype = c_int
+        lib.pf_overlay.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp]
+        lib.pf_overlay.restype = c_int
         lib.pf_format_float.restype = c_int
         lib.pf_gaussian_taps.argtypes = [ctypes.c_double, vp, c_int]
         del i32

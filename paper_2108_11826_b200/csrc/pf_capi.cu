@@ -148,6 +148,8 @@ struct pf_ctx {
     float *d_pk_score = nullptr;
     int *d_pk_base = nullptr, *d_pair_pp = nullptr, *d_npairs = nullptr, *d_pair_base = nullptr, *d_cand_n = nullptr;
     int2 *d_ferr = nullptr;
+    unsigned *d_owner = nullptr;            // overlay: draw-order owner per pixel
+    size_t overlay_px = 0;
     size_t split_frames = 0;
     int split_cap_frame = 0;
     size_t ws_frames = 0;
@@ -918,7 +920,8 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
                    ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_pk_cell, ctx->d_pk_score,
-                   ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n};
+                   ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n,
+                   ctx->d_owner};
     for (void *p : dev) cudaFree(p);
     void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
                     ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};
@@ -1376,6 +1379,27 @@ int pf_resize_device(pf_ctx *ctx, const float *src, int n_planes, int in_h, int 
     KernelTimer kt(ctx, kResize);
     CU(launch_resize_planes(src, (long long)in_h * in_w, 1, n_planes, in_h, in_w, dst, out_h, out_w, r->d_rec,
                             c->d_rec, ctx->stream));
+    return PF_OK;
+}
+
+int pf_overlay(pf_ctx *ctx, const pf_overlay_prim *prims, const int32_t *prim_first, int n_prims, int frames,
+               int h, int w, float *img)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    if (frames < 0 || h < 0 || w < 0 || n_prims < 0) return fail(ctx, PF_ERR_CONTRACT, "negative extents");
+    if ((long long)frames * h * w == 0) return PF_OK;
+    if (!img || !prim_first || (n_prims > 0 && !prims)) return fail(ctx, PF_ERR_CONTRACT, "null pointer");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    const size_t px = (size_t)frames * h * w;
+    if (px > ctx->overlay_px) {
+        cudaFree(ctx->d_owner);
+        ctx->d_owner = nullptr;
+        ctx->overlay_px = 0;
+        CU(dev_alloc(&ctx->d_owner, px));
+        ctx->overlay_px = px;
+    }
+    CU(launch_overlay(prims, prim_first, n_prims, frames, h, w, ctx->d_owner, img, ctx->sms, ctx->stream));
     return PF_OK;
 }
 

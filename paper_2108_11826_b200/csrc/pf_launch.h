@@ -175,6 +175,11 @@ struct RenderArgs {
 };
 cudaError_t launch_render_maps(const RenderArgs &a, int sms, cudaStream_t s);
 
+// pf_overlay.cu
+using OverlayPrim = pf_overlay_prim;
+cudaError_t launch_overlay(const OverlayPrim *prims, const int *prim_first, int n_prims, int frames, int h, int w,
+                           unsigned *owner, float *img, int sms, cudaStream_t s);
+
 // pf_image.cu
 constexpr int kMaxBlurRadius = 64;
 struct BlurTaps { double w[2 * kMaxBlurRadius + 1]; int r; };
