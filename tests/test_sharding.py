@@ -90,3 +90,30 @@ def test_gloo_world2_matches_single_process(tmp_path):
     want = "\n".join(r for _, r in single) + "\n"
     assert (tmp_path / "merged.jsonl").read_text() == want
     assert float((tmp_path / "tmax").read_text()) == 2.0
+
+
+def test_sharded_result_frame_order():
+    """ShardedResult maps frame indices onto the per-device shards (host logic)."""
+    from paper_2108_11826_b200.sharding import ShardedResult, shard_bounds
+
+    class Fake:
+        def __init__(self, lo, hi):
+            self.lo, self.total_humans = lo, hi - lo
+
+        def poses(self, f):
+            return ["frame", self.lo + f]
+
+    n, world = 11, 4
+    shards = []
+    for r in range(world):
+        lo, hi = shard_bounds(n, r, world)
+        shards.append((lo, Fake(lo, hi) if hi > lo else None))
+    res = ShardedResult(n, shards)
+    assert [p[1] for p in res.all_poses()] == list(range(n))
+    assert res.total_humans == n
+    one = ShardedResult(1, [(0, Fake(0, 1)), (1, None), (1, None)])      # empty trailing shards
+    assert one.poses(0) == ["frame", 0]
+    import pytest
+
+    with pytest.raises(IndexError):
+        res.poses(n)
