@@ -146,7 +146,8 @@ struct pf_ctx {
     int parse_split = PF_PARSE_SPLIT_DEFAULT;
     uint32_t *d_pk_cell = nullptr;          // split parse staging (ensure_split_ws)
     float *d_pk_score = nullptr;
-    int *d_pk_base = nullptr, *d_pair_pp = nullptr, *d_npairs = nullptr, *d_pair_base = nullptr, *d_cand_n = nullptr;
+    int *d_pk_base = nullptr, *d_pair_pp = nullptr, *d_npairs = nullptr, *d_cand_n = nullptr;
+    long long *d_pair_base = nullptr;       // [frames + 1]: prefix, then the total
     int2 *d_ferr = nullptr;
     unsigned *d_owner = nullptr;            // overlay: draw-order owner per pixel
     size_t overlay_px = 0;
@@ -381,8 +382,8 @@ int ensure_split_ws(pf_ctx *ctx, size_t frames)
     CU(dev_alloc(&ctx->d_pk_score, f * cf));
     CU(dev_alloc(&ctx->d_pk_base, f * (PF_MAX_KEYPOINTS + 1)));
     CU(dev_alloc(&ctx->d_pair_pp, f * (PF_MAX_LIMBS + 1)));
-    CU(dev_alloc(&ctx->d_npairs, f + 1));            // + the pair total
-    CU(dev_alloc(&ctx->d_pair_base, f));
+    CU(dev_alloc(&ctx->d_npairs, f));
+    CU(dev_alloc(&ctx->d_pair_base, f + 1));         // + the pair total
     CU(dev_alloc(&ctx->d_ferr, f));
     CU(dev_alloc(&ctx->d_cand_n, f));
     ctx->split_frames = f;
@@ -686,7 +687,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.split = 1;
         a.pk_cell = ctx->d_pk_cell; a.pk_score = ctx->d_pk_score; a.pk_base = ctx->d_pk_base;
         a.pair_pp = ctx->d_pair_pp; a.n_pairs = ctx->d_npairs; a.pair_base = ctx->d_pair_base;
-        a.pair_total = ctx->d_npairs + ctx->split_frames;
+        a.pair_total = ctx->d_pair_base + ctx->split_frames;
         a.ferr = ctx->d_ferr; a.cand_n = ctx->d_cand_n;
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }

@@ -138,7 +138,8 @@ struct ParseArgs {
     float *pk_score;
     int *pk_base;        // [B][K+1] part prefix
     int *pair_pp;        // [B][L+1] pair prefix per limb
-    int *n_pairs, *pair_base, *pair_total;   // [B], [B], scalar
+    int *n_pairs;                            // [B]
+    long long *pair_base, *pair_total;       // [B] exclusive prefix, scalar (64-bit: crowded chunks)
     int2 *ferr;          // [B] capacity error (what, value) from k_parse_peaks
     struct Cand *cand_g; // [B][cap_cands] gated candidates
     int *cand_n;         // [B]

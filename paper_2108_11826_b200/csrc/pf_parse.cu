@@ -696,33 +696,33 @@ k_parse_peaks(const ParseArgs a, int B)
 __global__ void __launch_bounds__(1024)
 k_pair_scan(const ParseArgs a, int B)
 {
-    __shared__ int wsum[32];
-    __shared__ int carry;
+    __shared__ long long wsum[32];
+    __shared__ long long carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int b0 = 0; b0 < B; b0 += 1024) {
         const int b = b0 + threadIdx.x;
-        const int v = b < B ? a.n_pairs[b] : 0;
-        int incl = v;
+        const long long v = b < B ? a.n_pairs[b] : 0;
+        long long incl = v;
 #pragma unroll
         for (int d = 1; d < kWarp; d <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, d);
+            const long long t = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += t;
         }
         if (lane == 31) wsum[warp] = incl;
         __syncthreads();
         if (warp == 0) {
-            int w = wsum[lane];
+            long long w = wsum[lane];
 #pragma unroll
             for (int d = 1; d < kWarp; d <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, w, d);
+                const long long t = __shfl_up_sync(0xffffffffu, w, d);
                 if (lane >= d) w += t;
             }
             wsum[lane] = w;                                // inclusive over warps
         }
         __syncthreads();
-        const int before = carry + (warp ? wsum[warp - 1] : 0);
+        const long long before = carry + (warp ? wsum[warp - 1] : 0);
         if (b < B) a.pair_base[b] = before + incl - v;
         __syncthreads();
         if (threadIdx.x == 1023) carry = before + incl;
@@ -739,9 +739,10 @@ k_score_pairs(const ParseArgs a, int B)
         s_t[u] = __ddiv_rn((double)u, (double)(a.n_samples - 1));
     __syncthreads();
     const int K = a.topo.K, L = a.topo.L;
-    const int total = *a.pair_total;
+    const long long total = *a.pair_total;
     const int max_fail = a.n_samples - a.good_need;
-    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+         g += (long long)gridDim.x * blockDim.x) {
         // frame: last b with pair_base[b] <= g (frames with no pairs share bases)
         int lo = 0, hi = B - 1;
         while (lo < hi) {
@@ -750,7 +751,7 @@ k_score_pairs(const ParseArgs a, int B)
             else hi = mid - 1;
         }
         const int b = lo;
-        const int local0 = g - __ldg(a.pair_base + b);
+        const int local0 = (int)(g - __ldg(a.pair_base + b));
         const int *pp = a.pair_pp + (size_t)b * (L + 1);
         int l = 0;
         while (local0 >= __ldg(pp + l + 1)) ++l;
