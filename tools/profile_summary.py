@@ -3,6 +3,9 @@
 
   python tools/profile_summary.py ROUND LAUNCHES.csv FULL.ncu-rep FRAMES_PER_LAUNCH
 
+  python tools/profile_summary.py --unfused ROUND UNFUSED.ncu-rep FRAMES
+  python tools/profile_summary.py --e2e-pcie ROUND E2E_SYSMEM.csv FRAMES
+
 Writes profiles/<ROUND>_launches.md, profiles/<ROUND>_ncu_full.md and
 profiles/<ROUND>_traffic.json (dram bytes per launch of each profiled kernel,
 read by bench.py for the roofline "traffic" field).
@@ -74,7 +77,68 @@ def to_bytes(v):
     return float(val.replace(",", "")) * BYTES.get(unit, 1)
 
 
+# materialised Mode U kernels (tools/unfused_run.py): compulsory bytes per frame
+UNFUSED_ALG = {"k_resize_planes": 18 * 46 * 82 * 4 + 18 * 368 * 656 * 4, "k_nms_plane": 18 * 368 * 656 * 4}
+
+
+def unfused(rnd, rep, frames):
+    """profiles/<rnd>_ncu_unfused.md from the --set full capture of tools/unfused_run.py."""
+    path = os.path.join(ROOT, "profiles", f"{rnd}_ncu_unfused.md")
+    with open(path, "w") as f:
+        f.write(f"# {rnd}: ncu --set full of the materialised Mode U kernels (first launch of each: {frames} frames "
+                "= the 2 GiB workspace chunk)\n\n`python tools/unfused_run.py`.  Algorithmic bytes per frame: "
+                f"resize = read 18 low-res part planes + write 18 x 368x656 f32 = {UNFUSED_ALG['k_resize_planes']:,} B; "
+                f"NMS = read 18 x 368x656 f32 = {UNFUSED_ALG['k_nms_plane']:,} B.\n\n")
+        seen = set()
+        for d in full_metrics(rep):
+            if d["kernel"] in seen or d["kernel"] not in UNFUSED_ALG:
+                continue
+            seen.add(d["kernel"])
+            f.write(f"## {d['kernel']}\n\n| metric | value | unit |\n|---|---|---|\n")
+            for k, v in d.items():
+                if k not in ("kernel", "stalls"):
+                    f.write(f"| {k} | {v[0]} | {v[1]} |\n")
+            rd, wr = to_bytes(d["dram__bytes_read.sum"]), to_bytes(d["dram__bytes_write.sum"])
+            us = float(d["gpu__time_duration.sum"][0].replace(",", "")) * UNITS[d["gpu__time_duration.sum"][1]]
+            alg = UNFUSED_ALG[d["kernel"]]
+            f.write(f"| dram read+write per frame | {(rd + wr) / frames:.0f} | byte |\n")
+            f.write(f"| algorithmic bytes per frame | {alg} | byte |\n")
+            f.write(f"| algorithmic GB/s (cold, serialised) | {alg * frames / us / 1e3:.0f} | GB/s |\n")
+            f.write("\nTop stall reasons (warps per issue): " +
+                    ", ".join(f"{n} {x:.2f}" for x, n in d["stalls"]) + "\n\n")
+    print(open(path).read())
+
+
+def e2e_pcie(rnd, csv_path, frames):
+    """profiles/<rnd>_e2e_pcie.json from tools/e2e_sysmem.py under ncu (PCIe metrics)."""
+    rows = list(csv.reader(open(csv_path)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hi]
+    ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    agg = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        name = r[ki].split("(")[0].replace("void ", "").split("<")[0]
+        m = agg.setdefault(name, collections.OrderedDict())
+        m[r[mi]] = m.get(r[mi], 0.0) + float(r[vi].replace(",", ""))
+    out = {"what": f"PCIe traffic of one pf_parse_host call ({frames} pinned frames of the bench e2e workload) "
+                   "with the PAF read in place (PF_OPT_PAF_ZERO_COPY) by the one-kernel k_parse_frames",
+           "command": "ncu --metrics syslts__d_sectors_fill_sysmem.sum,pcie__read_bytes.sum,pcie__write_bytes.sum,"
+                      "gpu__time_duration.sum python tools/e2e_sysmem.py", "frames": frames}
+    out.update(agg)
+    pk = agg.get("k_parse_frames", {})
+    out["paf_read_in_place_bytes_per_frame"] = round(pk.get("pcie__read_bytes.sum", 0.0) / frames)
+    out["paf_sysmem_sector_fill_bytes_per_frame"] = round(pk.get("syslts__d_sectors_fill_sysmem.sum", 0.0) * 32 / frames)
+    out["paf_bytes_per_frame_if_copied"] = 38 * 46 * 82 * 4
+    with open(os.path.join(ROOT, "profiles", f"{rnd}_e2e_pcie.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+
+
 def main():
+    if sys.argv[1] == "--unfused":
+        return unfused(sys.argv[2], sys.argv[3], int(sys.argv[4]))
+    if sys.argv[1] == "--e2e-pcie":
+        return e2e_pcie(sys.argv[2], sys.argv[3], int(sys.argv[4]))
     rnd, lpath, rep, frames = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
