@@ -55,7 +55,8 @@ __device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y)
 struct CandStore {
     Cand *s;
     Cand *g;
-    __device__ __forceinline__ Cand &operator[](int i) const { return i < kCandSmem ? s[i] : g[i - kCandSmem]; }
+    int ns;              // entries in shared memory
+    __device__ __forceinline__ Cand &operator[](int i) const { return i < ns ? s[i] : g[i - ns]; }
 };
 
 // PAF value pair at parse-grid cell (ci, cj): the feature grid itself
@@ -174,7 +175,10 @@ k_parse_frames(const ParseArgs a)
     __shared__ int s_seg[PF_MAX_LIMBS + 1];     // candidate segment start per limb
     __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base;
     __shared__ int s_lcnt[PF_MAX_LIMBS], s_lcur[PF_MAX_LIMBS];
-    __shared__ uint16_t s_bucket[kCandSmem], s_order[kCandSmem];   // by limb; sorted within limb
+    // split: fewer candidates in shared memory and the peak table read from
+    // the k_parse_peaks slab, so more frames stay resident per SM
+    constexpr int CS = SPLIT ? kCandSmemSplit : kCandSmem;
+    __shared__ uint16_t s_bucket[CS], s_order[CS];   // by limb; sorted within limb
     __shared__ int8_t s_la[PF_MAX_LIMBS], s_lb[PF_MAX_LIMBS];
     __shared__ int16_t s_cx[PF_MAX_LIMBS], s_cy[PF_MAX_LIMBS];
     __shared__ double s_t[kParseTTab];          // u / (n - 1), paf.py:139
@@ -186,11 +190,14 @@ k_parse_frames(const ParseArgs a)
     }
 
     // ---- shared layout (sizes from the caps; see parse_smem_bytes) ----
-    Cand *cand_s = reinterpret_cast<Cand *>(smem_raw);                       // kCandSmem
-    double *h_score = reinterpret_cast<double *>(cand_s + kCandSmem);        // cap_humans (conn, then final)
-    uint32_t *p_cell = reinterpret_cast<uint32_t *>(h_score + a.cap_humans); // cap_frame
-    float *p_score = reinterpret_cast<float *>(p_cell + a.cap_frame);        // cap_frame
-    uint32_t *h_mask = reinterpret_cast<uint32_t *>(p_score + a.cap_frame);  // cap_humans
+    Cand *cand_s = reinterpret_cast<Cand *>(smem_raw);                       // CS
+    double *h_score = reinterpret_cast<double *>(cand_s + CS);               // cap_humans (conn, then final)
+    uint32_t *p_cell = SPLIT ? const_cast<uint32_t *>(a.pk_cell) + (size_t)b * a.cap_frame
+                             : reinterpret_cast<uint32_t *>(h_score + a.cap_humans);   // cap_frame
+    float *p_score = SPLIT ? const_cast<float *>(a.pk_score) + (size_t)b * a.cap_frame
+                           : reinterpret_cast<float *>(p_cell + a.cap_frame);          // cap_frame
+    uint32_t *h_mask = SPLIT ? reinterpret_cast<uint32_t *>(h_score + a.cap_humans)
+                             : reinterpret_cast<uint32_t *>(p_score + a.cap_frame);    // cap_humans
     int *h_pos = reinterpret_cast<int *>(h_mask + a.cap_humans);             // cap_humans
     const int bm_words = (a.cap_frame + 31) / 32;
     uint32_t *used = reinterpret_cast<uint32_t *>(h_pos + a.cap_humans);     // n_warps*2*bm_words
@@ -201,8 +208,10 @@ k_parse_frames(const ParseArgs a)
     int8_t *h_alive = h_n + a.cap_humans;                                     // cap_humans
     // split: the frame's candidates already sit in cand_g; entries past the
     // shared part are used (and sorted) in place there
-    const CandStore cand{cand_s, SPLIT ? a.cand_g + (size_t)b * a.cap_cands + kCandSmem
-                                       : reinterpret_cast<Cand *>(a.cand_spill) + (size_t)b * (a.cap_cands - kCandSmem)};
+    const CandStore cand{cand_s,
+                         SPLIT ? a.cand_g + (size_t)b * a.cap_cands + CS
+                               : reinterpret_cast<Cand *>(a.cand_spill) + (size_t)b * (a.cap_cands - kCandSmem),
+                         CS};
 
     // ---- 1. peak counts, prefix, capacity checks; reset counters ----
     if (tid == 0) { s_err = 0; s_ncand = 0; }
@@ -243,11 +252,7 @@ k_parse_frames(const ParseArgs a)
 
     // ---- 2. rank-sort each part's peaks (read straight from the NMS slab) ----
     if (SPLIT) {
-        for (int e = tid; e < P; e += nthr) {
-            p_cell[e] = __ldcg(a.pk_cell + (size_t)b * a.cap_frame + e);
-            p_score[e] = __ldcg(a.pk_score + (size_t)b * a.cap_frame + e);
-            owner[e] = -1;
-        }
+        for (int e = tid; e < P; e += nthr) owner[e] = -1;
     }
     for (int e = tid; !SPLIT && e < P; e += nthr) {
         int part = 0;
@@ -327,7 +332,7 @@ k_parse_frames(const ParseArgs a)
         const Cand *cg = a.cand_g + (size_t)b * a.cap_cands;
         for (int i = tid; i < ncg && i < a.cap_cands; i += nthr) {
             const Cand c = cg[i];
-            if (i < kCandSmem) cand_s[i] = c;
+            if (i < CS) cand_s[i] = c;
             atomicAdd(&s_lcnt[c.lg >> 24], 1);
         }
         if (tid == 0) s_ncand = ncg;
@@ -350,7 +355,7 @@ k_parse_frames(const ParseArgs a)
     // ranks its bucket (the key is a total order, so ranks are distinct) and
     // its lane 0 walks the ranks with used-bitmaps — no CTA-wide sort.
     // Crowded frames (spill slab): bitonic sort over the whole store.
-    const bool fast = nc <= kCandSmem;
+    const bool fast = nc <= CS;
     if (fast) {
         if (tid == 0) {
             int acc = 0;
@@ -778,13 +783,13 @@ k_score_pairs(const ParseArgs a, int B)
     }
 }
 
-size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps)
+size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps, bool split)
 {
     (void)cap_cands;
     const int bm_words = (cap_frame + 31) / 32;
-    size_t s = (size_t)kCandSmem * sizeof(Cand);
+    size_t s = (size_t)(split ? kCandSmemSplit : kCandSmem) * sizeof(Cand);
     s += (size_t)cap_humans * sizeof(double);
-    s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
+    if (!split) s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
     s += (size_t)cap_humans * (sizeof(uint32_t) + sizeof(int));
     s += (size_t)n_warps * 2 * bm_words * sizeof(uint32_t);
     s += (size_t)cap_frame * sizeof(int16_t);
