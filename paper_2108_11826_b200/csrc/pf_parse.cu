@@ -200,8 +200,8 @@ k_parse_frames(const ParseArgs a)
                              : reinterpret_cast<uint32_t *>(p_score + a.cap_frame);    // cap_humans
     int *h_pos = reinterpret_cast<int *>(h_mask + a.cap_humans);             // cap_humans
     const int bm_words = (a.cap_frame + 31) / 32;
-    uint32_t *used = reinterpret_cast<uint32_t *>(h_pos + a.cap_humans);     // n_warps*2*bm_words
-    int16_t *owner = reinterpret_cast<int16_t *>(used + n_warps * 2 * bm_words);  // cap_frame
+    uint32_t *used = reinterpret_cast<uint32_t *>(h_pos + a.cap_humans);     // max(n_warps, L)*2*bm_words
+    int16_t *owner = reinterpret_cast<int16_t *>(used + max(n_warps, L) * 2 * bm_words);  // cap_frame
     int16_t *h_parts = owner + a.cap_frame;                                   // cap_humans*K
     int8_t *h_order = reinterpret_cast<int8_t *>(h_parts + a.cap_humans * K); // cap_humans*K
     int8_t *h_n = h_order + a.cap_humans * K;                                 // cap_humans
@@ -413,25 +413,25 @@ k_parse_frames(const ParseArgs a)
     // sorted position e -> candidate
     auto at = [&](int e) -> Cand & { return fast ? cand_s[s_order[e]] : cand[e]; };
 
-    uint32_t *used_a = used + warp * 2 * bm_words;
-    uint32_t *used_b = used_a + bm_words;
-    for (int l = warp; l < L; l += n_warps) {
-        const int s0 = s_seg[l], s1 = s_seg[l + 1];
-        if (s0 == s1) continue;                           // warp-uniform
-        if (fast) {
-            for (int k = s0 + lane; k < s1; k += kWarp) {
-                const int i = s_bucket[k];
-                const Cand c = cand_s[i];
-                int rank = 0;
-                for (int k2 = s0; k2 < s1; ++k2) rank += cand_less(cand_s[s_bucket[k2]], c);
-                s_order[s0 + rank] = uint16_t(i);
-            }
+    if (fast) {
+        // rank within the limb, thread per candidate (the key is a total
+        // order, so ranks are distinct) ...
+        for (int k = tid; k < nc; k += nthr) {
+            const int i = s_bucket[k];
+            const Cand c = cand_s[i];
+            const int l = int(c.lg >> 24);
+            const int s0 = s_seg[l], s1 = s_seg[l + 1];
+            int rank = 0;
+            for (int k2 = s0; k2 < s1; ++k2) rank += cand_less(cand_s[s_bucket[k2]], c);
+            s_order[s0 + rank] = uint16_t(i);
         }
-        for (int q = lane; q < bm_words; q += kWarp) { used_a[q] = 0u; used_b[q] = 0u; }
-        __syncwarp();
-        if (lane == 0) {
-            for (int e = s0; e < s1; ++e) {
-                Cand &c = at(e);
+        for (int q = tid; q < L * 2 * bm_words; q += nthr) used[q] = 0u;
+        __syncthreads();
+        // ... then every limb's greedy walk at once, thread per limb
+        for (int l = tid; l < L; l += nthr) {
+            uint32_t *used_a = used + l * 2 * bm_words, *used_b = used_a + bm_words;
+            for (int e = s_seg[l], e1 = s_seg[l + 1]; e < e1; ++e) {
+                Cand &c = cand_s[s_order[e]];
                 const uint32_t ab = c.ab;
                 const int ia = int((ab >> 16) & 0x7fff), ib = int(ab & 0xffff);
                 if ((used_a[ia >> 5] >> (ia & 31)) & 1u) continue;
@@ -441,7 +441,28 @@ k_parse_frames(const ParseArgs a)
                 c.ab = ab | kAccepted;
             }
         }
-        __syncwarp();
+    } else {
+        uint32_t *used_a = used + warp * 2 * bm_words;
+        uint32_t *used_b = used_a + bm_words;
+        for (int l = warp; l < L; l += n_warps) {
+            const int s0 = s_seg[l], s1 = s_seg[l + 1];
+            if (s0 == s1) continue;                           // warp-uniform
+            for (int q = lane; q < bm_words; q += kWarp) { used_a[q] = 0u; used_b[q] = 0u; }
+            __syncwarp();
+            if (lane == 0) {
+                for (int e = s0; e < s1; ++e) {
+                    Cand &c = cand[e];
+                    const uint32_t ab = c.ab;
+                    const int ia = int((ab >> 16) & 0x7fff), ib = int(ab & 0xffff);
+                    if ((used_a[ia >> 5] >> (ia & 31)) & 1u) continue;
+                    if ((used_b[ib >> 5] >> (ib & 31)) & 1u) continue;
+                    used_a[ia >> 5] |= 1u << (ia & 31);
+                    used_b[ib >> 5] |= 1u << (ib & 31);
+                    c.ab = ab | kAccepted;
+                }
+            }
+            __syncwarp();
+        }
     }
     __syncthreads();
     if (a.debug && tid == 0) {
@@ -783,7 +804,7 @@ k_score_pairs(const ParseArgs a, int B)
     }
 }
 
-size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int n_warps, bool split)
+size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int L, int n_warps, bool split)
 {
     (void)cap_cands;
     const int bm_words = (cap_frame + 31) / 32;
@@ -791,7 +812,7 @@ size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int
     s += (size_t)cap_humans * sizeof(double);
     if (!split) s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
     s += (size_t)cap_humans * (sizeof(uint32_t) + sizeof(int));
-    s += (size_t)n_warps * 2 * bm_words * sizeof(uint32_t);
+    s += (size_t)(n_warps > L ? n_warps : L) * 2 * bm_words * sizeof(uint32_t);
     s += (size_t)cap_frame * sizeof(int16_t);
     s += (size_t)cap_humans * K * (sizeof(int16_t) + sizeof(int8_t));
     s += (size_t)cap_humans * 2;
