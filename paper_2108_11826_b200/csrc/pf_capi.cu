@@ -692,7 +692,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }
     const int threads = psplit ? kParseFinThreads : kParseThreads;
-    const size_t smem = parse_smem_bytes(a.cap_frame, a.cap_cands, a.cap_humans, K, ctx->topo.L, threads / 32, psplit);
+    const size_t smem =
+        parse_smem_bytes(a.cap_frame, a.cap_part, a.cap_cands, a.cap_humans, K, ctx->topo.L, threads / 32, psplit);
     if (a.split) {
         {
             KernelTimer kt(ctx, kParsePeaks, 2);   // k_parse_peaks + k_pair_scan
@@ -793,9 +794,9 @@ bool grow_cap(pf_ctx *ctx, const Status &st)
     default:
         return false;
     }
-    const size_t smem = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
-                                         PF_MAX_KEYPOINTS, PF_MAX_LIMBS, std::max(kParseThreads, kParseFinThreads) / 32,
-                                         false) + 2048;
+    const size_t smem = parse_smem_bytes(c.max_peaks_per_frame, c.max_peaks_per_part, c.max_candidates,
+                                         c.max_humans_per_frame, PF_MAX_KEYPOINTS, PF_MAX_LIMBS,
+                                         std::max(kParseThreads, kParseFinThreads) / 32, false) + 2048;
     if (smem > (size_t)ctx->max_smem) return false;
     if (c.max_peaks_per_part == ctx->caps.max_peaks_per_part && c.max_candidates == ctx->caps.max_candidates &&
         c.max_peaks_per_frame == ctx->caps.max_peaks_per_frame &&
@@ -902,9 +903,9 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
         cu(configure_corner_kernels(max_smem), "configure k_nms_up_corner") ||
         cu(configure_parse_kernels(max_smem), "configure k_parse_frames"))
         return bail(PF_ERR_CUDA);
-    const size_t need = parse_smem_bytes(c.max_peaks_per_frame, c.max_candidates, c.max_humans_per_frame,
-                                         PF_MAX_KEYPOINTS, PF_MAX_LIMBS, std::max(kParseThreads, kParseFinThreads) / 32,
-                                         false) + 2048;
+    const size_t need = parse_smem_bytes(c.max_peaks_per_frame, c.max_peaks_per_part, c.max_candidates,
+                                         c.max_humans_per_frame, PF_MAX_KEYPOINTS, PF_MAX_LIMBS,
+                                         std::max(kParseThreads, kParseFinThreads) / 32, false) + 2048;
     if (need > (size_t)max_smem) {
         fail(ctx, PF_ERR_CONFIG, "caps need %zu B of shared memory per frame CTA (> %d)", need, max_smem);
         return bail(PF_ERR_CONFIG);

@@ -163,7 +163,8 @@ constexpr int kParseFinThreads = PF_PARSE_FIN_THREADS;   // k_parse_frames<true>
 size_t cand_spill_bytes_per_frame(int cap_cands);
 size_t cand_record_bytes();
 enum { kCapPart = 1, kCapFrame = 2, kCapCands = 3, kCapHumans = 4, kCapPool = 5 };
-size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int L, int n_warps, bool split);
+size_t parse_smem_bytes(int cap_frame, int cap_part, int cap_cands, int cap_humans, int K, int L, int n_warps,
+                        bool split);
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s);
 cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s);    // k_parse_peaks + k_pair_scan
 cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s);

@@ -28,6 +28,8 @@
 //                      filters (paf.py:276-281), stable rank by -score
 //                      (paf.py:288), cell_to_pixel (types.py:233-235), and a
 //                      compact write into the output pool.
+#include <algorithm>
+
 #include "pf_launch.h"
 
 namespace pf {
@@ -200,8 +202,9 @@ k_parse_frames(const ParseArgs a)
                              : reinterpret_cast<uint32_t *>(p_score + a.cap_frame);    // cap_humans
     int *h_pos = reinterpret_cast<int *>(h_mask + a.cap_humans);             // cap_humans
     const int bm_words = (a.cap_frame + 31) / 32;
-    uint32_t *used = reinterpret_cast<uint32_t *>(h_pos + a.cap_humans);     // max(n_warps, L)*2*bm_words
-    int16_t *owner = reinterpret_cast<int16_t *>(used + max(n_warps, L) * 2 * bm_words);  // cap_frame
+    const int pm_words = (a.cap_part + 31) / 32;
+    uint32_t *used = reinterpret_cast<uint32_t *>(h_pos + a.cap_humans);     // used_words(), see parse_smem_bytes
+    int16_t *owner = reinterpret_cast<int16_t *>(used + max(n_warps * 2 * bm_words, L * 2 * pm_words));  // cap_frame
     int16_t *h_parts = owner + a.cap_frame;                                   // cap_humans*K
     int8_t *h_order = reinterpret_cast<int8_t *>(h_parts + a.cap_humans * K); // cap_humans*K
     int8_t *h_n = h_order + a.cap_humans * K;                                 // cap_humans
@@ -425,15 +428,17 @@ k_parse_frames(const ParseArgs a)
             for (int k2 = s0; k2 < s1; ++k2) rank += cand_less(cand_s[s_bucket[k2]], c);
             s_order[s0 + rank] = uint16_t(i);
         }
-        for (int q = tid; q < L * 2 * bm_words; q += nthr) used[q] = 0u;
+        for (int q = tid; q < L * 2 * pm_words; q += nthr) used[q] = 0u;
         __syncthreads();
-        // ... then every limb's greedy walk at once, thread per limb
+        // ... then every limb's greedy walk at once, thread per limb (used
+        // bitmaps over the peak's index within its part)
         for (int l = tid; l < L; l += nthr) {
-            uint32_t *used_a = used + l * 2 * bm_words, *used_b = used_a + bm_words;
+            uint32_t *used_a = used + l * 2 * pm_words, *used_b = used_a + pm_words;
+            const int ba = s_base[s_la[l]], bb = s_base[s_lb[l]];
             for (int e = s_seg[l], e1 = s_seg[l + 1]; e < e1; ++e) {
                 Cand &c = cand_s[s_order[e]];
                 const uint32_t ab = c.ab;
-                const int ia = int((ab >> 16) & 0x7fff), ib = int(ab & 0xffff);
+                const int ia = int((ab >> 16) & 0x7fff) - ba, ib = int(ab & 0xffff) - bb;
                 if ((used_a[ia >> 5] >> (ia & 31)) & 1u) continue;
                 if ((used_b[ib >> 5] >> (ib & 31)) & 1u) continue;
                 used_a[ia >> 5] |= 1u << (ia & 31);
@@ -804,15 +809,16 @@ k_score_pairs(const ParseArgs a, int B)
     }
 }
 
-size_t parse_smem_bytes(int cap_frame, int cap_cands, int cap_humans, int K, int L, int n_warps, bool split)
+size_t parse_smem_bytes(int cap_frame, int cap_part, int cap_cands, int cap_humans, int K, int L, int n_warps,
+                        bool split)
 {
     (void)cap_cands;
-    const int bm_words = (cap_frame + 31) / 32;
+    const int bm_words = (cap_frame + 31) / 32, pm_words = (cap_part + 31) / 32;
     size_t s = (size_t)(split ? kCandSmemSplit : kCandSmem) * sizeof(Cand);
     s += (size_t)cap_humans * sizeof(double);
     if (!split) s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
     s += (size_t)cap_humans * (sizeof(uint32_t) + sizeof(int));
-    s += (size_t)(n_warps > L ? n_warps : L) * 2 * bm_words * sizeof(uint32_t);
+    s += (size_t)std::max(n_warps * 2 * bm_words, L * 2 * pm_words) * sizeof(uint32_t);
     s += (size_t)cap_frame * sizeof(int16_t);
     s += (size_t)cap_humans * K * (sizeof(int16_t) + sizeof(int8_t));
     s += (size_t)cap_humans * 2;
