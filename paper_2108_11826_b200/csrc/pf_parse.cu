@@ -533,12 +533,16 @@ k_parse_frames(const ParseArgs a)
                 const int hidx = ha >= 0 ? ha : hb;
                 const int part = ha >= 0 ? b_part : a_part;
                 const int pid = ha >= 0 ? pb : pa;
-                if (!((h_mask[hidx] >> part) & 1u)) {
+                // one round of independent loads, then the stores
+                const uint32_t m = h_mask[hidx];
+                const int nn = h_n[hidx];
+                const double hs = h_score[hidx];
+                if (!((m >> part) & 1u)) {
                     h_parts[hidx * K + part] = int16_t(pid);
-                    h_order[hidx * K + h_n[hidx]] = int8_t(part);
-                    h_n[hidx] = int8_t(h_n[hidx] + 1);
-                    h_mask[hidx] |= 1u << part;
-                    h_score[hidx] = dadd(h_score[hidx], c.score);
+                    h_order[hidx * K + nn] = int8_t(part);
+                    h_n[hidx] = int8_t(nn + 1);
+                    h_mask[hidx] = m | (1u << part);
+                    h_score[hidx] = dadd(hs, c.score);
                     owner[pid] = int16_t(hidx);
                 }
             }
@@ -577,6 +581,13 @@ k_parse_frames(const ParseArgs a)
         h_pos[hh] = keep ? 1 : 0;
     }
     __syncthreads();
+    // the frame's slice of the pool: thread 0's atomic is in flight while
+    // the ranks are computed
+    int pool_base = 0, nk = 0;
+    if (tid == 0) {
+        for (int hh = 0; hh < nh; ++hh) nk += h_pos[hh];
+        if (nk) pool_base = atomicAdd(&a.st->pool_used, nk);
+    }
     // stable rank by -score among kept humans (paf.py:288)
     for (int hh = tid; hh < nh; hh += nthr) {
         if (!h_pos[hh]) continue;
@@ -591,9 +602,7 @@ k_parse_frames(const ParseArgs a)
     }
     __syncthreads();
     if (tid == 0) {
-        int nk = 0;
-        for (int hh = 0; hh < nh; ++hh) nk += h_pos[hh];
-        const int base = nk ? atomicAdd(&a.st->pool_used, nk) : 0;
+        const int base = pool_base;
         if (base + nk > a.pool_cap) {
             report_capacity(a.st, gframe, kCapPool, base + nk);
             s_pool_base = -1;
