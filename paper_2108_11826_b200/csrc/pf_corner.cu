@@ -505,7 +505,7 @@ __device__ __noinline__ void redo_plane(const UpCornerArgs &a, const Bands &bd, 
 #endif
 template <int NWS>   // hot words per source row, (w + 31) / 32: fixed so phase A is straight-line code
 __global__ void __launch_bounds__(kCornerThreads, PF_CORNER_MINB)
-k_nms_up_corner(const UpCornerArgs a)
+k_nms_up_corner(const __grid_constant__ UpCornerArgs a)
 {
     extern __shared__ __align__(128) unsigned char smc[];
     const int h = a.h, w = a.w, hw = h * w;
@@ -1027,7 +1027,7 @@ __device__ __noinline__ void classify_inline(const UpCornerArgs &a, const Bands 
 
 
 __global__ void __launch_bounds__(kFinThreads, 4)
-k_corner_finish(const UpCornerArgs a)
+k_corner_finish(const __grid_constant__ UpCornerArgs a)
 {
     extern __shared__ __align__(16) unsigned char smf[];
     const int nbr = a.nbr, nbc = a.nbc;
@@ -1092,7 +1092,7 @@ k_corner_finish(const UpCornerArgs a)
 constexpr int kCrowdCands = 2048;
 
 __global__ void __launch_bounds__(kFinThreads, 3)
-k_corner_crowded(const UpCornerArgs a)
+k_corner_crowded(const __grid_constant__ UpCornerArgs a)
 {
     extern __shared__ __align__(16) unsigned char smf[];
     const int nbr = a.nbr, nbc = a.nbc;
