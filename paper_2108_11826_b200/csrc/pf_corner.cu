@@ -803,6 +803,7 @@ __global__ void __launch_bounds__(kScanThreads, PF_SCAN_MINB)
 k_nms_up_scan(const UpCornerArgs a)
 {
     extern __shared__ __align__(128) unsigned char smc[];
+    pdl_trigger();                                       // k_corner_finish may queue behind the persistent grid
     const int h = a.h, w = a.w, hw = h * w;
     const int nbr = a.nbr, nbc = a.nbc, nst = a.nst;
     const ScanLayout L = scan_layout(h, w, nst);
@@ -1042,6 +1043,8 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
         else fill_band(a.cols, a.cdt, a.cband, b - nbr, CB[b - nbr], CT[b - nbr]);
     }
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();                                          // the scan's survivors
     const int grp = threadIdx.x / kFinGroup, gl = threadIdx.x % kFinGroup;
     const unsigned gmask = kFinGroup == kWarp ? 0xffffffffu
                                               : ((1u << kFinGroup) - 1u) << ((threadIdx.x & 31) & ~(kFinGroup - 1));
@@ -1102,6 +1105,8 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a)
     BandT *CT = RT + nbr;
     uint32_t *cand = reinterpret_cast<uint32_t *>(CT + nbc);
     __shared__ int n_cand, n_pk;
+    pdl_trigger();
+    pdl_wait();                                          // the crowd list and the finished planes' counts
     const int nlist = min(*a.crowd_n, a.B * a.K);
     if ((int)blockIdx.x >= nlist) return;                 // the usual case: nothing crowded
     for (int b = threadIdx.x; b < nbr + nbc; b += kFinThreads) {
@@ -1173,7 +1178,9 @@ cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s)
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const long long need = (P * (kCornerSurv / kFinGroup) + kFinGroups - 1) / kFinGroups;
-    k_corner_finish<<<(unsigned)std::min<long long>(need, (long long)occ * sms), kFinThreads, smem, s>>>(a);
+    e = launch_pdl(k_corner_finish, dim3((unsigned)std::min<long long>(need, (long long)occ * sms)), dim3(kFinThreads),
+                   smem, s, a);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -1186,7 +1193,9 @@ cudaError_t launch_corner_crowded(const UpCornerArgs &a, cudaStream_t s)
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
     const size_t smem_c = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) + kCrowdCands * sizeof(uint32_t);
-    k_corner_crowded<<<(unsigned)std::min<long long>(P, (long long)sms * 3), kFinThreads, smem_c, s>>>(a);
+    e = launch_pdl(k_corner_crowded, dim3((unsigned)std::min<long long>(P, (long long)sms * 3)), dim3(kFinThreads),
+                   smem_c, s, a);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -6,6 +6,34 @@
 
 namespace pf {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// launch_pdl may start while its predecessor on the stream drains; it runs
+// its input-independent prologue, then pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible.  pdl_trigger()
+// lets the successor be scheduled before this grid exits.  Both are no-ops
+// for an ordinary launch.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+#endif
+
 // One output coordinate of operators.bilinear_resize packed for a single
 // 16-byte load: i0 | i1 << 16, t (1 - t is recomputed: the host's omt is the
 // same single rounded subtraction).

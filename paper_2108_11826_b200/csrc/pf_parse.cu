@@ -170,6 +170,7 @@ k_parse_frames(const ParseArgs a)
     const int b = blockIdx.x;
     const int gframe = a.frame_base + b;
     const int tid = threadIdx.x, nthr = blockDim.x;
+    pdl_wait();                                          // peaks / candidates of the previous kernels
     const int warp = tid / kWarp, lane = tid % kWarp, n_warps = nthr / kWarp;
 
     __shared__ int s_base[PF_MAX_KEYPOINTS + 1];
@@ -661,6 +662,8 @@ k_parse_peaks(const ParseArgs a, int B)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * kPeakFrames + warp;
     __shared__ int s_base[kPeakFrames][PF_MAX_KEYPOINTS + 1];
+    pdl_trigger();
+    pdl_wait();                                          // the NMS slabs
     if (b >= B) return;
     const int gframe = a.frame_base + b;
     int c = 0;
@@ -738,6 +741,8 @@ k_pair_scan(const ParseArgs a, int B)
 {
     __shared__ long long wsum[32];
     __shared__ long long carry;
+    pdl_trigger();
+    pdl_wait();
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -778,6 +783,8 @@ k_score_pairs(const ParseArgs a, int B)
     for (int u = threadIdx.x; u < kParseTTab && u < a.n_samples; u += blockDim.x)
         s_t[u] = __ddiv_rn((double)u, (double)(a.n_samples - 1));
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();                                          // pair offsets of k_pair_scan
     const int K = a.topo.K, L = a.topo.L;
     const long long total = *a.pair_total;
     const int max_fail = a.n_samples - a.good_need;
@@ -844,19 +851,18 @@ size_t cand_spill_bytes_per_frame(int cap_cands)
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s)
 {
     if (B == 0) return cudaSuccess;
-    if (a.split) k_parse_frames<true><<<B, threads, smem, s>>>(a);
-    else k_parse_frames<false><<<B, threads, smem, s>>>(a);
+    if (a.split) return launch_pdl(k_parse_frames<true>, dim3(B), dim3(threads), smem, s, a);
+    k_parse_frames<false><<<B, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s)
 {
     if (B == 0) return cudaSuccess;
-    k_parse_peaks<<<(B + kPeakFrames - 1) / kPeakFrames, kPeakFrames * kWarp, 0, s>>>(a, B);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(k_parse_peaks, dim3((B + kPeakFrames - 1) / kPeakFrames), dim3(kPeakFrames * kWarp), 0,
+                               s, a, B);
     if (e != cudaSuccess) return e;
-    k_pair_scan<<<1, 1024, 0, s>>>(a, B);
-    return cudaGetLastError();
+    return launch_pdl(k_pair_scan, dim3(1), dim3(1024), 0, s, a, B);
 }
 
 cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s)
@@ -866,8 +872,7 @@ cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s)
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    k_score_pairs<<<sms * 8, kScoreThreads, 0, s>>>(a, B);
-    return cudaGetLastError();
+    return launch_pdl(k_score_pairs, dim3(sms * 8), dim3(kScoreThreads), 0, s, a, B);
 }
 
 cudaError_t configure_parse_kernels(int max_smem)
