@@ -770,7 +770,10 @@ k_nms_up_corner(const __grid_constant__ UpCornerArgs a)
 // walks the hot words instead); a plane with more than kCornerSurv survivors
 // is marked crowded (surv_n = -2) and k_corner_crowded walks it from the
 // sources.
-constexpr int kScanThreads = 128;
+#ifndef PF_SCAN_THREADS
+#define PF_SCAN_THREADS 96   // three warps: measured 0.593 vs 0.615 ms (128), 0.630 (64), 0.68-0.81 (160-256)
+#endif
+constexpr int kScanThreads = PF_SCAN_THREADS;
 constexpr int kScanCrowd = 64;       // more survivors than this: k_corner_crowded (CTA per plane)
 #ifndef PF_SCAN_MINB
 #define PF_SCAN_MINB 10
