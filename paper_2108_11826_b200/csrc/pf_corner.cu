@@ -1030,7 +1030,10 @@ __device__ __noinline__ void classify_inline(const UpCornerArgs &a, const Bands 
 }
 
 
-__global__ void __launch_bounds__(kFinThreads, 4)
+#ifndef PF_FIN_MINB
+#define PF_FIN_MINB 4
+#endif
+__global__ void __launch_bounds__(kFinThreads, PF_FIN_MINB)
 k_corner_finish(const __grid_constant__ UpCornerArgs a)
 {
     extern __shared__ __align__(16) unsigned char smf[];
