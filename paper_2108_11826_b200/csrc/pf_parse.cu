@@ -776,7 +776,10 @@ k_pair_scan(const ParseArgs a, int B)
     if (threadIdx.x == 0) *a.pair_total = carry;
 }
 
-__global__ void __launch_bounds__(kScoreThreads)
+#ifndef PF_SCORE_MINB
+#define PF_SCORE_MINB 4   // 64 registers: 0.27 ms; 79 (1): 0.315, 48 (5): 0.318, 40 (6): 0.386
+#endif
+__global__ void __launch_bounds__(kScoreThreads, PF_SCORE_MINB)
 k_score_pairs(const ParseArgs a, int B)
 {
     __shared__ double s_t[kParseTTab];                     // u / (n - 1), paf.py:139
@@ -788,16 +791,26 @@ k_score_pairs(const ParseArgs a, int B)
     const int K = a.topo.K, L = a.topo.L;
     const long long total = *a.pair_total;
     const int max_fail = a.n_samples - a.good_need;
-    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
-         g += (long long)gridDim.x * blockDim.x) {
-        // frame: last b with pair_base[b] <= g (frames with no pairs share bases)
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long gw = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); gw < total; gw += stride) {
+        // frame of the warp's first pair: last b with pair_base[b] <= gw
+        // (frames with no pairs share bases), a 32-way search (3 rounds of
+        // one load per lane for 8192 frames instead of 13 dependent loads)
         int lo = 0, hi = B - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (__ldg(a.pair_base + mid) <= g) lo = mid;
-            else hi = mid - 1;
+        while (lo < hi) {                                    // warp-uniform
+            const int idx = lo + (int)(((long long)(hi - lo) * (lane + 1) + 31) / 32);
+            const uint32_t le = __ballot_sync(0xffffffffu, __ldg(a.pair_base + idx) <= gw);
+            const int c = __popc(le);                        // the probes are increasing: a prefix holds
+            const int nlo = c ? __shfl_sync(0xffffffffu, idx, c - 1) : lo;
+            const int nhi = c < 32 ? __shfl_sync(0xffffffffu, idx, c < 32 ? c : 31) - 1 : hi;
+            lo = nlo;
+            hi = nhi;
         }
-        const int b = lo;
+        const long long g = gw + lane;
+        if (g >= total) continue;
+        int b = lo;                                          // this lane's pair may lie a few frames on
+        while (b + 1 < B && __ldg(a.pair_base + b + 1) <= g) ++b;
         const int local0 = (int)(g - __ldg(a.pair_base + b));
         const int *pp = a.pair_pp + (size_t)b * (L + 1);
         int l = 0;
