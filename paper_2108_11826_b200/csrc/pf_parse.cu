@@ -54,6 +54,14 @@ __device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y)
 
 // Candidate storage: the first kCandSmem entries in shared memory, the rest
 // (crowded frames only) in this frame's global spill slab.
+// An accepted connection, parts resolved, for the serial assembly.
+struct ConnRec {
+    uint16_t pa, pb;
+    uint8_t a_part, b_part;
+    uint16_t pad;
+    double score;
+};
+
 struct CandStore {
     Cand *s;
     Cand *g;
@@ -176,7 +184,8 @@ k_parse_frames(const ParseArgs a)
     __shared__ int s_base[PF_MAX_KEYPOINTS + 1];
     __shared__ int s_pp[PF_MAX_LIMBS + 1];      // pair prefix per limb
     __shared__ int s_seg[PF_MAX_LIMBS + 1];     // candidate segment start per limb
-    __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base;
+    __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base, s_nacc;
+    __shared__ int s_wacc[(kParseThreads > kParseFinThreads ? kParseThreads : kParseFinThreads) / kWarp];
     __shared__ int s_lcnt[PF_MAX_LIMBS], s_lcur[PF_MAX_LIMBS];
     // split: fewer candidates in shared memory and the peak table read from
     // the k_parse_peaks slab, so more frames stay resident per SM
@@ -210,6 +219,8 @@ k_parse_frames(const ParseArgs a)
     int8_t *h_order = reinterpret_cast<int8_t *>(h_parts + a.cap_humans * K); // cap_humans*K
     int8_t *h_n = h_order + a.cap_humans * K;                                 // cap_humans
     int8_t *h_alive = h_n + a.cap_humans;                                     // cap_humans
+    ConnRec *conn = reinterpret_cast<ConnRec *>((reinterpret_cast<uintptr_t>(h_alive + a.cap_humans) + 15) &
+                                                ~uintptr_t(15));                 // CS accepted connections
     // split: the frame's candidates already sit in cand_g; entries past the
     // shared part are used (and sorted) in place there
     const CandStore cand{cand_s,
@@ -488,14 +499,58 @@ k_parse_frames(const ParseArgs a)
     }
 
     // ---- 6. assembly: exact sequential replay (paf.py:241-271) ----
-    if (tid == 0) {
-        int nh = 0, err = 0;
-        for (int e = 0; e < nc && !err; ++e) {
-            const Cand c = at(e);
+    // Usual frames: the accepted connections are first compacted in sorted
+    // order into self-contained records (parts resolved), so the serial
+    // replay reads one record per connection at an address that does not
+    // depend on the state it is updating.
+    if (fast) {
+        const int per = (nc + nthr - 1) / nthr;             // consecutive sorted positions per thread
+        const int e0 = tid * per;
+        int cnt = 0;
+        for (int j = 0; j < per; ++j)
+            cnt += (e0 + j < nc) && (cand_s[s_order[e0 + j]].ab & kAccepted) ? 1 : 0;
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        if (lane == kWarp - 1) s_wacc[warp] = incl;
+        __syncthreads();
+        int off = incl - cnt;
+        for (int w2 = 0; w2 < warp; ++w2) off += s_wacc[w2];
+        if (tid == nthr - 1) s_nacc = off + cnt;
+        for (int j = 0; j < per && e0 + j < nc; ++j) {
+            const Cand c = cand_s[s_order[e0 + j]];
             if (!(c.ab & kAccepted)) continue;
             const int l = int(c.lg >> 24);
-            const int a_part = s_la[l], b_part = s_lb[l];
-            const int pa = int((c.ab >> 16) & 0x7fff), pb = int(c.ab & 0xffff);
+            ConnRec r;
+            r.pa = uint16_t((c.ab >> 16) & 0x7fff);
+            r.pb = uint16_t(c.ab & 0xffff);
+            r.a_part = uint8_t(s_la[l]);
+            r.b_part = uint8_t(s_lb[l]);
+            r.score = c.score;
+            conn[off++] = r;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        int nh = 0, err = 0;
+        const int n_it = fast ? s_nacc : nc;
+        for (int e = 0; e < n_it && !err; ++e) {
+            int a_part, b_part, pa, pb;
+            double cscore;
+            if (fast) {
+                const ConnRec r = conn[e];
+                a_part = r.a_part; b_part = r.b_part; pa = r.pa; pb = r.pb; cscore = r.score;
+            } else {
+                const Cand c = cand[e];
+                if (!(c.ab & kAccepted)) continue;
+                const int l = int(c.lg >> 24);
+                a_part = s_la[l]; b_part = s_lb[l];
+                pa = int((c.ab >> 16) & 0x7fff); pb = int(c.ab & 0xffff);
+                cscore = c.score;
+            }
             const int ha = owner[pa], hb = owner[pb];
             if (ha < 0 && hb < 0) {                                  // paf.py:246-253
                 if (nh >= a.cap_humans) { err = 1; break; }
@@ -507,14 +562,14 @@ k_parse_frames(const ParseArgs a)
                 h_order[nh * K + 1] = int8_t(b_part);
                 h_n[nh] = 2;
                 h_mask[nh] = (1u << a_part) | (1u << b_part);
-                h_score[nh] = c.score;
+                h_score[nh] = cscore;
                 h_alive[nh] = 1;
                 owner[pa] = int16_t(nh);
                 owner[pb] = int16_t(nh);
                 ++nh;
             } else if (ha >= 0 && hb >= 0) {
                 if (ha == hb) {                                      // paf.py:255-256
-                    h_score[ha] = dadd(h_score[ha], c.score);
+                    h_score[ha] = dadd(h_score[ha], cscore);
                 } else if ((h_mask[ha] & h_mask[hb]) == 0u) {        // paf.py:257-262
                     const int nB = h_n[hb];
                     int nA = h_n[ha];
@@ -527,7 +582,7 @@ k_parse_frames(const ParseArgs a)
                     }
                     h_n[ha] = int8_t(nA);
                     h_mask[ha] |= h_mask[hb];
-                    h_score[ha] = dadd(h_score[ha], dadd(h_score[hb], c.score));
+                    h_score[ha] = dadd(h_score[ha], dadd(h_score[hb], cscore));
                     h_alive[hb] = 0;
                 }                                                    // else paf.py:263
             } else {                                                 // paf.py:264-271
@@ -543,7 +598,7 @@ k_parse_frames(const ParseArgs a)
                     h_order[hidx * K + nn] = int8_t(part);
                     h_n[hidx] = int8_t(nn + 1);
                     h_mask[hidx] = m | (1u << part);
-                    h_score[hidx] = dadd(hs, c.score);
+                    h_score[hidx] = dadd(hs, cscore);
                     owner[pid] = int16_t(hidx);
                 }
             }
@@ -851,6 +906,8 @@ size_t parse_smem_bytes(int cap_frame, int cap_part, int cap_cands, int cap_huma
     s += (size_t)cap_frame * sizeof(int16_t);
     s += (size_t)cap_humans * K * (sizeof(int16_t) + sizeof(int8_t));
     s += (size_t)cap_humans * 2;
+    s = (s + 15) & ~size_t(15);
+    s += (size_t)(split ? kCandSmemSplit : kCandSmem) * sizeof(ConnRec);
     return (s + 15) & ~size_t(15);
 }
 
