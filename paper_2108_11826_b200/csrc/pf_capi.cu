@@ -1190,7 +1190,7 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     if (rc) return rc;
     int chunk = chunk_for(ctx, p, grid_h, grid_w);
 #ifndef PF_HOST_CHUNK
-#define PF_HOST_CHUNK 256
+#define PF_HOST_CHUNK 128   // e2e (8192 frames): 131.5-132k at 128-192, 127.6k at 256, 120.6k at 64, 112k at 512
 #endif
     if (chunk > PF_HOST_CHUNK) chunk = PF_HOST_CHUNK;   // copy/compute overlap granularity
     // PF_OPT_PAF_ZERO_COPY: a pinned (mapped) host PAF is read in place by
