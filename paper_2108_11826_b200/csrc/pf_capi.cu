@@ -120,6 +120,11 @@ cudaError_t host_alloc(T **p, size_t n)
 
 }  // namespace
 
+#ifndef PF_HOST_SLOTS
+#define PF_HOST_SLOTS 2   // 3 measured the same (132.2k vs 131.7k e2e)
+#endif
+constexpr int kHostSlots = PF_HOST_SLOTS;   // device input slots of pf_parse_host (copy / compute overlap)
+
 struct pf_ctx {
     int device = 0;
     int sms = 148;
@@ -180,9 +185,9 @@ struct pf_ctx {
     size_t full_elems = 0;
 
     // host-path staging (double buffered)
-    float *d_in[2] = {nullptr, nullptr};
+    float *d_in[kHostSlots] = {};
     size_t in_elems = 0;
-    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copied[kHostSlots] = {}, ev_free[kHostSlots] = {};
 
     // debug slabs
     int *d_dbg_np = nullptr, *d_dbg_nc = nullptr, *d_dbg_ci = nullptr;
@@ -889,7 +894,7 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
         cu(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream"))
         return bail(PF_ERR_CUDA);
     ctx->stream = ctx->own_stream;
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kHostSlots; ++k) {
         if (cu(cudaEventCreateWithFlags(&ctx->ev_copied[k], cudaEventDisableTiming), "event") ||
             cu(cudaEventCreateWithFlags(&ctx->ev_free[k], cudaEventDisableTiming), "event"))
             return bail(PF_ERR_CUDA);
@@ -921,12 +926,13 @@ void pf_destroy(pf_ctx *ctx)
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     void *dev[] = {ctx->d_counts, ctx->d_peaks, ctx->d_spill, ctx->d_frame_first, ctx->d_frame_count,
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
-                   ctx->d_status, ctx->d_full, ctx->d_tmp, ctx->d_in[0], ctx->d_in[1],
+                   ctx->d_status, ctx->d_full, ctx->d_tmp,
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
                    ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_pk_cell, ctx->d_pk_score,
                    ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n,
                    ctx->d_owner};
     for (void *p : dev) cudaFree(p);
+    for (float *p : ctx->d_in) cudaFree(p);
     void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
                     ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};
     for (void *p : host) cudaFreeHost(p);
@@ -939,7 +945,7 @@ void pf_destroy(pf_ctx *ctx)
     }
     for (auto &p : ctx->pending) { ctx->ev_pool.push_back(p.second.first); ctx->ev_pool.push_back(p.second.second); }
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kHostSlots; ++k) {
         if (ctx->ev_copied[k]) cudaEventDestroy(ctx->ev_copied[k]);
         if (ctx->ev_free[k]) cudaEventDestroy(ctx->ev_free[k]);
     }
@@ -1217,10 +1223,11 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     const size_t conf_frame = (size_t)(K + 1) * plane, paf_frame = (size_t)2 * L * plane;
     const size_t slot = (size_t)chunk * (conf_frame + paf_frame);
     if (slot > ctx->in_elems) {
-        cudaFree(ctx->d_in[0]);
-        cudaFree(ctx->d_in[1]);
-        CU(dev_alloc(&ctx->d_in[0], slot));
-        CU(dev_alloc(&ctx->d_in[1], slot));
+        for (float *&p : ctx->d_in) {
+            cudaFree(p);
+            p = nullptr;
+        }
+        for (float *&p : ctx->d_in) CU(dev_alloc(&p, slot));
         ctx->in_elems = slot;
     }
     // a PAF read in place over PCIe: the one-kernel parse keeps each frame's
@@ -1233,11 +1240,11 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
         ~Restore() { c->parse_split = v; }
     } restore{ctx, saved_split};
     // slots start free
-    for (int k = 0; k < 2; ++k) CU(cudaEventRecord(ctx->ev_free[k], ctx->stream));
+    for (int k = 0; k < kHostSlots; ++k) CU(cudaEventRecord(ctx->ev_free[k], ctx->stream));
     int ci = 0;
     for (int f0 = 0; f0 < batch; f0 += chunk, ++ci) {
         const int n = batch - f0 < chunk ? batch - f0 : chunk;
-        const int sl = ci & 1;
+        const int sl = ci % kHostSlots;
         float *dconf = ctx->d_in[sl];
         float *dpaf = dconf + (size_t)n * conf_frame;
         CU(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_free[sl], 0));
