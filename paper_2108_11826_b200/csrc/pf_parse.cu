@@ -69,6 +69,59 @@ struct CandStore {
     __device__ __forceinline__ Cand &operator[](int i) const { return i < ns ? s[i] : g[i - ns]; }
 };
 
+// Crowded frames (candidates past the shared-memory part): the accepted
+// connections, as ConnRec records, compacted in place over the sorted
+// candidates in windows (every read of a window happens before its writes,
+// which never pass the window's end).  Kept out of line so the usual path's
+// register allocation is not disturbed.  Returns the number of records.
+__device__ __noinline__ int compact_crowded(const CandStore cand, int nc, const int8_t *s_la, const int8_t *s_lb,
+                                            int *s_wacc)
+{
+    constexpr int kWin = 4;
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, n_warps = nthr >> 5;
+    int kbase = 0;                                           // block-uniform
+    for (int w0 = 0; w0 < nc; w0 += nthr * kWin) {
+        Cand v[kWin];
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < kWin; ++j) {
+            const int e = w0 + tid * kWin + j;
+            if (e < nc) v[j] = cand[e];
+            else v[j].ab = 0u;
+            cnt += (v[j].ab & kAccepted) ? 1 : 0;
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const int x = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += x;
+        }
+        if (lane == kWarp - 1) s_wacc[warp] = incl;
+        __syncthreads();
+        int off = kbase + incl - cnt, tot = 0;
+        for (int w2 = 0; w2 < n_warps; ++w2) {
+            if (w2 < warp) off += s_wacc[w2];
+            tot += s_wacc[w2];
+        }
+#pragma unroll
+        for (int j = 0; j < kWin; ++j) {
+            if (!(v[j].ab & kAccepted)) continue;
+            const int l = int(v[j].lg >> 24);
+            ConnRec r;
+            r.pa = uint16_t((v[j].ab >> 16) & 0x7fff);
+            r.pb = uint16_t(v[j].ab & 0xffff);
+            r.a_part = uint8_t(s_la[l]);
+            r.b_part = uint8_t(s_lb[l]);
+            r.pad = 0;
+            r.score = v[j].score;
+            *reinterpret_cast<ConnRec *>(&cand[off++]) = r;
+        }
+        kbase += tot;
+        __syncthreads();
+    }
+    return kbase;
+}
+
 // PAF value pair at parse-grid cell (ci, cj): the feature grid itself
 // (up == 1), or the x`up` bilinear value of operators.py:102-107 re-derived
 // from the low-res PAF with one packed axis record per axis.  Loads (fetch)
@@ -211,10 +264,9 @@ k_parse_frames(const ParseArgs a)
     uint32_t *h_mask = SPLIT ? reinterpret_cast<uint32_t *>(h_score + a.cap_humans)
                              : reinterpret_cast<uint32_t *>(p_score + a.cap_frame);    // cap_humans
     int *h_pos = reinterpret_cast<int *>(h_mask + a.cap_humans);             // cap_humans
-    const int bm_words = (a.cap_frame + 31) / 32;
     const int pm_words = (a.cap_part + 31) / 32;
     uint32_t *used = reinterpret_cast<uint32_t *>(h_pos + a.cap_humans);     // used_words(), see parse_smem_bytes
-    int16_t *owner = reinterpret_cast<int16_t *>(used + max(n_warps * 2 * bm_words, L * 2 * pm_words));  // cap_frame
+    int16_t *owner = reinterpret_cast<int16_t *>(used + L * 2 * pm_words);  // cap_frame
     int16_t *h_parts = owner + a.cap_frame;                                   // cap_humans*K
     int8_t *h_order = reinterpret_cast<int8_t *>(h_parts + a.cap_humans * K); // cap_humans*K
     int8_t *h_n = h_order + a.cap_humans * K;                                 // cap_humans
@@ -440,10 +492,12 @@ k_parse_frames(const ParseArgs a)
             for (int k2 = s0; k2 < s1; ++k2) rank += cand_less(cand_s[s_bucket[k2]], c);
             s_order[s0 + rank] = uint16_t(i);
         }
-        for (int q = tid; q < L * 2 * pm_words; q += nthr) used[q] = 0u;
-        __syncthreads();
-        // ... then every limb's greedy walk at once, thread per limb (used
-        // bitmaps over the peak's index within its part)
+    }
+    // every limb's greedy walk at once, thread per limb (used bitmaps over
+    // the peak's index within its part)
+    for (int q = tid; q < L * 2 * pm_words; q += nthr) used[q] = 0u;
+    __syncthreads();
+    if (fast) {
         for (int l = tid; l < L; l += nthr) {
             uint32_t *used_a = used + l * 2 * pm_words, *used_b = used_a + pm_words;
             const int ba = s_base[s_la[l]], bb = s_base[s_lb[l]];
@@ -458,27 +512,20 @@ k_parse_frames(const ParseArgs a)
                 c.ab = ab | kAccepted;
             }
         }
-    } else {
-        uint32_t *used_a = used + warp * 2 * bm_words;
-        uint32_t *used_b = used_a + bm_words;
-        for (int l = warp; l < L; l += n_warps) {
-            const int s0 = s_seg[l], s1 = s_seg[l + 1];
-            if (s0 == s1) continue;                           // warp-uniform
-            for (int q = lane; q < bm_words; q += kWarp) { used_a[q] = 0u; used_b[q] = 0u; }
-            __syncwarp();
-            if (lane == 0) {
-                for (int e = s0; e < s1; ++e) {
-                    Cand &c = cand[e];
-                    const uint32_t ab = c.ab;
-                    const int ia = int((ab >> 16) & 0x7fff), ib = int(ab & 0xffff);
-                    if ((used_a[ia >> 5] >> (ia & 31)) & 1u) continue;
-                    if ((used_b[ib >> 5] >> (ib & 31)) & 1u) continue;
-                    used_a[ia >> 5] |= 1u << (ia & 31);
-                    used_b[ib >> 5] |= 1u << (ib & 31);
-                    c.ab = ab | kAccepted;
-                }
+    } else {                                                 // crowded: the bitonic-sorted store
+        for (int l = tid; l < L; l += nthr) {
+            uint32_t *used_a = used + l * 2 * pm_words, *used_b = used_a + pm_words;
+            const int ba = s_base[s_la[l]], bb = s_base[s_lb[l]];
+            for (int e = s_seg[l], e1 = s_seg[l + 1]; e < e1; ++e) {
+                Cand &c = cand[e];
+                const uint32_t ab = c.ab;
+                const int ia = int((ab >> 16) & 0x7fff) - ba, ib = int(ab & 0xffff) - bb;
+                if ((used_a[ia >> 5] >> (ia & 31)) & 1u) continue;
+                if ((used_b[ib >> 5] >> (ib & 31)) & 1u) continue;
+                used_a[ia >> 5] |= 1u << (ia & 31);
+                used_b[ib >> 5] |= 1u << (ib & 31);
+                c.ab = ab | kAccepted;
             }
-            __syncwarp();
         }
     }
     __syncthreads();
@@ -533,27 +580,22 @@ k_parse_frames(const ParseArgs a)
             conn[off++] = r;
         }
         __syncthreads();
+    } else {
+        const int kb = compact_crowded(cand, nc, s_la, s_lb, s_wacc);
+        if (tid == 0) s_nacc = kb;
+        __syncthreads();
     }
     if (tid == 0) {
         int nh = 0, err = 0;
-        const int n_it = fast ? s_nacc : nc;
-        for (int e = 0; e < n_it && !err; ++e) {
-            int a_part, b_part, pa, pb;
-            double cscore;
-            if (fast) {
-                const ConnRec r = conn[e];
-                a_part = r.a_part; b_part = r.b_part; pa = r.pa; pb = r.pb; cscore = r.score;
-            } else {
-                const Cand c = cand[e];
-                if (!(c.ab & kAccepted)) continue;
-                const int l = int(c.lg >> 24);
-                a_part = s_la[l]; b_part = s_lb[l];
-                pa = int((c.ab >> 16) & 0x7fff); pb = int(c.ab & 0xffff);
-                cscore = c.score;
-            }
+        const int n_it = s_nacc;
+        // one replay step (the loop is specialised per record source so the
+        // usual path keeps its shared-memory loads)
+        auto step = [&](const ConnRec r) {
+            const int a_part = r.a_part, b_part = r.b_part, pa = r.pa, pb = r.pb;
+            const double cscore = r.score;
             const int ha = owner[pa], hb = owner[pb];
             if (ha < 0 && hb < 0) {                                  // paf.py:246-253
-                if (nh >= a.cap_humans) { err = 1; break; }
+                if (nh >= a.cap_humans) { err = 1; return; }
                 int16_t *parts = h_parts + nh * K;
                 for (int k = 0; k < K; ++k) parts[k] = -1;
                 parts[a_part] = int16_t(pa);
@@ -602,6 +644,11 @@ k_parse_frames(const ParseArgs a)
                     owner[pid] = int16_t(hidx);
                 }
             }
+        };
+        if (fast) {
+            for (int e = 0; e < n_it && !err; ++e) step(conn[e]);
+        } else {
+            for (int e = 0; e < n_it && !err; ++e) step(*reinterpret_cast<const ConnRec *>(&cand[e]));
         }
         s_nh = nh;
         s_err = err;
@@ -897,12 +944,12 @@ size_t parse_smem_bytes(int cap_frame, int cap_part, int cap_cands, int cap_huma
                         bool split)
 {
     (void)cap_cands;
-    const int bm_words = (cap_frame + 31) / 32, pm_words = (cap_part + 31) / 32;
+    const int pm_words = (cap_part + 31) / 32;
     size_t s = (size_t)(split ? kCandSmemSplit : kCandSmem) * sizeof(Cand);
     s += (size_t)cap_humans * sizeof(double);
     if (!split) s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
     s += (size_t)cap_humans * (sizeof(uint32_t) + sizeof(int));
-    s += (size_t)std::max(n_warps * 2 * bm_words, L * 2 * pm_words) * sizeof(uint32_t);
+    s += (size_t)L * 2 * pm_words * sizeof(uint32_t);
     s += (size_t)cap_frame * sizeof(int16_t);
     s += (size_t)cap_humans * K * (sizeof(int16_t) + sizeof(int8_t));
     s += (size_t)cap_humans * 2;
