@@ -1100,7 +1100,10 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
 // threads, candidates collected in shared memory and tested lane by lane.
 constexpr int kCrowdCands = 2048;
 
-__global__ void __launch_bounds__(kFinThreads, 3)
+#ifndef PF_CROWD_MINB
+#define PF_CROWD_MINB 6   // C3 Mode U: 1.27 ms (3 CTAs/SM), 1.14 (4), 1.08 (6), 1.07 (8, more spills)
+#endif
+__global__ void __launch_bounds__(kFinThreads, PF_CROWD_MINB)
 k_corner_crowded(const __grid_constant__ UpCornerArgs a)
 {
     extern __shared__ __align__(16) unsigned char smf[];
@@ -1199,7 +1202,8 @@ cudaError_t launch_corner_crowded(const UpCornerArgs &a, cudaStream_t s)
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
     const size_t smem_c = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) + kCrowdCands * sizeof(uint32_t);
-    e = launch_pdl(k_corner_crowded, dim3((unsigned)std::min<long long>(P, (long long)sms * 3)), dim3(kFinThreads),
+    e = launch_pdl(k_corner_crowded, dim3((unsigned)std::min<long long>(P, (long long)sms * PF_CROWD_MINB)),
+                   dim3(kFinThreads),
                    smem_c, s, a);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
