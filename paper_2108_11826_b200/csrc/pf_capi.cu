@@ -521,7 +521,11 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
                             ctx->d_counts, ctx->d_peaks, s));
     } else if (!blur && half == 1 && !ctx->materialise && !ctx->generic_fused && ctx->win_variant == 4 &&
                rows->canonical && cols->canonical && h + 1 <= 256 && w + 1 <= 256 &&
-               nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) <= 100 * 1024) {
+               (nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) <= 100 * 1024 ||
+                (ctx->corner_split != 0 && nms_up_scan_smem(h, w, 1) + 2048 <= (size_t)ctx->max_smem))) {
+        // maps too large for the one-kernel form's shared-memory budget
+        // (e.g. 135x240) take the split kernels at any batch size
+        const bool big = nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) > 100 * 1024;
         UpCornerArgs a{};
         a.conf = conf; a.B = n; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
         a.thr = thr; a.cap = ctx->caps.max_peaks_per_part;
@@ -537,7 +541,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             CU(dev_alloc(&ctx->d_corner_spill, nms_up_corner_spill_entries(ctx->sms * 16)));
         a.cand_spill = ctx->d_corner_spill;
         // split kernels pay off on batches; a few frames take the one-kernel path (fewer launches)
-        const bool csplit = ctx->corner_split == 2 || (ctx->corner_split == 1 && n >= kSplitMinFrames);
+        const bool csplit = ctx->corner_split == 2 || (ctx->corner_split == 1 && (n >= kSplitMinFrames || big));
         if (csplit) {
             const size_t planes = (size_t)n * K;
             if (planes > ctx->surv_planes) {

@@ -114,6 +114,7 @@ cudaError_t launch_nms_up_scan(const UpCornerArgs &a, cudaStream_t s);
 size_t corner_surv_entries_per_plane();
 size_t nms_up_corner_spill_entries(int max_ctas);
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
+size_t nms_up_scan_smem(int h, int w, int nst);
 #ifndef PF_CORNER_STAGES
 #define PF_CORNER_STAGES 1
 #endif

@@ -424,3 +424,28 @@ def test_split_paths_agree(topo, up):
     for f in (0, 6):
         want = oracle_run(conf[f], paf[f], topo, params)
         assert out[0][2][f] == record_of(want.humans, topo, f)
+
+
+def test_large_maps_take_the_split_kernels(eng, topo):
+    """135x240 maps (1080x1920 input): too large for the one-kernel corner
+    form, so even a 2-frame batch runs k_nms_up_scan -> k_corner_finish; the
+    peaks and records equal the oracle's and the materialised path's."""
+    scenes = [pf.procedural_scene(31, s, 1920, 1080, SP) for s in range(2)]
+    conf, paf = render(scenes, topo)
+    assert conf.shape[2:] == (135, 240)
+    params = pf.ParserParams(upsample=8)
+    e = pf.PafParser(topo, debug=True)
+    e.set_timing(True)
+    e.kernel_times(reset=True)
+    got = e.parse_arrays(conf, paf, 8, params)
+    kt = e.kernel_times(reset=True)
+    assert "k_nms_up_scan" in kt and "k_corner_finish" in kt, kt
+    split = [pf.pose_record(f, got.poses(f), topo) for f in range(len(scenes))]
+    peaks = [e.peaks(f) for f in range(len(scenes))]
+    e.ctx.set_option(pf._native.PF_OPT_MATERIALISE, 1)
+    got = e.parse_arrays(conf, paf, 8, params)
+    assert [pf.pose_record(f, got.poses(f), topo) for f in range(len(scenes))] == split
+    assert [e.peaks(f) for f in range(len(scenes))] == peaks
+    e.close()
+    want = oracle_run(conf[0], paf[0], topo, params)
+    assert split[0] == record_of(want.humans, topo, 0)
