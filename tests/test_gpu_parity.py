@@ -279,7 +279,7 @@ def test_pinned_paf_read_in_place(topo, up):
     oracle's, on procedural and crowded frames across several host chunks."""
     scenes = [pf.procedural_scene(12, s, 656, 368, SP) for s in range(5)] + [pf.crowd_scene(4, 0)]
     conf, paf = render(scenes, topo)
-    reps = 50                                          # 300 frames: host chunks of 128, 128 and 44 frames
+    reps = 46                                          # 276 frames: host chunks of 128, 128 and 20 frames
                                                        # (the last below the split threshold: one-kernel NMS)
     pc = pf._native.PinnedArray((len(scenes) * reps,) + conf.shape[1:])
     pp = pf._native.PinnedArray((len(scenes) * reps,) + paf.shape[1:])
