@@ -162,10 +162,11 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_WIN_VARIANT 5     /* Mode U 3x3 kernel: 4 corner-pruned (default), 3/2/1 strip kernels */
 #define PF_OPT_NO_CHAIN 6        /* corner kernel: disable the chain pre-filter (A/B parity checks) */
 #define PF_OPT_CORNER_SPLIT 9    /* Mode U 3x3: survivors classified by a second kernel;
-                                    0 off, 1 auto (batches of >= 64 frames, default), 2 always */
+                                    0 off, 1 auto (batches of >= 32 frames, or planes too large
+                                    for the one-kernel form; default), 2 always */
 #define PF_OPT_CONF_ZERO_COPY 11 /* pf_parse_host: NMS kernels read a pinned host conf in place (default 0) */
 #define PF_OPT_PARSE_SPLIT 10    /* line integral over all frames' pairs in its own kernel;
-                                    0 off, 1 auto (batches of >= 64 frames, default), 2 always */
+                                    0 off, 1 auto (batches of >= 32 frames, default), 2 always */
 #define PF_OPT_PAF_ZERO_COPY 8   /* pf_parse_host (default 1): a pinned host PAF is read in place by the
                                     parse kernel, so only the sampled cells cross PCIe; 0: copy it whole */
 int pf_set_option(pf_ctx *ctx, int option, int value);
