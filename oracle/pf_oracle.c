@@ -217,7 +217,7 @@ void orc_score_limb(const float *paf_x, const float *paf_y, int h, int w,
     (void)h;
     if (ai == bi && aj == bj) { *score = 0.0; *good = 0.0; return; }
     int di = bi - ai, dj = bj - aj;
-    double norm = sqrt((double)(di * di + dj * dj));
+    double norm = sqrt((double)((long long)di * di + (long long)dj * dj));
     double vx = (double)dj / norm, vy = (double)di / norm;
     double total = 0.0;
     int ngood = 0;

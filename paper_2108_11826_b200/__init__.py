@@ -44,14 +44,7 @@ from .pipeline_ops import (
 from .overlay import OverlayStyle, part_color, visualize, visualize_batch
 from .sharding import MultiDeviceParser, ShardedResult
 from .skeleton import load_topology, parse_topology
-from .synth import (
-    GroundTruthHuman,
-    GroundTruthScene,
-    SynthParams,
-    crowd_scene,
-    procedural_scene,
-    render_feature_maps,
-)
+from .producer import render_maps_gpu
 
 __version__ = "0.1.0"
 

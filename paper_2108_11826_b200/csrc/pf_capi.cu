@@ -525,7 +525,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     } else if (!blur && half == 1 && !ctx->materialise && !ctx->generic_fused && ctx->win_variant == 4 &&
                rows->canonical && cols->canonical && h + 1 <= 256 && w + 1 <= 256 &&
                (nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) <= 100 * 1024 ||
-                (ctx->corner_split != 0 && nms_up_scan_smem(h, w, 1) + 2048 <= (size_t)ctx->max_smem))) {
+                (ctx->corner_split != 0 && nms_up_scan_launch_smem(h, w) + 2048 <= (size_t)ctx->max_smem))) {
         // maps too large for the one-kernel form's shared-memory budget
         // (e.g. 135x240) take the split kernels at any batch size
         const bool big = nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) > 100 * 1024;

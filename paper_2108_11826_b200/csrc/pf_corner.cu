@@ -954,6 +954,11 @@ size_t nms_up_scan_smem(int h, int w, int nst)
     return scan_layout(h, w, nst).total;
 }
 
+size_t nms_up_scan_launch_smem(int h, int w)
+{
+    return nms_up_scan_smem(h, w, PF_SCAN_STAGES);   // what launch_nms_up_scan requests
+}
+
 cudaError_t launch_nms_up_scan(const UpCornerArgs &a_in, cudaStream_t s)
 {
     UpCornerArgs a = a_in;

@@ -115,6 +115,7 @@ size_t corner_surv_entries_per_plane();
 size_t nms_up_corner_spill_entries(int max_ctas);
 size_t nms_up_corner_smem(int h, int w, int nbr, int nbc, int nst);
 size_t nms_up_scan_smem(int h, int w, int nst);
+size_t nms_up_scan_launch_smem(int h, int w);   // the shared memory launch_nms_up_scan requests
 #ifndef PF_CORNER_STAGES
 #define PF_CORNER_STAGES 1
 #endif

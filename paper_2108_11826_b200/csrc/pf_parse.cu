@@ -178,7 +178,7 @@ __device__ __forceinline__ bool score_pair(const ParseArgs &a, const float *__re
     const int ai = int(ca >> 16), aj = int(ca & 0xffff);
     const int di = int(cbp >> 16) - ai, dj = int(cbp & 0xffff) - aj;
     if ((di | dj) == 0) return false;                     // coincident cells score (0, 0): never gated
-    const double norm = __dsqrt_rn((double)(di * di + dj * dj));
+    const double norm = __dsqrt_rn((double)((long long)di * di + (long long)dj * dj));   // exact (Python ints)
     const double vx = __ddiv_rn((double)dj, norm);
     const double vy = __ddiv_rn((double)di, norm);
     const float *chx = paf_f + (size_t)a.topo.cx[l] * a.h * a.w;
@@ -787,6 +787,7 @@ k_parse_peaks(const ParseArgs a, int B)
     {   // exclusive prefix: s_base[k] = incl of lane k - 1 (every lane takes part in the shuffle)
         const int prev = __shfl_sync(0xffffffffu, incl, min(max(lane - 1, 0), 31));
         if (lane <= K) s_base[warp][lane] = lane == 0 ? 0 : prev;
+        if (lane == 0 && K == kWarp) s_base[warp][K] = P;   // K = 32: the total has no lane of its own
     }
     __syncwarp();
     if (lane == 0) {

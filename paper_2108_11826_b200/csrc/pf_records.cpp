@@ -70,12 +70,28 @@ void put_float(std::string &o, double v)
     }
 }
 
-// json.dumps string escaping (ensure_ascii=True) for the part names.
+// json.dumps string escaping (ensure_ascii=True) for the part names: the
+// UTF-8 bytes are decoded to code points; every one outside ' '..'~' becomes
+// \uXXXX, with a surrogate pair above U+FFFF (CPython's py_encode_basestring_ascii).
+void put_u16(std::string &o, unsigned v)
+{
+    char u[8];
+    std::snprintf(u, sizeof(u), "\\u%04x", v);
+    o += u;
+}
+
 void put_string(std::string &o, const char *s)
 {
     o += '"';
-    for (const unsigned char *c = reinterpret_cast<const unsigned char *>(s); *c; ++c) {
-        switch (*c) {
+    const unsigned char *c = reinterpret_cast<const unsigned char *>(s);
+    while (*c) {
+        unsigned cp = *c++;
+        if (cp >= 0x80) {   // multi-byte sequence (names come from Python str.encode(): valid UTF-8)
+            const int extra = cp >= 0xf0 ? 3 : cp >= 0xe0 ? 2 : 1;
+            cp &= extra == 3 ? 0x07u : extra == 2 ? 0x0fu : 0x1fu;
+            for (int k = 0; k < extra && (*c & 0xc0) == 0x80; ++k) cp = (cp << 6) | (*c++ & 0x3fu);
+        }
+        switch (cp) {
         case '"': o += "\\\""; break;
         case '\\': o += "\\\\"; break;
         case '\n': o += "\\n"; break;
@@ -84,12 +100,16 @@ void put_string(std::string &o, const char *s)
         case '\b': o += "\\b"; break;
         case '\f': o += "\\f"; break;
         default:
-            if (*c < 0x20 || *c >= 0x7f) {
-                char u[8];
-                std::snprintf(u, sizeof(u), "\\u%04x", *c);
-                o += u;
+            if (cp < 0x20 || cp >= 0x7f) {
+                if (cp > 0xffff) {
+                    cp -= 0x10000;
+                    put_u16(o, 0xd800 | (cp >> 10));
+                    put_u16(o, 0xdc00 | (cp & 0x3ff));
+                } else {
+                    put_u16(o, cp);
+                }
             } else {
-                o += static_cast<char>(*c);
+                o += static_cast<char>(cp);
             }
         }
     }

@@ -137,6 +137,10 @@ class PafParser:
         self.topo = topo
         self.ctx.set_topology(topo)
         self.device = device
+        # the maps of the last parse_tensors call (including .contiguous()
+        # temporaries): pf_get_results may replay the call from them when an
+        # automatic capacity grows, so they stay alive until results() returns
+        self._inflight = None
         if debug:
             self.set_debug(True)
 
@@ -192,7 +196,11 @@ class PafParser:
     def parse_device(self, conf_ptr: int, paf_ptr: int, batch: int, grid_h: int, grid_w: int,
                      stride: int, params: ParserParams) -> None:
         """Asynchronous parse of device-resident maps (raw CUDA pointers, the
-        FeatureMaps layout batched); collect with ``results()``."""
+        FeatureMaps layout batched); collect with ``results()``.  The memory
+        behind the pointers must stay valid until ``results()`` returns (a
+        capacity grow replays the call from it); ``parse_tensors`` keeps its
+        tensors alive itself."""
+        self._inflight = None
         p = _params_of(params).to_native()
         self.ctx.check(self.ctx.lib.pf_parse_device(
             self.ctx.handle, ctypes.c_void_p(conf_ptr), ctypes.c_void_p(paf_ptr), int(batch),
@@ -215,11 +223,15 @@ class PafParser:
         self.set_stream(torch.cuda.current_stream(conf.device).cuda_stream)
         b, _, h, w = conf.shape
         self.parse_device(conf.data_ptr(), paf.data_ptr(), b, h, w, stride, params)
+        self._inflight = (conf, paf)
 
     def results(self) -> BatchResult:
         res = _native.PfResults()
-        self.ctx.check(self.ctx.lib.pf_get_results(self.ctx.handle, ctypes.byref(res)))
-        return BatchResult(res)
+        try:
+            self.ctx.check(self.ctx.lib.pf_get_results(self.ctx.handle, ctypes.byref(res)))
+            return BatchResult(res)
+        finally:
+            self._inflight = None
 
     def peaks(self, frame: int):
         """Debug capture: [(part, row, col, score, id)] in id order."""

@@ -9,9 +9,9 @@ and the plugin types of ``poseflow/dataflow.py:37-170``).
 * ``make_postprocess(topo, params)`` [operators.py:147-157] —
   ``(Frame, FeatureMaps) -> (Frame, [HumanPose])`` through the GPU parser.
 * ``make_batched_postprocess`` — the batched GPU stage of SURVEY.md §8(f)2:
-  a ``runner`` that drains whatever is queued (the ``make_batching_operator``
-  pattern, scheduler.py:108-136) into one ``parse_batch`` call, emitting in
-  ascending ``seq_id``.
+  the reference batching operator (``accumulate_batch`` with ``linger_us``,
+  ``batch_hist``, ``ctx.timed``, ``split_batch_results``; scheduler.py:55-131)
+  around one ``parse_batch`` call per drained batch.
 * ``preprocess_batch`` — u8 HWC frames -> f32 CHW on the device.
 * ``bilinear_resize`` / ``hwc_to_chw`` [operators.py:79-111] and
   ``pose_record`` [operators.py:293-310].
@@ -177,64 +177,114 @@ def _is_packet(item) -> bool:
     return hasattr(item, "seq_id") and hasattr(item, "payload")
 
 
-def make_batched_postprocess(topo: SkeletonTopology, params, batch_max: int = 256,
-                             device: int = 0, devices: Optional[Sequence[int]] = None) -> OperatorSpec:
-    """Batched GPU post-processing stage.
+def _is_end(item) -> bool:
+    # the reference's channel sentinels (dataflow.py:26-37) by name; this
+    # package never imports the reference
+    return repr(item) == "END_OF_STREAM"
 
-    ``runner(ctx, in_ch, out_ch)`` follows the reference batching operator
-    (scheduler.py:108-136): block for one item, drain what is queued up to
-    ``batch_max`` without waiting, parse the batch in one GPU call, emit in
-    ascending ``seq_id``.  ``fn`` is the per-item form for sequential runs.
-    With ``devices`` (more than one entry) a drained batch is cut into
-    contiguous shards parsed concurrently on those GPUs (``MultiDeviceParser``)
-    and merged back in ``seq_id`` order.  Outputs are identical for every
-    batch composition and device count (parse is pure).
+
+def accumulate_batch(ctx, in_ch, batch_max: int, linger_us: int = 0):
+    """The reference batch former (scheduler.py:55-86): block for the first
+    item, then drain without waiting up to ``batch_max`` — or keep waiting
+    inside the ``linger_us`` window.  Returns (batch, saw_end)."""
+    import time
+
+    first = ctx.recv(in_ch)
+    if _is_end(first):
+        return [], True
+    batch = [first]
+    deadline = time.monotonic() + linger_us / 1e6 if linger_us else None
+    while len(batch) < batch_max:
+        item = ctx.try_recv(in_ch)
+        if not _is_packet(item) and not _is_end(item):          # NO_ITEM
+            if deadline is None:
+                break
+            remaining = deadline - time.monotonic()
+            if remaining <= 0:
+                break
+            item = ctx.recv_timeout(in_ch, remaining)
+            if not _is_packet(item) and not _is_end(item):
+                break
+        if _is_end(item):
+            return batch, True
+        batch.append(item)
+    return batch, False
+
+
+def split_batch_results(outputs: Sequence[Any], batch: Sequence[Packet]) -> List[Packet]:
+    """Re-wrap one output per packet, checking count and ascending seq order
+    exactly as the reference does (scheduler.py:89-105)."""
+    from .errors import BackendError
+
+    if len(outputs) != len(batch):
+        raise BackendError(f"backend returned {len(outputs)} outputs for batch of {len(batch)} "
+                           f"(seq_ids {[p.seq_id for p in batch]})")
+    for prev, cur in zip(batch, batch[1:]):
+        if cur.seq_id <= prev.seq_id:
+            raise BackendError(f"batch seq_ids not ascending: {prev.seq_id} then {cur.seq_id}")
+    return [Packet(seq_id=pkt.seq_id, ingest_ns=pkt.ingest_ns, payload=out) for pkt, out in zip(batch, outputs)]
+
+
+def make_batched_postprocess(topo: SkeletonTopology, params, batch_max: int = 256, linger_us: int = 0,
+                             device: int = 0, devices: Optional[Sequence[int]] = None,
+                             name: str = "postprocess") -> OperatorSpec:
+    """Batched GPU post-processing stage (SURVEY.md §8(f) 2).
+
+    ``runner(ctx, in_ch, out_ch)`` is the reference batching operator
+    (``make_batching_operator``, scheduler.py:108-131) with the GPU parse as
+    its backend call: ``accumulate_batch`` (block for one item, drain up to
+    ``batch_max``, optional ``linger_us`` window), ``ctx.batch_hist[len] += 1``,
+    the parse of the whole batch under ``ctx.timed`` (so the reference's
+    ``PipelineStats`` charge it as busy time), ``split_batch_results`` (count
+    and ascending-seq checks), then one packet per frame downstream.
+    ``fn`` is the per-item form for sequential runs.  With ``devices`` (more
+    than one entry) a batch is cut into contiguous shards parsed concurrently
+    on those GPUs (``MultiDeviceParser``) and merged back in frame order.
+    Outputs are identical for every batch composition and device count
+    (parse is pure).
     """
     params = _params_of(params)
+    params.validate()
     if batch_max < 1:
         raise ContractError("batch_max must be >= 1")
+    if linger_us < 0:
+        raise ContractError("linger_us must be >= 0")
     multi = None
     if devices is not None and len(devices) > 1:
         from .sharding import MultiDeviceParser
 
         multi = MultiDeviceParser(topo, devices)
 
-    def run_batch(batch: Sequence[Packet]) -> List[Packet]:
-        batch = sorted(batch, key=lambda p: p.seq_id)
+    def backend_call(batch: Sequence[Packet]) -> List[Any]:
         maps = [p.payload[1] for p in batch]
         if multi is None:
             poses = parse_batch(maps, topo, params, device=device)
         else:
-            params.validate()
             for m in maps:
                 m.validate(topo)
             conf, paf, stride = _stack_maps(maps, topo)
             poses = multi.parse_arrays(conf, paf, stride, params).all_poses()
-        return [Packet(p.seq_id, p.ingest_ns, (p.payload[0], hp)) for p, hp in zip(batch, poses)]
+        return [(p.payload[0], hp) for p, hp in zip(batch, poses)]
 
     def runner(ctx, in_ch, out_ch):
         while True:
-            first = ctx.recv(in_ch)
-            if not _is_packet(first):          # END_OF_STREAM
-                out_ch.close()
-                return
-            batch, ended = [first], False
-            while len(batch) < batch_max:
-                item = ctx.try_recv(in_ch)
-                if not _is_packet(item):
-                    ended = repr(item) == "END_OF_STREAM"
-                    break
-                batch.append(item)
-            for pkt in run_batch(batch):
-                ctx.send(out_ch, pkt)
-            if ended:
+            batch, saw_end = accumulate_batch(ctx, in_ch, batch_max, linger_us)
+            if batch:
+                hist = getattr(ctx, "batch_hist", None)
+                if hist is not None:
+                    hist[len(batch)] += 1
+                timed = getattr(ctx, "timed", None)
+                outputs = timed(backend_call, batch) if timed is not None else backend_call(batch)
+                for pkt in split_batch_results(outputs, batch):
+                    ctx.send(out_ch, pkt)
+            if saw_end:
                 out_ch.close()
                 return
 
     def item_fn(pkt: Packet) -> Packet:
-        return run_batch([pkt])[0]
+        return split_batch_results(backend_call([pkt]), [pkt])[0]
 
-    return OperatorSpec(name="postprocess", kind="transform", fn=item_fn, runner=runner)
+    return OperatorSpec(name=name, kind="transform", fn=item_fn, runner=runner)
 
 
 def pose_record(seq_id: int, poses: Sequence[HumanPose], topo: SkeletonTopology) -> str:

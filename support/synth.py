@@ -1,6 +1,8 @@
-"""Synthetic scenes and feature maps (input generator, host side).
+"""Synthetic scenes and feature maps — TEST / BENCHMARK INPUT GENERATION.
 
-Restates the reference's synthetic backend so the GPU box — where the
+Not product code: it lives outside ``paper_2108_11826_b200`` and only
+``tests/``, ``bench.py``, ``__graft_entry__.smoke()`` and ``tools/`` use it.
+It restates the reference's synthetic backend so the GPU box — where the
 reference is absent — can produce the same inputs:
 
 * ``SynthParams``          — ``synth.py:29-52``
@@ -10,7 +12,8 @@ reference is absent — can produce the same inputs:
   unit limb vectors in a corridor, averaged where limbs overlap, clamped to
   unit length; computed in fp64, stored as fp32.  Same operation order as
   the reference, so on the same numpy the maps are bit-identical
-  (``tests/test_synth_golden.py`` checks against reference-rendered maps).
+  (``tests/test_host_api.py::TestSynth`` checks against reference-rendered
+  maps, ``tests/golden/frames_golden.npz``).
 * ``procedural_scene``     — ``synth.py:224-275`` (1-5 separated stick figures,
   ``default_rng([seed, seq])``), same RNG call sequence.
 * ``crowd_scene``          — SURVEY.md §8(d) C3: 40 unseparated figures.
@@ -25,8 +28,8 @@ from typing import List, Optional, Tuple
 
 import numpy as np
 
-from .core import FeatureMaps, SkeletonTopology, TensorF32, pixel_to_cell
-from .errors import ConfigError, ContractError
+from paper_2108_11826_b200.core import FeatureMaps, SkeletonTopology, TensorF32, pixel_to_cell
+from paper_2108_11826_b200.errors import ConfigError, ContractError
 
 
 @dataclass
@@ -241,15 +244,12 @@ def render_batch(scenes, topo: SkeletonTopology, p: SynthParams):
 
 
 def render_batch_gpu(scenes, topo: SkeletonTopology, p: SynthParams, device: int = 0):
-    """``render_batch`` on the GPU (pf_render_maps): torch
-    CUDA tensors conf [B,K+1,H,W] and paf [B,2L,H,W].  Input generation only;
-    equal to the host renderer except where fp64 exp() differs from numpy's in
-    the last bit and that decides an fp32 rounding."""
-    import ctypes
-
-    import torch
-
-    from .parser import default_parser
+    """``render_batch`` on the GPU through the product's producer kernel
+    (``paper_2108_11826_b200.producer.render_maps_gpu`` -> pf_render_maps,
+    SURVEY.md §8(f) 1): torch CUDA tensors conf [B,K+1,H,W] and paf
+    [B,2L,H,W].  Equal to the host renderer except where fp64 exp() differs
+    from numpy's in the last bit and that decides an fp32 rounding."""
+    from paper_2108_11826_b200.producer import render_maps_gpu
 
     p.validate()
     k = topo.n_keypoints
@@ -262,7 +262,6 @@ def render_batch_gpu(scenes, topo: SkeletonTopology, p: SynthParams, device: int
             raise ContractError("render_batch_gpu needs scenes of one size")
     if w0 % p.stride or h0 % p.stride:
         raise ContractError("scene extents must be divisible by the stride")
-    gh, gw = h0 // p.stride, w0 // p.stride
     hmax = max(1, max(len(s.humans) for s in scenes))
     kp = np.full((len(scenes), hmax, k, 2), np.nan, dtype=np.float64)
     nh = np.zeros(len(scenes), dtype=np.int32)
@@ -272,16 +271,5 @@ def render_batch_gpu(scenes, topo: SkeletonTopology, p: SynthParams, device: int
             for part, xy in enumerate(hum.keypoints):
                 if xy is not None:
                     kp[f, hh, part] = pixel_to_cell(xy[0], xy[1], p.stride)
-    dev = torch.device("cuda", device)
-    kp_d = torch.from_numpy(kp).to(dev)
-    nh_d = torch.from_numpy(nh).to(dev)
-    conf = torch.empty((len(scenes), k + 1, gh, gw), dtype=torch.float32, device=dev)
-    paf = torch.empty((len(scenes), 2 * topo.n_limbs, gh, gw), dtype=torch.float32, device=dev)
-    eng = default_parser(topo, device)
-    ctx = eng.ctx
-    ctx.check(ctx.lib.pf_set_stream(ctx.handle, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
-    ctx.check(ctx.lib.pf_render_maps(ctx.handle, ctypes.c_void_p(kp_d.data_ptr()), ctypes.c_void_p(nh_d.data_ptr()),
-                                     len(scenes), hmax, gh, gw, float(p.sigma_conf), float(p.paf_halfwidth),
-                                     ctypes.c_void_p(conf.data_ptr()), ctypes.c_void_p(paf.data_ptr())))
-    torch.cuda.synchronize(dev)
-    return conf, paf
+    return render_maps_gpu(kp, nh, topo, h0 // p.stride, w0 // p.stride, p.sigma_conf, p.paf_halfwidth,
+                           device=device)

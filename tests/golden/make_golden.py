@@ -42,7 +42,7 @@ from poseflow.topology import load_topology  # noqa: E402
 from poseflow.types import FeatureMaps, TensorF32  # noqa: E402
 from poseflow import oracles  # noqa: E402
 
-import paper_2108_11826_b200.synth as our_synth  # noqa: E402  (crowd keypoints only: pure numpy)
+import support.synth as our_synth  # noqa: E402  (crowd keypoints only: pure numpy)
 
 TOPO = load_topology("coco18")
 P = ParserParams()

@@ -12,10 +12,11 @@ import pytest
 
 import oracle
 import paper_2108_11826_b200 as pf
+from support import synth
 from conftest import record_of
 
 pytestmark = pytest.mark.gpu
-SP = pf.SynthParams()
+SP = synth.SynthParams()
 THREADS = max(1, min(32, os.cpu_count() or 1))
 
 
@@ -39,7 +40,7 @@ def gpu_records(res, topo, idx=None):
 
 
 def test_c1_single_frame_modes(topo):
-    conf, paf = pf.synth.render_batch([pf.procedural_scene(0, 1, 656, 368, SP)], topo, SP)
+    conf, paf = synth.render_batch([synth.procedural_scene(0, 1, 656, 368, SP)], topo, SP)
     e = pf.PafParser(topo)
     for up in (1, 8):
         params = pf.ParserParams(upsample=up)
@@ -49,8 +50,8 @@ def test_c1_single_frame_modes(topo):
 
 
 def test_c2_batch64_mode_u(topo):
-    scenes = [pf.procedural_scene(7, s, 656, 368, SP) for s in range(64)]
-    conf, paf = pf.synth.render_batch(scenes, topo, SP)
+    scenes = [synth.procedural_scene(7, s, 656, 368, SP) for s in range(64)]
+    conf, paf = synth.render_batch(scenes, topo, SP)
     params = pf.ParserParams(upsample=8)
     e = pf.PafParser(topo)
     got = gpu_records(e.parse_arrays(conf, paf, 8, params), topo)
@@ -59,8 +60,8 @@ def test_c2_batch64_mode_u(topo):
 
 
 def test_c3_crowded_batch256(topo):
-    scenes = [pf.crowd_scene(42, s) for s in range(256)]
-    conf, paf = pf.synth.render_batch(scenes, topo, SP)
+    scenes = [synth.crowd_scene(42, s) for s in range(256)]
+    conf, paf = synth.render_batch(scenes, topo, SP)
     e = pf.PafParser(topo)
     params = pf.ParserParams()
     assert gpu_records(e.parse_arrays(conf, paf, 8, params), topo) == oracle_records(conf, paf, topo, params)
@@ -72,12 +73,12 @@ def test_c3_crowded_batch256(topo):
 
 @pytest.mark.parametrize("people", [6, 40])
 def test_c4_highres_1080p(topo, people):
-    sp = pf.SynthParams()
+    sp = synth.SynthParams()
     if people == 40:
-        scene = pf.crowd_scene(9, 0, 1920, 1080, 40, (150.0, 300.0))
+        scene = synth.crowd_scene(9, 0, 1920, 1080, 40, (150.0, 300.0))
     else:
-        scene = pf.GroundTruthScene(pf.crowd_scene(9, 1, 1920, 1080, 6, (300.0, 500.0)).humans, 1920, 1080)
-    conf, paf = pf.synth.render_batch([scene], topo, sp)
+        scene = synth.GroundTruthScene(synth.crowd_scene(9, 1, 1920, 1080, 6, (300.0, 500.0)).humans, 1920, 1080)
+    conf, paf = synth.render_batch([scene], topo, sp)
     assert conf.shape == (1, 19, 135, 240)
     e = pf.PafParser(topo)
     for up in (1, 8):
@@ -102,8 +103,8 @@ def test_c5_stream_8192_properties(topo):
     repeatable, and an oracle spot check on 48 frames."""
     import torch
 
-    scenes = [pf.procedural_scene(5, s, 656, 368, SP) for s in range(128)]
-    conf_h, paf_h = pf.synth.render_batch(scenes, topo, SP)
+    scenes = [synth.procedural_scene(5, s, 656, 368, SP) for s in range(128)]
+    conf_h, paf_h = synth.render_batch(scenes, topo, SP)
     idx = np.arange(8192) % 128
     conf = torch.from_numpy(conf_h).cuda()[torch.from_numpy(idx).cuda()].contiguous()
     paf = torch.from_numpy(paf_h).cuda()[torch.from_numpy(idx).cuda()].contiguous()

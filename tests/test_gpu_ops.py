@@ -8,6 +8,7 @@ import pytest
 
 import oracle
 import paper_2108_11826_b200 as pf
+from support import synth
 from conftest import golden_path
 
 pytestmark = pytest.mark.gpu
@@ -82,8 +83,8 @@ def test_bilinear_resize_api():
 
 
 def test_batched_postprocess_operator(topo):
-    sp = pf.SynthParams()
-    maps = [pf.render_feature_maps(pf.procedural_scene(12, s, 656, 368, sp), topo, sp) for s in range(5)]
+    sp = synth.SynthParams()
+    maps = [synth.render_feature_maps(synth.procedural_scene(12, s, 656, 368, sp), topo, sp) for s in range(5)]
     op = pf.make_batched_postprocess(topo, pf.ParserParams(upsample=8), batch_max=3)
     one = pf.make_postprocess(topo, pf.ParserParams(upsample=8))
     pkts = [pf.Packet(s, 0, (None, m)) for s, m in enumerate(maps)]
@@ -92,19 +93,34 @@ def test_batched_postprocess_operator(topo):
     assert [pf.pose_record(i, x, topo) for i, x in enumerate(a)] == \
            [pf.pose_record(i, x, topo) for i, x in enumerate(b)]
 
-    class Ctx:                                   # the reference runner protocol
+    class Sentinel:                              # dataflow.py:26-37 channel sentinels
+        def __init__(self, name):
+            self.name = name
+
+        def __repr__(self):
+            return self.name
+
+    END, NO_ITEM = Sentinel("END_OF_STREAM"), Sentinel("NO_ITEM")
+
+    class Ctx:                                   # the reference runner protocol (dataflow.py:240-280)
         def __init__(self, items):
             self.items = list(items)
             self.out = []
+            self.batch_hist = {}
+            self.busy = 0
 
         def recv(self, ch):
-            return self.items.pop(0) if self.items else "END"
+            return self.items.pop(0) if self.items else END
 
         def try_recv(self, ch):
-            return self.items.pop(0) if self.items else "NO_ITEM"
+            return self.items.pop(0) if self.items else NO_ITEM
 
         def send(self, ch, pkt):
             self.out.append(pkt)
+
+        def timed(self, fn, *args):
+            self.busy += 1
+            return fn(*args)
 
     class Ch:
         closed = False
@@ -112,9 +128,15 @@ def test_batched_postprocess_operator(topo):
         def close(self):
             self.closed = True
 
+    import collections
+
     ctx, ch = Ctx(pkts), Ch()
+    ctx.batch_hist = collections.Counter()
     op.runner(ctx, None, ch)
     assert ch.closed and [p.seq_id for p in ctx.out] == list(range(5))
+    assert dict(ctx.batch_hist) == {3: 1, 2: 1} and ctx.busy == 2      # batch_max 3: 3 + 2
+    with pytest.raises(pf.BackendError):                                 # scheduler.py:96-101
+        op.runner(Ctx([pkts[1], pkts[0]]), None, Ch())
     assert [pf.pose_record(p.seq_id, p.payload[1], topo) for p in ctx.out] == \
            [pf.pose_record(i, x, topo) for i, x in enumerate(b)]
 
@@ -123,9 +145,9 @@ def test_multi_device_parser_and_operator(topo):
     """In-process sharding: contiguous shards on several
     contexts (two on this one GPU, plus an empty shard) give the single-context
     results in frame order; the batched operator with ``devices`` likewise."""
-    sp = pf.SynthParams()
-    scenes = [pf.procedural_scene(21, s, 656, 368, sp) for s in range(7)] + [pf.crowd_scene(6, 0)]
-    conf, paf = pf.synth.render_batch(scenes, topo, sp)
+    sp = synth.SynthParams()
+    scenes = [synth.procedural_scene(21, s, 656, 368, sp) for s in range(7)] + [synth.crowd_scene(6, 0)]
+    conf, paf = synth.render_batch(scenes, topo, sp)
     params = pf.ParserParams(upsample=8)
     single = pf.PafParser(topo).parse_arrays(conf, paf, 8, params)
     want = [pf.pose_record(f, single.poses(f), topo) for f in range(len(scenes))]
@@ -137,7 +159,7 @@ def test_multi_device_parser_and_operator(topo):
         one = multi.parse_arrays(conf[:1], paf[:1], 8, params)     # shards 1 and 2 empty
         assert pf.pose_record(0, one.poses(0), topo) == want[0]
         multi.close()
-    maps = [pf.render_feature_maps(s, topo, sp) for s in scenes[:5]]
+    maps = [synth.render_feature_maps(s, topo, sp) for s in scenes[:5]]
     op = pf.make_batched_postprocess(topo, params, batch_max=4, devices=[0, 0])
     pkts = [pf.Packet(s, 0, (None, m)) for s, m in enumerate(maps)]
     got = [pf.pose_record(p.seq_id, op.fn(p).payload[1], topo) for p in pkts]
@@ -149,10 +171,10 @@ def test_gpu_renderer_matches_host(topo):
     procedural and crowded scenes: bit-identical except where fp64 exp()
     rounds differently from numpy's (then within 1 fp32 ulp), and the parse
     of both renderings gives the same records."""
-    sp = pf.SynthParams()
-    scenes = [pf.procedural_scene(3, s, 656, 368, sp) for s in range(6)] + [pf.crowd_scene(2, 0)]
-    conf_h, paf_h = pf.synth.render_batch(scenes, topo, sp)
-    conf_g, paf_g = pf.synth.render_batch_gpu(scenes, topo, sp)
+    sp = synth.SynthParams()
+    scenes = [synth.procedural_scene(3, s, 656, 368, sp) for s in range(6)] + [synth.crowd_scene(2, 0)]
+    conf_h, paf_h = synth.render_batch(scenes, topo, sp)
+    conf_g, paf_g = synth.render_batch_gpu(scenes, topo, sp)
     conf_g, paf_g = conf_g.cpu().numpy(), paf_g.cpu().numpy()
     assert np.array_equal(paf_g, paf_h)                      # sqrt / division only: exact
     diff = conf_g != conf_h

@@ -9,11 +9,12 @@ import pytest
 
 import oracle
 import paper_2108_11826_b200 as pf
+from support import synth
 from conftest import golden_path, record_of
 
 pytestmark = pytest.mark.gpu
 
-SP = pf.SynthParams()
+SP = synth.SynthParams()
 
 
 @pytest.fixture(scope="module")
@@ -42,7 +43,7 @@ def assert_batch_matches(eng, topo, conf, paf, params, stride=8, stages=True):
 
 
 def render(scenes, topo):
-    return pf.synth.render_batch(scenes, topo, SP)
+    return synth.render_batch(scenes, topo, SP)
 
 
 # ---------------------------------------------------------------- golden
@@ -124,7 +125,7 @@ def test_score_limb_golden():
 # ---------------------------------------------------------------- vs oracle
 @pytest.mark.parametrize("up", [1, 8])
 def test_procedural_frames(eng, topo, up):
-    scenes = [pf.procedural_scene(7, s, 656, 368, SP) for s in range(24 if up == 1 else 8)]
+    scenes = [synth.procedural_scene(7, s, 656, 368, SP) for s in range(24 if up == 1 else 8)]
     conf, paf = render(scenes, topo)
     assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
 
@@ -133,7 +134,7 @@ def test_procedural_frames(eng, topo, up):
 def test_crowded_frames(eng, topo, up):
     """40-person scenes: merges, part conflicts, slot-taken skips, min_parts drops,
     and > kCandSmem gated candidates (the global spill path)."""
-    scenes = [pf.crowd_scene(3, s) for s in range(3 if up == 1 else 1)]
+    scenes = [synth.crowd_scene(3, s) for s in range(3 if up == 1 else 1)]
     conf, paf = render(scenes, topo)
     assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
 
@@ -146,21 +147,21 @@ def test_crowded_frames(eng, topo, up):
                                 dict(min_human_score=0.0), dict(min_human_score=0.9)])
 @pytest.mark.parametrize("up", [1, 8])
 def test_param_variants(eng, topo, kw, up):
-    scenes = [pf.procedural_scene(19, s, 656, 368, SP) for s in range(3)] + [pf.crowd_scene(5, 0)]
+    scenes = [synth.procedural_scene(19, s, 656, 368, SP) for s in range(3)] + [synth.crowd_scene(5, 0)]
     conf, paf = render(scenes, topo)
     assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up, **kw))
 
 
 @pytest.mark.parametrize("up", [2, 4])
 def test_other_upsample_factors(eng, topo, up):
-    scenes = [pf.procedural_scene(23, s, 656, 368, SP) for s in range(3)]
+    scenes = [synth.procedural_scene(23, s, 656, 368, SP) for s in range(3)]
     conf, paf = render(scenes, topo)
     assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
 
 
 def test_stride_and_odd_grid(eng, topo):
     # 45x37 grid, stride 8 -> 360x296 input; 1 person near the border
-    scene = pf.GroundTruthScene(humans=(pf.procedural_scene(2, 0, 360, 296, SP).humans), input_w=360,
+    scene = synth.GroundTruthScene(humans=(synth.procedural_scene(2, 0, 360, 296, SP).humans), input_w=360,
                                 input_h=296)
     conf, paf = render([scene], topo)
     for up in (1, 2, 8):
@@ -185,7 +186,7 @@ def test_corner_kernel_overflow_and_nonfinite(eng, topo):
     """Mode U corner kernel edge cases: an all-hot smooth frame (hot cells beyond
     the shared list -> whole-plane slow path), a noise part map (candidate list
     overflow), NaN / +inf / -inf sources; Mode R sees the same non-finite maps."""
-    scenes = [pf.procedural_scene(41, s, 656, 368, SP) for s in range(4)]
+    scenes = [synth.procedural_scene(41, s, 656, 368, SP) for s in range(4)]
     conf, paf = render(scenes, topo)
     K = topo.n_keypoints
     yy, xx = np.mgrid[0:conf.shape[2], 0:conf.shape[3]].astype(np.float32)
@@ -202,14 +203,14 @@ def test_corner_kernel_overflow_and_nonfinite(eng, topo):
 
 
 def test_blur_paths(eng, topo):
-    scenes = [pf.procedural_scene(29, s, 656, 368, SP) for s in range(2)]
+    scenes = [synth.procedural_scene(29, s, 656, 368, SP) for s in range(2)]
     conf, paf = render(scenes, topo)
     for up, sigma in ((8, 1.0), (8, 2.5), (1, 0.8)):
         assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up, blur_sigma=sigma))
 
 
 def test_materialised_and_generic_paths_agree(topo):
-    scenes = [pf.procedural_scene(31, s, 656, 368, SP) for s in range(4)] + [pf.crowd_scene(8, 1)]
+    scenes = [synth.procedural_scene(31, s, 656, 368, SP) for s in range(4)] + [synth.crowd_scene(8, 1)]
     conf, paf = render(scenes, topo)
     params = pf.ParserParams(upsample=8)
     e = pf.PafParser(topo, debug=True)
@@ -225,8 +226,8 @@ def test_materialised_and_generic_paths_agree(topo):
 # ---------------------------------------------------------------- API contract
 def test_parse_drop_in(topo):
     """parse(maps, topo, params) returns HumanPose lists equal to the reference's."""
-    scene = pf.procedural_scene(0, 1, 656, 368, SP)
-    maps = pf.render_feature_maps(scene, topo, SP)
+    scene = synth.procedural_scene(0, 1, 656, 368, SP)
+    maps = synth.render_feature_maps(scene, topo, SP)
     poses = pf.parse(maps, topo, pf.ParserParams())
     want = oracle.parse(maps.conf.array, maps.paf.array, topo, pf.ParserParams(), 8)
     assert pf.pose_record(0, poses, topo) == record_of(want.humans, topo)
@@ -236,7 +237,7 @@ def test_parse_drop_in(topo):
 
 
 def test_parse_batch_equals_per_frame(topo):
-    maps = [pf.render_feature_maps(pf.procedural_scene(4, s, 656, 368, SP), topo, SP) for s in range(5)]
+    maps = [synth.render_feature_maps(synth.procedural_scene(4, s, 656, 368, SP), topo, SP) for s in range(5)]
     params = pf.ParserParams(upsample=8)
     batch = pf.parse_batch(maps, topo, params)
     single = [pf.parse(m, topo, params) for m in maps]
@@ -248,7 +249,7 @@ def test_parse_batch_equals_per_frame(topo):
 
 
 def test_deterministic(eng, topo):
-    conf, paf = render([pf.crowd_scene(4, s) for s in range(2)], topo)
+    conf, paf = render([synth.crowd_scene(4, s) for s in range(2)], topo)
     a = eng.parse_arrays(conf, paf, 8, pf.ParserParams(upsample=8))
     b = eng.parse_arrays(conf, paf, 8, pf.ParserParams(upsample=8))
     assert [pf.pose_record(f, a.poses(f), topo) for f in range(2)] == \
@@ -258,7 +259,7 @@ def test_deterministic(eng, topo):
 def test_device_tensor_path(topo):
     import torch
 
-    conf, paf = render([pf.procedural_scene(6, s, 656, 368, SP) for s in range(6)], topo)
+    conf, paf = render([synth.procedural_scene(6, s, 656, 368, SP) for s in range(6)], topo)
     params = pf.ParserParams(upsample=8)
     e = pf.PafParser(topo)
     host = e.parse_arrays(conf, paf, 8, params)
@@ -277,7 +278,7 @@ def test_pinned_paf_read_in_place(topo, up):
     """pf_parse_host with pinned host maps: the PAF read in place over PCIe
     (PF_OPT_PAF_ZERO_COPY, default) gives the copied path's results and the
     oracle's, on procedural and crowded frames across several host chunks."""
-    scenes = [pf.procedural_scene(12, s, 656, 368, SP) for s in range(5)] + [pf.crowd_scene(4, 0)]
+    scenes = [synth.procedural_scene(12, s, 656, 368, SP) for s in range(5)] + [synth.crowd_scene(4, 0)]
     conf, paf = render(scenes, topo)
     reps = 46                                          # 276 frames: host chunks of 128, 128 and 20 frames
                                                        # (the last below the split threshold: one-kernel NMS)
@@ -304,7 +305,7 @@ def test_pinned_paf_read_in_place(topo, up):
 
 def test_empty_inputs(eng, topo):
     assert pf.parse_batch([], topo, pf.ParserParams()) == []
-    zero = pf.render_feature_maps(pf.GroundTruthScene((), 64, 64), topo, SP)
+    zero = synth.render_feature_maps(synth.GroundTruthScene((), 64, 64), topo, SP)
     assert pf.parse(zero, topo, pf.ParserParams()) == []
     r = eng.parse_arrays(np.zeros((3, 19, 0, 0), np.float32), np.zeros((3, 38, 0, 0), np.float32), 8,
                          pf.ParserParams())
@@ -316,7 +317,7 @@ def test_empty_inputs(eng, topo):
 
 
 def test_errors_before_work(topo):
-    maps = pf.render_feature_maps(pf.procedural_scene(0, 1, 656, 368, SP), topo, SP)
+    maps = synth.render_feature_maps(synth.procedural_scene(0, 1, 656, 368, SP), topo, SP)
     with pytest.raises(pf.ConfigError):
         pf.parse(maps, topo, pf.ParserParams(nms_window=4))
     stub = pf.SkeletonTopology.create(["a", "b"], [[0, 1]])
@@ -329,7 +330,7 @@ def test_errors_before_work(topo):
 
 
 def test_capacity_errors_are_loud(topo):
-    conf, paf = render([pf.crowd_scene(3, 0)], topo)
+    conf, paf = render([synth.crowd_scene(3, 0)], topo)
     e = pf.PafParser(topo, caps=dict(max_peaks_per_part=8))
     with pytest.raises(pf.CapacityError, match="max_peaks_per_part"):
         e.parse_arrays(conf, paf, 8, pf.ParserParams())
@@ -407,7 +408,7 @@ def test_split_paths_agree(topo, up):
     scoring over all frames + finish) give the one-kernel paths' peaks,
     connections and records on procedural, crowded and random frames."""
     rng = np.random.default_rng(99)
-    scenes = [pf.procedural_scene(77, s, 656, 368, SP) for s in range(6)] + [pf.crowd_scene(11, s) for s in range(2)]
+    scenes = [synth.procedural_scene(77, s, 656, 368, SP) for s in range(6)] + [synth.crowd_scene(11, s) for s in range(2)]
     conf, paf = render(scenes, topo)
     conf[5, :topo.n_keypoints] = rng.random(conf.shape[1:])[:topo.n_keypoints].astype(np.float32)   # noise part maps
     params = pf.ParserParams(upsample=up)
@@ -430,7 +431,7 @@ def test_large_maps_take_the_split_kernels(eng, topo):
     """135x240 maps (1080x1920 input): too large for the one-kernel corner
     form, so even a 2-frame batch runs k_nms_up_scan -> k_corner_finish; the
     peaks and records equal the oracle's and the materialised path's."""
-    scenes = [pf.procedural_scene(31, s, 1920, 1080, SP) for s in range(2)]
+    scenes = [synth.procedural_scene(31, s, 1920, 1080, SP) for s in range(2)]
     conf, paf = render(scenes, topo)
     assert conf.shape[2:] == (135, 240)
     params = pf.ParserParams(upsample=8)

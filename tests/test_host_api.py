@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2108_11826_b200 as pf
+from support import synth
 from conftest import golden_path
 
 
@@ -146,24 +147,24 @@ class TestSynthPort:
 
     def test_procedural_scenes(self):
         want = json.load(open(golden_path("scenes_golden.json")))
-        sp = pf.SynthParams()
+        sp = synth.SynthParams()
         for key, humans in want.items():
             seed, seq = (int(x) for x in key.split("_"))
-            got = pf.procedural_scene(seed, seq, 656, 368, sp)
+            got = synth.procedural_scene(seed, seq, 656, 368, sp)
             assert [[list(k) for k in h.keypoints] for h in got.humans] == humans
 
     def test_render_matches_reference(self, topo, golden_frames):
         data, recs = golden_frames
-        sp = pf.SynthParams()
+        sp = synth.SynthParams()
         for name in recs["names"]:
             kps = data[f"{name}.kps"]
-            humans = tuple(pf.GroundTruthHuman(tuple(None if np.isnan(k[0]) else (float(k[0]), float(k[1]))
+            humans = tuple(synth.GroundTruthHuman(tuple(None if np.isnan(k[0]) else (float(k[0]), float(k[1]))
                                                      for k in h)) for h in kps)
-            m = pf.render_feature_maps(pf.GroundTruthScene(humans, 656, 368), topo, sp)
+            m = synth.render_feature_maps(synth.GroundTruthScene(humans, 656, 368), topo, sp)
             assert np.array_equal(m.conf.array, data[f"{name}.conf"]), name
             assert np.array_equal(m.paf.array, data[f"{name}.paf"]), name
 
     def test_crowd_scene(self):
-        s = pf.crowd_scene(3, 0)
+        s = synth.crowd_scene(3, 0)
         assert len(s.humans) == 40
         s.validate(18)

@@ -90,3 +90,18 @@ def test_records_empty_batch():
     topo = pf.load_topology("coco18")
     fake = _Fake(np.random.default_rng(0), 0, topo.n_keypoints)
     assert format_records(fake, topo) == []
+
+
+def test_records_non_ascii_part_names():
+    # json.dumps(ensure_ascii=True) escapes by code point: é for U+00E9,
+    # 中 for a BMP ideograph, a surrogate pair for U+1F600; control and
+    # DEL characters as \u00XX; quotes and backslashes by their short forms
+    names = ["nosé", "中心", "smile\U0001F600", "tab\tq\"b\\", "del\x7f", "ctl\x01",
+             "ÿĀ߿ࠀ￿", "plain"]
+    limbs = [(k, k + 1) for k in range(len(names) - 1)]
+    topo = pf.SkeletonTopology.create(names, limbs)
+    rng = np.random.default_rng(99)
+    fake = _Fake(rng, 40, topo.n_keypoints)
+    got = format_records(fake, topo, 5)
+    want = [pf.pose_record(5 + f, fake.poses(f), topo) for f in range(fake.n_frames)]
+    assert got == want

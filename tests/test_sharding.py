@@ -12,6 +12,7 @@ import pytest
 import torch.multiprocessing as mp
 
 import paper_2108_11826_b200 as pf
+from support import synth
 from paper_2108_11826_b200 import sharding
 
 
@@ -47,9 +48,9 @@ def _oracle_parse_fn(topo, params):
 
 def _inputs():
     topo = pf.load_topology("coco18")
-    sp = pf.SynthParams()
-    scenes = [pf.procedural_scene(11, s, 656, 368, sp) for s in range(6)]
-    conf, paf = pf.synth.render_batch(scenes, topo, sp)
+    sp = synth.SynthParams()
+    scenes = [synth.procedural_scene(11, s, 656, 368, sp) for s in range(6)]
+    conf, paf = synth.render_batch(scenes, topo, sp)
     return topo, conf, paf
 
 

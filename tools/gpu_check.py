@@ -4,9 +4,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import oracle
 import paper_2108_11826_b200 as pf
+from support import synth
 
 topo = pf.load_topology("coco18")
-sp = pf.SynthParams()
+sp = synth.SynthParams()
 
 def rec(f, humans):
     return pf.pose_record(f, [pf.HumanPose(keypoints=tuple(None if k is None else pf.Keypoint(*k) for k in kps), score=s, n_parts=n) for s, n, kps in humans], topo)
@@ -14,7 +15,7 @@ def rec(f, humans):
 def check(name, scenes, up, params=None, stride=8):
     params = params or pf.ParserParams(upsample=up)
     params.upsample = up
-    conf, paf = pf.synth.render_batch(scenes, topo, sp)
+    conf, paf = synth.render_batch(scenes, topo, sp)
     eng = pf.PafParser(topo, debug=True)
     t0 = time.time()
     got = eng.parse_arrays(conf, paf, stride, params)
@@ -45,12 +46,12 @@ def check(name, scenes, up, params=None, stride=8):
     return bad
 
 total = 0
-total += check("procedural-R", [pf.procedural_scene(7, s, 656, 368, sp) for s in range(16)], 1)
-total += check("procedural-U", [pf.procedural_scene(7, s, 656, 368, sp) for s in range(8)], 8)
-total += check("crowd-R", [pf.crowd_scene(3, s) for s in range(2)], 1)
-total += check("crowd-U", [pf.crowd_scene(3, s) for s in range(1)], 8)
+total += check("procedural-R", [synth.procedural_scene(7, s, 656, 368, sp) for s in range(16)], 1)
+total += check("procedural-U", [synth.procedural_scene(7, s, 656, 368, sp) for s in range(8)], 8)
+total += check("crowd-R", [synth.crowd_scene(3, s) for s in range(2)], 1)
+total += check("crowd-U", [synth.crowd_scene(3, s) for s in range(1)], 8)
 print("TOTAL mismatching", total)
-total += check("procedural-U-w5", [pf.procedural_scene(9, s, 656, 368, sp) for s in range(4)], 8, pf.ParserParams(nms_window=5))
-total += check("procedural-U-w7", [pf.procedural_scene(9, s, 656, 368, sp) for s in range(2)], 8, pf.ParserParams(nms_window=7))
-total += check("procedural-U-x4", [pf.procedural_scene(9, s, 656, 368, sp) for s in range(2)], 4)
+total += check("procedural-U-w5", [synth.procedural_scene(9, s, 656, 368, sp) for s in range(4)], 8, pf.ParserParams(nms_window=5))
+total += check("procedural-U-w7", [synth.procedural_scene(9, s, 656, 368, sp) for s in range(2)], 8, pf.ParserParams(nms_window=7))
+total += check("procedural-U-x4", [synth.procedural_scene(9, s, 656, 368, sp) for s in range(2)], 4)
 print("TOTAL2 mismatching", total)
