@@ -270,59 +270,28 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ PCIe
-class PcieCounters:
-    """NVML PCIe byte counters of one GPU (NVML_FI_DEV_PCIE_COUNT_RX/TX_BYTES):
-    the link traffic a region moved, measured in-run."""
+def gpu_numa(gpu: int):
+    """NUMA node and local CPUs of the GPU's PCIe slot (sysfs), for NUMA-local
+    pinned host buffers."""
+    try:
+        import torch
 
-    def __init__(self, gpu: int):
-        self.h = None
-        try:
-            import pynvml
-            import torch
-
-            pynvml.nvmlInit()
-            p = torch.cuda.get_device_properties(gpu)
-            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
-            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
-            self.nv = pynvml
-            self.bus = bus
-            if self.read() is None:
-                self.h = None
-        except Exception:
-            self.h = None
-
-    def read(self):
-        if self.h is None:
-            return None
-        try:
-            vals = self.nv.nvmlDeviceGetFieldValues(
-                self.h, [self.nv.NVML_FI_DEV_PCIE_COUNT_RX_BYTES, self.nv.NVML_FI_DEV_PCIE_COUNT_TX_BYTES])
-            if any(v.nvmlReturn != 0 for v in vals):
-                return None
-            return (int(vals[0].value.ullVal), int(vals[1].value.ullVal))
-        except Exception:
-            return None
-
-    def numa_cpus(self):
-        """CPUs local to the GPU's PCIe root (sysfs), for NUMA-local pinned buffers."""
-        if self.h is None:
-            return None, None
-        base = f"/sys/bus/pci/devices/{self.bus.lower()}"
-        try:
-            with open(os.path.join(base, "numa_node")) as f:
-                node = int(f.read().strip())
-            with open(os.path.join(base, "local_cpulist")) as f:
-                spec = f.read().strip()
-        except Exception:
-            return None, None
-        cpus = set()
-        for part in spec.split(","):
-            if "-" in part:
-                a, b = part.split("-")
-                cpus.update(range(int(a), int(b) + 1))
-            elif part:
-                cpus.add(int(part))
-        return node, cpus
+        p = torch.cuda.get_device_properties(gpu)
+        base = f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(os.path.join(base, "numa_node")) as f:
+            node = int(f.read().strip())
+        with open(os.path.join(base, "local_cpulist")) as f:
+            spec = f.read().strip()
+    except Exception:
+        return None, None
+    cpus = set()
+    for part in spec.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.update(range(int(a), int(b) + 1))
+        elif part:
+            cpus.add(int(part))
+    return node, cpus
 
 
 def pinned_copy_peaks(dev, nbytes: int = 1 << 30):
@@ -529,8 +498,7 @@ def run_b200(args, rank, world, local_rank):
     gpu = local_rank % ndev
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
-    pcie = PcieCounters(gpu)
-    numa_node, numa_cpus = pcie.numa_cpus()
+    numa_node, numa_cpus = gpu_numa(gpu)
     if numa_cpus and world > 1:
         try:      # pinned buffers are first-touched by this process: keep them on the GPU's NUMA node
             os.sched_setaffinity(0, numa_cpus & set(range(os.cpu_count() or 1)) or numa_cpus)
@@ -609,27 +577,26 @@ def run_b200(args, rank, world, local_rank):
         r = eng.parse_arrays(pin_conf.array, pin_paf.array, STRIDE, params)
     barrier()
     e2e_steps = min(args.steps, args.e2e_steps)
-    c0 = pcie.read()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):          # synchronous API: H2D + kernels + D2H of humans
         r = eng.parse_arrays(pin_conf.array, pin_paf.array, STRIDE, params)
     e2e_s_local = time.perf_counter() - t0
-    c1 = pcie.read()
     e2e_s = max_over_ranks(e2e_s_local)
     e2e_value = world * E * e2e_steps / e2e_s
     # counted bytes: conf planes copied by the copy engine (K of K+1 planes;
-    # the background plane is never read) and the humans read back
+    # the background plane is never read), the PAF sectors the parse kernel
+    # reads in place — counted in-run by one instrumented call of the same
+    # path (PF_OPT_COUNT_PAF: a bitmap of the 32-byte sectors sampled) — and
+    # the humans read back
     h2d_conf = E * K_PARTS * PLANE * 4
+    eng.ctx.set_option(_native.PF_OPT_COUNT_PAF, 1)
+    r_count = eng.parse_arrays(pin_conf.array, pin_paf.array, STRIDE, params)
+    paf_sectors = eng.ctx.paf_sectors()
+    eng.ctx.set_option(_native.PF_OPT_COUNT_PAF, 0)
+    h2d_paf = paf_sectors * 32
+    counted_same = r_count.total_humans == r.total_humans
     d2h = E * 8 + 32 + r.total_humans * (8 + 4 + K_PARTS * (8 + 8 + 4 + 4))
-    pcie_meas = None
-    if c0 is not None and c1 is not None:
-        rx = (c1[0] - c0[0]) / e2e_steps
-        tx = (c1[1] - c0[1]) / e2e_steps
-        pcie_meas = {"rx_bytes_per_step": rx, "tx_bytes_per_step": tx, "source": "NVML PCIE_COUNT_RX/TX_BYTES",
-                     "paf_in_place_bytes_per_frame_upper": max(0.0, rx - h2d_conf) / E,
-                     "note": "RX = every byte the GPU received on the link during the e2e steps: conf copies, "
-                             "PAF read completions for the in-place reads, protocol overhead"}
-    h2d = int(h2d_conf + (pcie_meas["rx_bytes_per_step"] - h2d_conf if pcie_meas else E * PAF_FRAME_BYTES))
+    h2d = int(h2d_conf + h2d_paf)
     h2d_gbs = h2d * e2e_steps / e2e_s_local / 1e9
 
     # ---- unfused Mode U stages (materialised x8 maps through HBM) ----
@@ -702,13 +669,13 @@ def run_b200(args, rank, world, local_rank):
             roof["stage_upsample_nms"] = {"kernels": fused, "ms_per_step": ms,
                                           "achieved_gbs": b / (ms / 1e3) / 1e9,
                                           "frac": b / (ms / 1e3) / 1e9 / peak_gbs}
-        step_bytes = F * (BYTES_FUSED_UN + (pcie_meas["paf_in_place_bytes_per_frame_upper"] if pcie_meas else 0))
+        step_bytes = F * BYTES_FUSED_UN + h2d_paf * F / E
         roof["step"] = {"compulsory_bytes_per_frame": step_bytes / F,
                         "floor_ms": step_bytes / (peak_gbs * 1e9) * 1e3,
                         "ms_per_step": elapsed_ms / args.steps,
                         "frac": (step_bytes / (peak_gbs * 1e9) * 1e3) / (elapsed_ms / args.steps),
-                        "note": "conf part planes + the PAF sectors the line integral samples (the in-place "
-                                "PCIe bytes of the e2e leg, an upper bound)"}
+                        "note": "conf part planes + the distinct 32-byte PAF sectors the line integral samples "
+                                "(counted in-run, PF_OPT_COUNT_PAF)"}
 
     # ---- CPU baselines (rank 0, N == 1) ----
     cpu = cpu_port = None
@@ -751,7 +718,11 @@ def run_b200(args, rank, world, local_rank):
                     "d2h_bytes_per_step": d2h, "frames_per_step": E, "steps": e2e_steps,
                     "h2d_gbs": h2d_gbs, "pcie_peak_gbs": copy_peak["h2d"], "d2h_peak_gbs": copy_peak["d2h"],
                     "frac_of_pcie_peak": h2d_gbs / copy_peak["h2d"] if copy_peak["h2d"] else None,
-                    "h2d_conf_copied": h2d_conf, "pcie_measured": pcie_meas,
+                    "h2d_conf_copied": h2d_conf, "h2d_paf_read_in_place": h2d_paf,
+                    "paf_bytes_per_frame": h2d_paf / E,
+                    "paf_bytes_source": "distinct 32-byte PAF sectors sampled, counted in-run by an instrumented "
+                                        "call of the same path (PF_OPT_COUNT_PAF)",
+                    "instrumented_call_same_humans": counted_same,
                     "numa_node": numa_node,
                     "path": "pf_parse_host (pinned host maps: conf planes H2D by copy engine, PAF read "
                             "in place over PCIe by the parse kernel -> kernels -> D2H humans)"},

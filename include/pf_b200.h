@@ -169,11 +169,20 @@ int pf_set_debug(pf_ctx *ctx, int enable);
                                     0 off, 1 auto (batches of >= 32 frames, default), 2 always */
 #define PF_OPT_PAF_ZERO_COPY 8   /* pf_parse_host (default 1): a pinned host PAF is read in place by the
                                     parse kernel, so only the sampled cells cross PCIe; 0: copy it whole */
+#define PF_OPT_PDL 12             /* bitmask: programmatic dependent launch per split-kernel launch site
+                                    (process-wide A/B; default 0 = measured fastest) */
+#define PF_OPT_COUNT_PAF 13       /* instrumented parse: count the 32-byte PAF sectors the line integral
+                                    reads (one-kernel parse; read with pf_get_paf_sectors) */
 int pf_set_option(pf_ctx *ctx, int option, int value);
+
+/* With PF_OPT_COUNT_PAF on: distinct 32-byte PAF sectors the last parse call
+ * sampled, summed over its frames (= the PCIe read bytes / 32 of an in-place
+ * pinned PAF, each sector fetched once). */
+int pf_get_paf_sectors(pf_ctx *ctx, long long *sectors);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch
  * counts accumulated since the last reset; ids index pf_kernel_name(). */
-#define PF_N_KERNELS 14
+#define PF_N_KERNELS 15
 const char *pf_kernel_name(int id);
 int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset);
 int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,

@@ -536,6 +536,9 @@ int orc_parse(const float *conf, const float *paf, int K, int L,
 }
 
 /* ------------------------------------------------------------------ */
+/* Separable Gaussian (no reference; DESIGN.md §5 defines it): horizontal then
+ * vertical, clamped edges, acc = fma(w_k, v, acc) in fp64 from 0.0 in ascending
+ * k, each pass rounded to fp32.  C99 fma() is correctly rounded. */
 int orc_blur_chw(float *maps, int C, int h, int w, const double *taps, int r)
 {
     if (r <= 0) return 0;
@@ -548,7 +551,7 @@ int orc_blur_chw(float *maps, int C, int h, int w, const double *taps, int r)
                 double acc = 0.0;
                 for (int k = -r; k <= r; ++k) {
                     int xx = x + k < 0 ? 0 : (x + k > w - 1 ? w - 1 : x + k);
-                    acc += taps[k + r] * (double)m[(size_t)y * w + xx];
+                    acc = fma(taps[k + r], (double)m[(size_t)y * w + xx], acc);
                 }
                 tmp[(size_t)y * w + x] = (float)acc;
             }
@@ -557,7 +560,7 @@ int orc_blur_chw(float *maps, int C, int h, int w, const double *taps, int r)
                 double acc = 0.0;
                 for (int k = -r; k <= r; ++k) {
                     int yy = y + k < 0 ? 0 : (y + k > h - 1 ? h - 1 : y + k);
-                    acc += taps[k + r] * (double)tmp[(size_t)yy * w + x];
+                    acc = fma(taps[k + r], (double)tmp[(size_t)yy * w + x], acc);
                 }
                 m[(size_t)y * w + x] = (float)acc;
             }

@@ -28,7 +28,9 @@ PF_OPT_PAF_ZERO_COPY = 8
 PF_OPT_CORNER_SPLIT = 9
 PF_OPT_PARSE_SPLIT = 10
 PF_OPT_CONF_ZERO_COPY = 11
-PF_N_KERNELS = 14
+PF_OPT_PDL = 12
+PF_OPT_COUNT_PAF = 13
+PF_N_KERNELS = 15
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (
@@ -39,7 +41,7 @@ EXPORTED_SYMBOLS = (
     "pf_get_kernel_times", "pf_get_peaks", "pf_get_connections",
     "pf_preprocess_device", "pf_preprocess_f32_device", "pf_resize_device", "pf_host_alloc", "pf_host_free",
     "pf_launch_count", "pf_gaussian_taps", "pf_format_records", "pf_format_float", "pf_render_maps",
-    "pf_overlay",
+    "pf_overlay", "pf_get_paf_sectors",
 )
 
 
@@ -143,6 +145,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pf_overlay.restype = c_int
         lib.pf_format_float.restype = c_int
         lib.pf_gaussian_taps.argtypes = [ctypes.c_double, vp, c_int]
+        lib.pf_get_paf_sectors.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
         del i32
         _lib = lib
         return lib
@@ -206,6 +209,12 @@ class Context:
 
     def set_option(self, option: int, value: int) -> None:
         self.check(self.lib.pf_set_option(self.handle, int(option), int(value)))
+
+    def paf_sectors(self) -> int:
+        """Distinct 32-byte PAF sectors the last parse sampled (PF_OPT_COUNT_PAF on)."""
+        n = ctypes.c_longlong()
+        self.check(self.lib.pf_get_paf_sectors(self.handle, ctypes.byref(n)))
+        return int(n.value)
 
     def kernel_times(self, reset: bool = False) -> dict:
         """{kernel name: (total ms, launches)} since the last reset (PF_OPT_TIMING)."""

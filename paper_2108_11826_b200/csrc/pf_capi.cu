@@ -23,6 +23,10 @@
 
 using namespace pf;
 
+namespace pf {
+int g_pdl_mask = 0;
+}
+
 #ifndef PF_CORNER_SPLIT_DEFAULT
 #define PF_CORNER_SPLIT_DEFAULT 1
 #endif
@@ -206,6 +210,9 @@ struct pf_ctx {
     int win_variant = 4;
     int no_chain = 0;
     int paf_zero_copy = 1;
+    int count_paf = 0;                      // PF_OPT_COUNT_PAF: instrumented one-kernel parse
+    uint32_t *d_paf_touch = nullptr;        // [batch][touch_words] sampled-sector bitmaps
+    size_t touch_cap = 0, touch_used = 0;
     int conf_zero_copy = 0;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -252,12 +259,13 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
     } while (0)
 
 enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
-                kNmsUpWin, kNmsUpCorner, kCornerFinish, kCornerCrowded, kNmsUpScan, kParsePeaks, kScorePairs };
+                kNmsUpWin, kNmsUpCorner, kCornerFinish, kCornerCrowded, kNmsUpScan, kParsePeaks, kScorePairs,
+                kUpBlur };
 const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
                                           "k_resize_planes", "k_blur_rows", "k_blur_cols",
                                           "k_preprocess", "k_nms_up_win", "k_nms_up_corner",
                                           "k_corner_finish", "k_corner_crowded", "k_nms_up_scan",
-                                          "k_parse_peaks", "k_score_pairs"};
+                                          "k_parse_peaks", "k_score_pairs", "k_up_blur_nms"};
 
 cudaEvent_t take_event(pf_ctx *ctx)
 {
@@ -505,6 +513,16 @@ void make_taps(double sigma, BlurTaps &t)
     for (int k = 0; k <= 2 * r; ++k) t.w[k] /= sum;
 }
 
+// Blur on an upsampled grid with the 3x3 window: the fused k_up_blur_nms
+// (upsample -> blur -> NMS without full-resolution maps in HBM).
+bool fused_blur(const pf_ctx *ctx, const pf_params *p, int W)
+{
+    if (!(p->blur_sigma > 0.0) || p->upsample < 2 || p->nms_window != 3 || ctx->materialise) return false;
+    const int r = (int)std::ceil(3.0 * p->blur_sigma);
+    const int tw = up_blur_tile_width(W, r);
+    return tw >= 1 && up_blur_smem(tw, r) + 2048 <= (size_t)ctx->max_smem;   // + the static taps table
+}
+
 int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame_base,
               int h, int w, int stride, const pf_params *p, AxisCache *rows, AxisCache *cols,
               int pool_cap)
@@ -522,6 +540,16 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         KernelTimer kt(ctx, kNmsPlane);
         CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
                             ctx->d_counts, ctx->d_peaks, s));
+    } else if (fused_blur(ctx, p, W)) {
+        // fused upsample -> blur -> 3x3 NMS (nothing full-resolution in HBM)
+        UpBlurArgs a{};
+        a.conf = conf; a.B = n; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
+        a.rrec = rows->d_rec; a.crec = cols->d_rec;
+        make_taps(p->blur_sigma, a.taps);
+        a.thr = thr; a.cap = ctx->caps.max_peaks_per_part;
+        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+        KernelTimer kt(ctx, kUpBlur);
+        CU(launch_up_blur_nms(a, s));
     } else if (!blur && half == 1 && !ctx->materialise && !ctx->generic_fused && ctx->win_variant == 4 &&
                rows->canonical && cols->canonical && h + 1 <= 256 && w + 1 <= 256 &&
                (nms_up_corner_smem(h, w, h + 1, w + 1, kCornerStages) <= 100 * 1024 ||
@@ -551,7 +579,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
                 cudaFree(ctx->d_surv);
                 cudaFree(ctx->d_surv_n);
                 cudaFree(ctx->d_crowd);
-                ctx->d_surv = nullptr; ctx->d_surv_n = nullptr; ctx->d_crowd = nullptr; ctx->surv_planes = 0;
+                ctx->d_surv = nullptr; ctx->d_surv_n = nullptr; ctx->d_crowd = nullptr;
+                ctx->surv_planes = 0;
                 CU(dev_alloc(&ctx->d_surv, planes * corner_surv_entries_per_plane()));
                 CU(dev_alloc(&ctx->d_surv_n, planes));
                 CU(dev_alloc(&ctx->d_crowd, planes + 1));
@@ -692,7 +721,11 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     a.dbg_npeaks = ctx->d_dbg_np; a.dbg_peaks = ctx->d_dbg_peaks;
     a.dbg_nconns = ctx->d_dbg_nc; a.dbg_conn_i = ctx->d_dbg_ci; a.dbg_conn_d = ctx->d_dbg_cd;
     a.cand_spill = ctx->d_spill;
-    const bool psplit = ctx->parse_split == 2 || (ctx->parse_split == 1 && n >= kSplitMinFrames);
+    const bool psplit = !ctx->count_paf && (ctx->parse_split == 2 || (ctx->parse_split == 1 && n >= kSplitMinFrames));
+    if (ctx->count_paf && L > 0) {
+        a.paf_touch = ctx->d_paf_touch;
+        a.touch_words = (int)(((size_t)2 * L * h * w + 255) / 256);   // 8 floats per sector, 32 sectors per word
+    }
     if (psplit) {
         int rc = ensure_split_ws(ctx, (size_t)n);
         if (rc) return rc;
@@ -731,6 +764,24 @@ int check_call(pf_ctx *ctx, int batch, int grid_h, int grid_w, int stride, const
         return fail(ctx, PF_ERR_CONTRACT, "stride %d not divisible by upsample %d", stride, p->upsample);
     if ((long long)grid_h * p->upsample > 65535 || (long long)grid_w * p->upsample > 65535)
         return fail(ctx, PF_ERR_CONTRACT, "parse grid exceeds 65535 cells per axis");
+    return PF_OK;
+}
+
+// PF_OPT_COUNT_PAF: one zeroed sampled-sector bitmap per frame of the call.
+int prepare_paf_touch(pf_ctx *ctx, int batch, int h, int w)
+{
+    ctx->touch_used = 0;
+    if (!ctx->count_paf || ctx->topo.L == 0 || batch == 0) return PF_OK;
+    const size_t words = (size_t)batch * (((size_t)2 * ctx->topo.L * h * w + 255) / 256);
+    if (words > ctx->touch_cap) {
+        cudaFree(ctx->d_paf_touch);
+        ctx->d_paf_touch = nullptr;
+        ctx->touch_cap = 0;
+        CU(dev_alloc(&ctx->d_paf_touch, words));
+        ctx->touch_cap = words;
+    }
+    CU(cudaMemsetAsync(ctx->d_paf_touch, 0, words * sizeof(uint32_t), ctx->stream));
+    ctx->touch_used = words;
     return PF_OK;
 }
 
@@ -833,7 +884,7 @@ int prepare_axes(pf_ctx *ctx, int h, int w, const pf_params *p, AxisCache **rows
 int chunk_for(pf_ctx *ctx, const pf_params *p, int h, int w)
 {
     int chunk = ctx->caps.chunk_frames;
-    const bool materialise = p->blur_sigma > 0.0 ||
+    const bool materialise = (p->blur_sigma > 0.0 && !fused_blur(ctx, p, w * p->upsample)) ||
                              (p->upsample > 1 && (p->nms_window / 2 > kMaxFusedHalf || ctx->materialise));
     if (materialise) {
         // bound the full-resolution workspace ([chunk][K][H][W]) to ~2 GiB
@@ -913,7 +964,8 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
     ctx->max_smem = max_smem;
     if (cu(configure_nms_kernels(max_smem), "configure k_nms_up") ||
         cu(configure_corner_kernels(max_smem), "configure k_nms_up_corner") ||
-        cu(configure_parse_kernels(max_smem), "configure k_parse_frames"))
+        cu(configure_parse_kernels(max_smem), "configure k_parse_frames") ||
+        cu(configure_blur_kernels(max_smem), "configure k_up_blur_nms"))
         return bail(PF_ERR_CUDA);
     const size_t need = parse_smem_bytes(c.max_peaks_per_frame, c.max_peaks_per_part, c.max_candidates,
                                          c.max_humans_per_frame, PF_MAX_KEYPOINTS, PF_MAX_LIMBS,
@@ -935,7 +987,7 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp,
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
-                   ctx->d_corner_spill, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_pk_cell, ctx->d_pk_score,
+                   ctx->d_corner_spill, ctx->d_paf_touch, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_pk_cell, ctx->d_pk_score,
                    ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n,
                    ctx->d_owner};
     for (void *p : dev) cudaFree(p);
@@ -1039,6 +1091,8 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_CONF_ZERO_COPY: ctx->conf_zero_copy = value ? 1 : 0; return PF_OK;
     case PF_OPT_CORNER_SPLIT: ctx->corner_split = (value >= 0 && value <= 2) ? value : 1; return PF_OK;
     case PF_OPT_PARSE_SPLIT: ctx->parse_split = (value >= 0 && value <= 2) ? value : 1; return PF_OK;
+    case PF_OPT_PDL: g_pdl_mask = value; return PF_OK;
+    case PF_OPT_COUNT_PAF: ctx->count_paf = value ? 1 : 0; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }
@@ -1078,6 +1132,8 @@ int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch,
     const int K = ctx->topo.K, L = ctx->topo.L;
     const int pool = pool_cap_for(ctx, batch);
     rc = begin_call(ctx, batch, pool);
+    if (rc) return rc;
+    rc = prepare_paf_touch(ctx, batch, grid_h, grid_w);
     if (rc) return rc;
     ctx->last_batch = batch;
     ctx->last_K = K;
@@ -1192,6 +1248,8 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     const int pool = pool_cap_for(ctx, batch);
     rc = begin_call(ctx, batch, pool);
     if (rc) return rc;
+    rc = prepare_paf_touch(ctx, batch, grid_h, grid_w);
+    if (rc) return rc;
     ctx->last_batch = batch;
     ctx->last_K = K;
     ctx->last.kind = 2;
@@ -1272,6 +1330,23 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
         CU(cudaEventRecord(ctx->ev_free[sl], ctx->stream));
     }
     return out ? pf_get_results(ctx, out) : PF_OK;
+}
+
+int pf_get_paf_sectors(pf_ctx *ctx, long long *sectors)
+{
+    if (!ctx || !sectors) return PF_ERR_CONTRACT;
+    *sectors = 0;
+    if (!ctx->count_paf) return fail(ctx, PF_ERR_CONTRACT, "PF_OPT_COUNT_PAF is off");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->touch_used == 0) return PF_OK;
+    std::vector<uint32_t> bm(ctx->touch_used);
+    CU(cudaMemcpy(bm.data(), ctx->d_paf_touch, bm.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    long long n = 0;
+    for (uint32_t v : bm) n += __builtin_popcount(v);
+    *sectors = n;
+    return PF_OK;
 }
 
 int pf_sync(pf_ctx *ctx)

@@ -1192,7 +1192,7 @@ cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s)
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const long long need = (P * (kCornerSurv / kFinGroup) + kFinGroups - 1) / kFinGroups;
-    e = launch_pdl(k_corner_finish, dim3((unsigned)std::min<long long>(need, (long long)occ * sms)), dim3(kFinThreads),
+    e = launch_pdl(kPdlFinish, k_corner_finish, dim3((unsigned)std::min<long long>(need, (long long)occ * sms)), dim3(kFinThreads),
                    smem, s, a);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -1207,7 +1207,7 @@ cudaError_t launch_corner_crowded(const UpCornerArgs &a, cudaStream_t s)
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
     const size_t smem_c = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) + kCrowdCands * sizeof(uint32_t);
-    e = launch_pdl(k_corner_crowded, dim3((unsigned)std::min<long long>(P, (long long)sms * PF_CROWD_MINB)),
+    e = launch_pdl(kPdlCrowded, k_corner_crowded, dim3((unsigned)std::min<long long>(P, (long long)sms * PF_CROWD_MINB)),
                    dim3(kFinThreads),
                    smem_c, s, a);
     if (e != cudaSuccess) return e;

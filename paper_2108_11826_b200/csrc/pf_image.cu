@@ -168,8 +168,10 @@ k_resize_planes(const float *__restrict__ src, long long src_frame, int K, int h
     }
 }
 
-// Separable Gaussian (no reference; DESIGN.md §blur): taps k=-r..r, clamped
-// edges, fp64 accumulation in ascending k without FMA, rounded to fp32.
+// Separable Gaussian (no reference; DESIGN.md §5): taps k=-r..r, clamped
+// edges, fp64 fma chain in ascending k from 0.0, rounded to fp32 per pass.
+// The materialised form (Mode R blur, wide NMS windows); Mode U with the 3x3
+// window takes the fused k_up_blur_nms (pf_blur.cu).
 // Source and destination planes are addressed as (plane / K) * src_frame +
 // (plane % K) * HW so the blur can read part channels out of a [K+1]-channel
 // tensor.
@@ -190,7 +192,7 @@ k_blur_rows(const float *__restrict__ src, long long src_frame, float *__restric
         double acc = 0.0;
         for (int t = -taps.r; t <= taps.r; ++t) {
             const int xx = min(max(x + t, 0), W - 1);
-            acc = dadd(acc, dmul(taps.w[t + taps.r], (double)__ldg(s + xx)));
+            acc = __fma_rn(taps.w[t + taps.r], (double)__ldg(s + xx), acc);
         }
         dst[fb * dst_frame + (long long)k * HW + rem] = __double2float_rn(acc);
     }
@@ -212,7 +214,7 @@ k_blur_cols(const float *__restrict__ src, long long src_frame, float *__restric
         double acc = 0.0;
         for (int t = -taps.r; t <= taps.r; ++t) {
             const int yy = min(max(y + t, 0), H - 1);
-            acc = dadd(acc, dmul(taps.w[t + taps.r], (double)__ldg(s + (long long)yy * W)));
+            acc = __fma_rn(taps.w[t + taps.r], (double)__ldg(s + (long long)yy * W), acc);
         }
         dst[fb * dst_frame + (long long)k * HW + rem] = __double2float_rn(acc);
     }

@@ -16,8 +16,15 @@ namespace pf {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// PF_OPT_PDL: bit i allows programmatic dependent launch for launch site i
+// (process-wide; see kPdl*).  Measured on the C5 step: every edge on costs
+// 1.99 ms/step against 1.40 ms with none (the early-resident dependents slow
+// the running grid), so the default is 0.
+extern int g_pdl_mask;
+enum PdlSite { kPdlFinish = 0, kPdlCrowded, kPdlParsePeaks, kPdlPairScan, kPdlScorePairs, kPdlParseFrames };
+
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+inline cudaError_t launch_pdl(int site, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args)
 {
     cudaLaunchConfig_t cfg = {};
@@ -29,7 +36,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = (g_pdl_mask >> site) & 1;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 #endif
@@ -173,6 +180,10 @@ struct ParseArgs {
     int2 *ferr;          // [B] capacity error (what, value) from k_parse_peaks
     struct Cand *cand_g; // [B][cap_cands] gated candidates
     int *cand_n;         // [B]
+    // PF_OPT_COUNT_PAF: per-frame bitmaps of the 32-byte PAF sectors sampled
+    // (global frame index * touch_words), or null
+    uint32_t *paf_touch;
+    int touch_words;
 };
 #ifndef PF_CAND_SMEM
 #define PF_CAND_SMEM 256
@@ -219,6 +230,24 @@ cudaError_t launch_overlay(const OverlayPrim *prims, const int *prim_first, int 
 // pf_image.cu
 constexpr int kMaxBlurRadius = 64;
 struct BlurTaps { double w[2 * kMaxBlurRadius + 1]; int r; };
+
+// k_up_blur_nms (pf_blur.cu): x`up` upsample -> separable blur -> 3x3 NMS of
+// the K part planes, fused (nothing full-resolution in HBM).
+struct UpBlurArgs {
+    const float *conf;                   // low-res [B][C][h][w]
+    int B, C, K, h, w, H, W;
+    const AxisRec *rrec, *crec;          // per output row / column
+    BlurTaps taps;
+    float thr;
+    int cap;
+    int *counts;                         // [B*K], accumulated with atomics (zero on entry)
+    uint2 *peaks;                        // [B*K][cap]
+    int tw, tiles;                       // column tile width / tiles per plane (set by the launcher)
+};
+cudaError_t launch_up_blur_nms(const UpBlurArgs &a, cudaStream_t s);
+size_t up_blur_smem(int tw, int r);
+int up_blur_tile_width(int W, int r);
+cudaError_t configure_blur_kernels(int max_smem);
 cudaError_t launch_preprocess(const void *src, int src_is_f32, int B, int h, int w, float *dst,
                               int H, int W, const AxisRec *rrec, const AxisRec *crec, cudaStream_t s);
 cudaError_t launch_resize_planes(const float *src, long long src_frame, int K, long long P, int h, int w,

@@ -35,6 +35,10 @@
 namespace pf {
 
 constexpr int kParseTTab = 64;     // sample positions kept in shared memory
+#ifndef PF_PAR_ASM_MIN
+#define PF_PAR_ASM_MIN 96
+#endif
+constexpr int kParAsmMin = PF_PAR_ASM_MIN;   // accepted connections from which the assembly runs limb-parallel
 
 struct Cand {
     double score;
@@ -171,8 +175,19 @@ __device__ __forceinline__ double finish_sample(const ParseArgs &a, const Sample
 // order, so the fp64 running total is the reference's `total += d`; the pair
 // is left as soon as it can no longer pass (more failing samples than
 // max_fail = n - good_need).  True if gated (good >= good_min, score > 0).
+// COUNT: also mark, in this frame's bitmap (a.paf_touch), every 32-byte
+// sector of the PAF the sample reads — the instrumented pass that measures
+// the bytes an in-place (zero-copy) PAF moves over PCIe.
+__device__ __forceinline__ void touch_sector(uint32_t *bm, const float *base, const float *p)
+{
+    const size_t sec = (size_t)(p - base) >> 3;                  // 8 floats per 32-byte sector
+    atomicOr(bm + (sec >> 5), 1u << (sec & 31));
+}
+
+template <bool COUNT = false>
 __device__ __forceinline__ bool score_pair(const ParseArgs &a, const float *__restrict__ paf_f, int l, uint32_t ca,
-                                           uint32_t cbp, const double *t_tab, int max_fail, double &score, int &ngood)
+                                           uint32_t cbp, const double *t_tab, int max_fail, double &score, int &ngood,
+                                           uint32_t *touch = nullptr)
 {
     const int n = a.n_samples;
     const int ai = int(ca >> 16), aj = int(ca & 0xffff);
@@ -194,6 +209,22 @@ __device__ __forceinline__ bool score_pair(const ParseArgs &a, const float *__re
         const int cj = (int)floor(dadd(dadd((double)aj, dmul(t, (double)dj)), 0.5));
         SampleRaw r;
         fetch_sample(a, chx, chy, ci, cj, r);
+        if (COUNT) {
+            if (a.up == 1) {
+                touch_sector(touch, paf_f, chx + (size_t)ci * a.w + cj);
+                touch_sector(touch, paf_f, chy + (size_t)ci * a.w + cj);
+            } else {
+                const int4 ry = __ldg(reinterpret_cast<const int4 *>(a.rrec + ci));
+                const int4 rx = __ldg(reinterpret_cast<const int4 *>(a.crec + cj));
+                const int i0 = ry.x & 0xffff, i1 = ry.x >> 16, j0 = rx.x & 0xffff, j1 = rx.x >> 16;
+                for (const float *ch : {chx, chy}) {
+                    touch_sector(touch, paf_f, ch + (size_t)i0 * a.w + j0);
+                    touch_sector(touch, paf_f, ch + (size_t)i0 * a.w + j1);
+                    touch_sector(touch, paf_f, ch + (size_t)i1 * a.w + j0);
+                    touch_sector(touch, paf_f, ch + (size_t)i1 * a.w + j1);
+                }
+            }
+        }
         const double d = finish_sample(a, r, vx, vy);
         total = dadd(total, d);
         if (d >= a.dot_thr) ++ngood;
@@ -222,7 +253,7 @@ __device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
 // ranked by k_parse_peaks and pairs scored by k_score_pairs (all frames'
 // pairs spread over the whole GPU); this CTA takes the frame's gated
 // candidates from HBM and runs steps 4-7 (sort, greedy, assembly, scores).
-template <bool SPLIT>
+template <bool SPLIT, bool COUNT = false>
 __global__ void __launch_bounds__(SPLIT ? kParseFinThreads : kParseThreads, SPLIT ? PF_PARSE_FIN_MINB : PF_PARSE_MINB)
 k_parse_frames(const ParseArgs a)
 {
@@ -240,6 +271,7 @@ k_parse_frames(const ParseArgs a)
     __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base, s_nacc;
     __shared__ int s_wacc[(kParseThreads > kParseFinThreads ? kParseThreads : kParseFinThreads) / kWarp];
     __shared__ int s_lcnt[PF_MAX_LIMBS], s_lcur[PF_MAX_LIMBS];
+    __shared__ int s_aseg[PF_MAX_LIMBS + 1];    // accepted connections per limb, then their prefix
     // split: fewer candidates in shared memory and the peak table read from
     // the k_parse_peaks slab, so more frames stay resident per SM
     constexpr int CS = SPLIT ? kCandSmemSplit : kCandSmem;
@@ -382,7 +414,9 @@ k_parse_frames(const ParseArgs a)
             const int ib = s_base[pb_part] + (local - qa * nb);
             double score;
             int ngood;
-            if (!score_pair(a, paf_f, l, p_cell[ia], p_cell[ib], s_t, max_fail, score, ngood)) continue;
+            if (!score_pair<COUNT>(a, paf_f, l, p_cell[ia], p_cell[ib], s_t, max_fail, score, ngood,
+                                   COUNT ? a.paf_touch + (size_t)gframe * a.touch_words : nullptr))
+                continue;
             const int slot = atomicAdd(&s_ncand, 1);
             atomicAdd(&s_lcnt[l], 1);
             if (slot < a.cap_cands) {
@@ -501,6 +535,7 @@ k_parse_frames(const ParseArgs a)
         for (int l = tid; l < L; l += nthr) {
             uint32_t *used_a = used + l * 2 * pm_words, *used_b = used_a + pm_words;
             const int ba = s_base[s_la[l]], bb = s_base[s_lb[l]];
+            int acc = 0;
             for (int e = s_seg[l], e1 = s_seg[l + 1]; e < e1; ++e) {
                 Cand &c = cand_s[s_order[e]];
                 const uint32_t ab = c.ab;
@@ -510,12 +545,15 @@ k_parse_frames(const ParseArgs a)
                 used_a[ia >> 5] |= 1u << (ia & 31);
                 used_b[ib >> 5] |= 1u << (ib & 31);
                 c.ab = ab | kAccepted;
+                ++acc;
             }
+            s_aseg[l] = acc;
         }
     } else {                                                 // crowded: the bitonic-sorted store
         for (int l = tid; l < L; l += nthr) {
             uint32_t *used_a = used + l * 2 * pm_words, *used_b = used_a + pm_words;
             const int ba = s_base[s_la[l]], bb = s_base[s_lb[l]];
+            int acc = 0;
             for (int e = s_seg[l], e1 = s_seg[l + 1]; e < e1; ++e) {
                 Cand &c = cand[e];
                 const uint32_t ab = c.ab;
@@ -525,7 +563,9 @@ k_parse_frames(const ParseArgs a)
                 used_a[ia >> 5] |= 1u << (ia & 31);
                 used_b[ib >> 5] |= 1u << (ib & 31);
                 c.ab = ab | kAccepted;
+                ++acc;
             }
+            s_aseg[l] = acc;
         }
     }
     __syncthreads();
@@ -585,73 +625,171 @@ k_parse_frames(const ParseArgs a)
         if (tid == 0) s_nacc = kb;
         __syncthreads();
     }
-    if (tid == 0) {
-        int nh = 0, err = 0;
-        const int n_it = s_nacc;
-        // one replay step (the loop is specialised per record source so the
-        // usual path keeps its shared-memory loads)
-        auto step = [&](const ConnRec r) {
-            const int a_part = r.a_part, b_part = r.b_part, pa = r.pa, pb = r.pb;
-            const double cscore = r.score;
-            const int ha = owner[pa], hb = owner[pb];
-            if (ha < 0 && hb < 0) {                                  // paf.py:246-253
-                if (nh >= a.cap_humans) { err = 1; return; }
-                int16_t *parts = h_parts + nh * K;
-                for (int k = 0; k < K; ++k) parts[k] = -1;
-                parts[a_part] = int16_t(pa);
-                parts[b_part] = int16_t(pb);
-                h_order[nh * K + 0] = int8_t(a_part);
-                h_order[nh * K + 1] = int8_t(b_part);
-                h_n[nh] = 2;
-                h_mask[nh] = (1u << a_part) | (1u << b_part);
-                h_score[nh] = cscore;
-                h_alive[nh] = 1;
-                owner[pa] = int16_t(nh);
-                owner[pb] = int16_t(nh);
-                ++nh;
-            } else if (ha >= 0 && hb >= 0) {
-                if (ha == hb) {                                      // paf.py:255-256
-                    h_score[ha] = dadd(h_score[ha], cscore);
-                } else if ((h_mask[ha] & h_mask[hb]) == 0u) {        // paf.py:257-262
-                    const int nB = h_n[hb];
-                    int nA = h_n[ha];
-                    for (int q = 0; q < nB; ++q) {
-                        const int part = h_order[hb * K + q];
-                        const int pid = h_parts[hb * K + part];
-                        h_parts[ha * K + part] = int16_t(pid);
-                        h_order[ha * K + nA++] = int8_t(part);
-                        owner[pid] = int16_t(ha);
-                    }
-                    h_n[ha] = int8_t(nA);
-                    h_mask[ha] |= h_mask[hb];
-                    h_score[ha] = dadd(h_score[ha], dadd(h_score[hb], cscore));
-                    h_alive[hb] = 0;
-                }                                                    // else paf.py:263
-            } else {                                                 // paf.py:264-271
-                const int hidx = ha >= 0 ? ha : hb;
-                const int part = ha >= 0 ? b_part : a_part;
-                const int pid = ha >= 0 ? pb : pa;
-                // one round of independent loads, then the stores
-                const uint32_t m = h_mask[hidx];
-                const int nn = h_n[hidx];
-                const double hs = h_score[hidx];
-                if (!((m >> part) & 1u)) {
-                    h_parts[hidx * K + part] = int16_t(pid);
-                    h_order[hidx * K + nn] = int8_t(part);
-                    h_n[hidx] = int8_t(nn + 1);
-                    h_mask[hidx] = m | (1u << part);
-                    h_score[hidx] = dadd(hs, cscore);
-                    owner[pid] = int16_t(hidx);
+    // one replay step of paf.py:241-271 (shared by the serial replay and the
+    // serial fallback of a conflicting limb)
+    auto step = [&](const ConnRec r, int &nh, int &err) {
+        const int a_part = r.a_part, b_part = r.b_part, pa = r.pa, pb = r.pb;
+        const double cscore = r.score;
+        const int ha = owner[pa], hb = owner[pb];
+        if (ha < 0 && hb < 0) {                                  // paf.py:246-253
+            if (nh >= a.cap_humans) { err = 1; return; }
+            int16_t *parts = h_parts + nh * K;
+            for (int k = 0; k < K; ++k) parts[k] = -1;
+            parts[a_part] = int16_t(pa);
+            parts[b_part] = int16_t(pb);
+            h_order[nh * K + 0] = int8_t(a_part);
+            h_order[nh * K + 1] = int8_t(b_part);
+            h_n[nh] = 2;
+            h_mask[nh] = (1u << a_part) | (1u << b_part);
+            h_score[nh] = cscore;
+            h_alive[nh] = 1;
+            owner[pa] = int16_t(nh);
+            owner[pb] = int16_t(nh);
+            ++nh;
+        } else if (ha >= 0 && hb >= 0) {
+            if (ha == hb) {                                      // paf.py:255-256
+                h_score[ha] = dadd(h_score[ha], cscore);
+            } else if ((h_mask[ha] & h_mask[hb]) == 0u) {        // paf.py:257-262
+                const int nB = h_n[hb];
+                int nA = h_n[ha];
+                for (int q = 0; q < nB; ++q) {
+                    const int part = h_order[hb * K + q];
+                    const int pid = h_parts[hb * K + part];
+                    h_parts[ha * K + part] = int16_t(pid);
+                    h_order[ha * K + nA++] = int8_t(part);
+                    owner[pid] = int16_t(ha);
                 }
+                h_n[ha] = int8_t(nA);
+                h_mask[ha] |= h_mask[hb];
+                h_score[ha] = dadd(h_score[ha], dadd(h_score[hb], cscore));
+                h_alive[hb] = 0;
+            }                                                    // else paf.py:263
+        } else {                                                 // paf.py:264-271
+            const int hidx = ha >= 0 ? ha : hb;
+            const int part = ha >= 0 ? b_part : a_part;
+            const int pid = ha >= 0 ? pb : pa;
+            // one round of independent loads, then the stores
+            const uint32_t m = h_mask[hidx];
+            const int nn = h_n[hidx];
+            const double hs = h_score[hidx];
+            if (!((m >> part) & 1u)) {
+                h_parts[hidx * K + part] = int16_t(pid);
+                h_order[hidx * K + nn] = int8_t(part);
+                h_n[hidx] = int8_t(nn + 1);
+                h_mask[hidx] = m | (1u << part);
+                h_score[hidx] = dadd(hs, cscore);
+                owner[pid] = int16_t(hidx);
             }
-        };
-        if (fast) {
-            for (int e = 0; e < n_it && !err; ++e) step(conn[e]);
-        } else {
-            for (int e = 0; e < n_it && !err; ++e) step(*reinterpret_cast<const ConnRec *>(&cand[e]));
         }
-        s_nh = nh;
-        s_err = err;
+    };
+    auto rec = [&](int e) -> ConnRec {
+        return fast ? conn[e] : *reinterpret_cast<const ConnRec *>(&cand[e]);
+    };
+    const int n_it = s_nacc;
+    if (n_it < kParAsmMin) {
+        if (tid == 0) {
+            int nh = 0, err = 0;
+            if (fast) {
+                for (int e = 0; e < n_it && !err; ++e) step(conn[e], nh, err);
+            } else {
+                for (int e = 0; e < n_it && !err; ++e) step(*reinterpret_cast<const ConnRec *>(&cand[e]), nh, err);
+            }
+            s_nh = nh;
+            s_err = err;
+        }
+    } else {
+        // Limb-parallel replay (crowded frames).  Connections of one limb
+        // are a matching (distinct peaks), so two of them interact only if
+        // they touch the same human: when the humans they touch are pairwise
+        // distinct, every one's effect stays inside its own humans and peaks,
+        // new humans take their indices in acceptance order (a prefix sum)
+        // and the result equals the sequential replay.  A limb where two
+        // connections share a human is replayed serially.  h_pos counts the
+        // touches (it is free until step 7).
+        if (tid == 0) {
+            int acc = 0;
+            for (int l = 0; l < L; ++l) {
+                const int c = s_aseg[l];
+                s_aseg[l] = acc;
+                acc += c;
+            }
+            s_aseg[L] = acc;
+        }
+        for (int hh = tid; hh < a.cap_humans; hh += nthr) h_pos[hh] = 0;
+        __syncthreads();
+        int nh = 0, err = 0;
+        for (int l = 0; l < L && !err; ++l) {
+            const int e0 = s_aseg[l], m = s_aseg[l + 1] - e0;
+            if (m == 0) continue;
+            const int per = (m + nthr - 1) / nthr, i0 = tid * per;
+            int n_new = 0;
+            for (int j = 0; j < per && i0 + j < m; ++j) {
+                const ConnRec r = rec(e0 + i0 + j);
+                const int ha = owner[r.pa], hb = owner[r.pb];
+                if (ha >= 0) atomicAdd(&h_pos[ha], 1);
+                if (hb >= 0 && hb != ha) atomicAdd(&h_pos[hb], 1);
+                n_new += (ha < 0 && hb < 0) ? 1 : 0;
+            }
+            int incl = n_new;
+#pragma unroll
+            for (int d = 1; d < kWarp; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            if (lane == kWarp - 1) s_wacc[warp] = incl;
+            __syncthreads();
+            bool clash = false;
+            for (int j = 0; j < per && i0 + j < m; ++j) {
+                const ConnRec r = rec(e0 + i0 + j);
+                const int ha = owner[r.pa], hb = owner[r.pb];
+                clash |= (ha >= 0 && h_pos[ha] > 1) || (hb >= 0 && h_pos[hb] > 1);
+            }
+            int off = incl - n_new, tot = 0;
+            for (int w2 = 0; w2 < n_warps; ++w2) {
+                if (w2 < warp) off += s_wacc[w2];
+                tot += s_wacc[w2];
+            }
+            const bool any_clash = __syncthreads_or(clash);
+            // touches back to zero (nothing has moved yet: same owners)
+            for (int j = 0; j < per && i0 + j < m; ++j) {
+                const ConnRec r = rec(e0 + i0 + j);
+                const int ha = owner[r.pa], hb = owner[r.pb];
+                if (ha >= 0) h_pos[ha] = 0;
+                if (hb >= 0) h_pos[hb] = 0;
+            }
+            __syncthreads();
+            if (any_clash) {
+                if (tid == 0) {
+                    int nh0 = nh, e0r = 0;
+                    for (int e = e0; e < e0 + m && !e0r; ++e) step(rec(e), nh0, e0r);
+                    s_nh = nh0;
+                    s_err = e0r;
+                }
+                __syncthreads();
+                nh = s_nh;
+                err = s_err;
+                __syncthreads();
+                continue;
+            }
+            if (nh + tot > a.cap_humans) {                       // block-uniform
+                err = 1;
+                break;
+            }
+            int idx = nh + off;
+            for (int j = 0; j < per && i0 + j < m; ++j) {
+                const ConnRec r = rec(e0 + i0 + j);
+                const int ha = owner[r.pa], hb = owner[r.pb];
+                int nh_local = idx, e_local = 0;
+                step(r, nh_local, e_local);                      // touches only its own humans
+                idx += (ha < 0 && hb < 0) ? 1 : 0;
+            }
+            nh += tot;
+            __syncthreads();
+        }
+        if (tid == 0) {
+            s_nh = nh;
+            s_err = err;
+        }
     }
     __syncthreads();
     if (s_err) {
@@ -969,18 +1107,19 @@ size_t cand_spill_bytes_per_frame(int cap_cands)
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s)
 {
     if (B == 0) return cudaSuccess;
-    if (a.split) return launch_pdl(k_parse_frames<true>, dim3(B), dim3(threads), smem, s, a);
-    k_parse_frames<false><<<B, threads, smem, s>>>(a);
+    if (a.split) return launch_pdl(kPdlParseFrames, k_parse_frames<true>, dim3(B), dim3(threads), smem, s, a);
+    if (a.paf_touch) k_parse_frames<false, true><<<B, threads, smem, s>>>(a);
+    else k_parse_frames<false><<<B, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s)
 {
     if (B == 0) return cudaSuccess;
-    cudaError_t e = launch_pdl(k_parse_peaks, dim3((B + kPeakFrames - 1) / kPeakFrames), dim3(kPeakFrames * kWarp), 0,
+    cudaError_t e = launch_pdl(kPdlParsePeaks, k_parse_peaks, dim3((B + kPeakFrames - 1) / kPeakFrames), dim3(kPeakFrames * kWarp), 0,
                                s, a, B);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k_pair_scan, dim3(1), dim3(1024), 0, s, a, B);
+    return launch_pdl(kPdlPairScan, k_pair_scan, dim3(1), dim3(1024), 0, s, a, B);
 }
 
 cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s)
@@ -990,7 +1129,7 @@ cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s)
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k_score_pairs, dim3(sms * 8), dim3(kScoreThreads), 0, s, a, B);
+    return launch_pdl(kPdlScorePairs, k_score_pairs, dim3(sms * 8), dim3(kScoreThreads), 0, s, a, B);
 }
 
 cudaError_t configure_parse_kernels(int max_smem)
@@ -999,6 +1138,10 @@ cudaError_t configure_parse_kernels(int max_smem)
     cudaError_t e = cudaFuncGetAttributes(&fa, k_parse_frames<false>);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_parse_frames<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_frames<false, true>);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_parse_frames<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem - (int)fa.sharedSizeBytes);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_frames<true>);
     if (e == cudaSuccess)

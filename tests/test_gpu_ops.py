@@ -1,6 +1,7 @@
 """GPU pre-processing and resize kernels vs the reference fixtures and the
 oracle (bit-exact fp32 outputs of the fp64 bilinear formula)."""
 
+import collections
 import hashlib
 
 import numpy as np
@@ -106,7 +107,7 @@ def test_batched_postprocess_operator(topo):
         def __init__(self, items):
             self.items = list(items)
             self.out = []
-            self.batch_hist = {}
+            self.batch_hist = collections.Counter()
             self.busy = 0
 
         def recv(self, ch):
@@ -128,10 +129,7 @@ def test_batched_postprocess_operator(topo):
         def close(self):
             self.closed = True
 
-    import collections
-
     ctx, ch = Ctx(pkts), Ch()
-    ctx.batch_hist = collections.Counter()
     op.runner(ctx, None, ch)
     assert ch.closed and [p.seq_id for p in ctx.out] == list(range(5))
     assert dict(ctx.batch_hist) == {3: 1, 2: 1} and ctx.busy == 2      # batch_max 3: 3 + 2

@@ -175,3 +175,71 @@ def test_inputs_survive_capacity_replay(topo):
     del junk
     assert records(res, topo) == want
     eng.close()
+
+
+@pytest.mark.parametrize("sigma", [1.0, 2.0])
+def test_fused_blur_batch_vs_oracle_and_materialised(topo, sigma):
+    """k_up_blur_nms (upsample -> blur -> 3x3 NMS fused, split parse at 40
+    frames) against the oracle (bilinear_resize x8 -> blur_chw -> parse) on
+    every frame, and against the materialised path (k_resize_planes ->
+    k_blur_rows/cols -> k_nms_plane)."""
+    scenes = [synth.procedural_scene(61, s, 656, 368, SP) for s in range(38)] + \
+             [synth.crowd_scene(62, 0), synth.crowd_scene(62, 1)]
+    conf, paf = synth.render_batch(scenes, topo, SP)
+    params = pf.ParserParams(upsample=8, blur_sigma=sigma)
+    eng = pf.PafParser(topo)
+    res, launches = device_parse(eng, conf, paf, params)
+    assert launches.get("k_up_blur_nms", 0) >= 1, launches
+    got = records(res, topo)
+    taps = pf._native.gaussian_taps(sigma)
+
+    def one(f):
+        r = oracle.parse_upsampled(conf[f], paf[f], topo, params, 8, 8, taps)
+        return record_of(r.humans, topo, f)
+
+    with ThreadPoolExecutor(THREADS) as ex:
+        want = list(ex.map(one, range(conf.shape[0])))
+    assert got == want
+    eng.set_materialise(True)
+    mat, launches = device_parse(eng, conf, paf, params)
+    assert launches.get("k_blur_rows", 0) >= 1 and "k_up_blur_nms" not in launches, launches
+    assert records(mat, topo) == got
+    eng.close()
+
+
+def test_fused_blur_1080p_tiles(topo):
+    """1080x1920 output (8 column tiles per plane) with blur, vs the oracle."""
+    scenes = [synth.GroundTruthScene(synth.crowd_scene(91, s, 1920, 1080, 6, (300.0, 500.0)).humans, 1920, 1080)
+              for s in range(2)]
+    conf, paf = synth.render_batch(scenes, topo, SP)
+    params = pf.ParserParams(upsample=8, blur_sigma=1.5)
+    eng = pf.PafParser(topo)
+    res, launches = device_parse(eng, conf, paf, params)
+    assert launches.get("k_up_blur_nms", 0) >= 1, launches
+    taps = pf._native.gaussian_taps(1.5)
+    want = [record_of(oracle.parse_upsampled(conf[f], paf[f], topo, params, 8, 8, taps).humans, topo, f)
+            for f in range(2)]
+    assert records(res, topo) == want
+    eng.close()
+
+
+def test_paf_sector_count_instrumentation(topo):
+    """PF_OPT_COUNT_PAF (the bench's in-run count of the PAF bytes an in-place
+    PAF moves): same results as the uninstrumented call, deterministic, and
+    bounded by the frame's PAF sectors."""
+    scenes = [synth.procedural_scene(71, s, 656, 368, SP) for s in range(48)]
+    conf, paf = synth.render_batch(scenes, topo, SP)
+    params = pf.ParserParams(upsample=8)
+    eng = pf.PafParser(topo)
+    want = records(eng.parse_arrays(conf, paf, 8, params), topo)
+    eng.ctx.set_option(pf._native.PF_OPT_COUNT_PAF, 1)
+    got = records(eng.parse_arrays(conf, paf, 8, params), topo)
+    n1 = eng.ctx.paf_sectors()
+    eng.parse_arrays(conf, paf, 8, params)
+    n2 = eng.ctx.paf_sectors()
+    eng.ctx.set_option(pf._native.PF_OPT_COUNT_PAF, 0)
+    assert got == want
+    assert n1 == n2 and 0 < n1 <= 48 * paf[0].nbytes // 32
+    # every sampled pair touches at least 2 sectors (x and y channels)
+    assert n1 * 32 / 48 > 1000
+    eng.close()
