@@ -537,34 +537,38 @@ int orc_parse(const float *conf, const float *paf, int K, int L,
 
 /* ------------------------------------------------------------------ */
 /* Separable Gaussian (no reference; DESIGN.md §5 defines it): horizontal then
- * vertical, clamped edges, acc = fma(w_k, v, acc) in fp64 from 0.0 in ascending
- * k, each pass rounded to fp32.  C99 fma() is correctly rounded. */
+ * vertical, clamped edges, acc = fmaf(w_k, v, acc) in fp32 from 0.0f in
+ * ascending k with w_k = (float)taps[k] (the fp64-normalised taps rounded to
+ * nearest).  C99 fmaf() is correctly rounded. */
 int orc_blur_chw(float *maps, int C, int h, int w, const double *taps, int r)
 {
     if (r <= 0) return 0;
     float *tmp = malloc(sizeof(float) * (size_t)h * w);
-    if (!tmp) return 4;
+    float *tf = malloc(sizeof(float) * (size_t)(2 * r + 1));
+    if (!tmp || !tf) { free(tmp); free(tf); return 4; }
+    for (int k = 0; k <= 2 * r; ++k) tf[k] = (float)taps[k];
     for (int c = 0; c < C; ++c) {
         float *m = maps + (size_t)c * h * w;
         for (int y = 0; y < h; ++y)
             for (int x = 0; x < w; ++x) {
-                double acc = 0.0;
+                float acc = 0.0f;
                 for (int k = -r; k <= r; ++k) {
                     int xx = x + k < 0 ? 0 : (x + k > w - 1 ? w - 1 : x + k);
-                    acc = fma(taps[k + r], (double)m[(size_t)y * w + xx], acc);
+                    acc = fmaf(tf[k + r], m[(size_t)y * w + xx], acc);
                 }
-                tmp[(size_t)y * w + x] = (float)acc;
+                tmp[(size_t)y * w + x] = acc;
             }
         for (int y = 0; y < h; ++y)
             for (int x = 0; x < w; ++x) {
-                double acc = 0.0;
+                float acc = 0.0f;
                 for (int k = -r; k <= r; ++k) {
                     int yy = y + k < 0 ? 0 : (y + k > h - 1 ? h - 1 : y + k);
-                    acc = fma(taps[k + r], (double)tmp[(size_t)yy * w + x], acc);
+                    acc = fmaf(tf[k + r], tmp[(size_t)yy * w + x], acc);
                 }
-                m[(size_t)y * w + x] = (float)acc;
+                m[(size_t)y * w + x] = acc;
             }
     }
+    free(tf);
     free(tmp);
     return 0;
 }

@@ -545,6 +545,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         UpBlurArgs a{};
         a.conf = conf; a.B = n; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
         a.rrec = rows->d_rec; a.crec = cols->d_rec;
+        a.up = up;
         make_taps(p->blur_sigma, a.taps);
         a.thr = thr; a.cap = ctx->caps.max_peaks_per_part;
         a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;

@@ -169,7 +169,7 @@ k_resize_planes(const float *__restrict__ src, long long src_frame, int K, int h
 }
 
 // Separable Gaussian (no reference): taps k=-r..r, clamped
-// edges, fp64 fma chain in ascending k from 0.0, rounded to fp32 per pass.
+// edges, fp32 fma chain in ascending k from 0.0f with w_k = (float)taps[k].
 // The materialised form (Mode R blur, wide NMS windows); Mode U with the 3x3
 // window takes the fused k_up_blur_nms (pf_blur.cu).
 // Source and destination planes are addressed as (plane / K) * src_frame +
@@ -189,12 +189,12 @@ k_blur_rows(const float *__restrict__ src, long long src_frame, float *__restric
         const long long fb = plane / K;
         const int k = int(plane - fb * K);
         const float *s = src + fb * src_frame + (long long)k * HW + (long long)y * W;
-        double acc = 0.0;
+        float acc = 0.0f;
         for (int t = -taps.r; t <= taps.r; ++t) {
             const int xx = min(max(x + t, 0), W - 1);
-            acc = __fma_rn(taps.w[t + taps.r], (double)__ldg(s + xx), acc);
+            acc = __fmaf_rn((float)taps.w[t + taps.r], __ldg(s + xx), acc);
         }
-        dst[fb * dst_frame + (long long)k * HW + rem] = __double2float_rn(acc);
+        dst[fb * dst_frame + (long long)k * HW + rem] = acc;
     }
 }
 
@@ -211,12 +211,12 @@ k_blur_cols(const float *__restrict__ src, long long src_frame, float *__restric
         const long long fb = plane / K;
         const int k = int(plane - fb * K);
         const float *s = src + fb * src_frame + (long long)k * HW + x;
-        double acc = 0.0;
+        float acc = 0.0f;
         for (int t = -taps.r; t <= taps.r; ++t) {
             const int yy = min(max(y + t, 0), H - 1);
-            acc = __fma_rn(taps.w[t + taps.r], (double)__ldg(s + (long long)yy * W), acc);
+            acc = __fmaf_rn((float)taps.w[t + taps.r], __ldg(s + (long long)yy * W), acc);
         }
-        dst[fb * dst_frame + (long long)k * HW + rem] = __double2float_rn(acc);
+        dst[fb * dst_frame + (long long)k * HW + rem] = acc;
     }
 }
 

@@ -243,6 +243,8 @@ struct UpBlurArgs {
     int *counts;                         // [B*K], accumulated with atomics (zero on entry)
     uint2 *peaks;                        // [B*K][cap]
     int tw, tiles;                       // column tile width / tiles per plane (set by the launcher)
+    int up;                              // upsample factor (source rows per tile)
+    int th, tiles_y, tiles_x;            // k_up_blur_tile: block rows, blocks per plane (set by the launcher)
 };
 cudaError_t launch_up_blur_nms(const UpBlurArgs &a, cudaStream_t s);
 size_t up_blur_smem(int tw, int r);

@@ -202,6 +202,74 @@ def test_corner_kernel_overflow_and_nonfinite(eng, topo):
         assert_batch_matches(eng, topo, conf, paf, pf.ParserParams(upsample=up))
 
 
+def test_blur_fused_kernels_vs_materialised(topo):
+    """The fused upsample -> blur -> NMS kernels (2-D tiles for radius <= 8,
+    the row kernel beyond) against the materialised path (resize -> blur
+    rows / cols -> NMS over HBM maps) on 24 frames per sigma — peaks and
+    records identical — and against the oracle on two of them."""
+    scenes = [synth.procedural_scene(41, s, 656, 368, SP) for s in range(24)]
+    conf, paf = render(scenes, topo)
+    e = pf.PafParser(topo, debug=True)
+    for sigma in (0.5, 1.0, 2.5, 3.0):
+        params = pf.ParserParams(upsample=8, blur_sigma=sigma)
+        e.ctx.set_option(pf._native.PF_OPT_MATERIALISE, 0)
+        e.set_timing(True)
+        e.kernel_times(reset=True)
+        got = e.parse_arrays(conf, paf, 8, params)
+        assert "k_up_blur_nms" in e.kernel_times(reset=True)
+        e.set_timing(False)
+        fused = [pf.pose_record(f, got.poses(f), topo) for f in range(len(scenes))]
+        peaks = [e.peaks(f) for f in range(len(scenes))]
+        e.ctx.set_option(pf._native.PF_OPT_MATERIALISE, 1)
+        got = e.parse_arrays(conf, paf, 8, params)
+        assert [e.peaks(f) for f in range(len(scenes))] == peaks, sigma
+        assert [pf.pose_record(f, got.poses(f), topo) for f in range(len(scenes))] == fused, sigma
+        for f in (0, 17):
+            want = oracle_run(conf[f], paf[f], topo, params)
+            assert peaks[f] == want.peaks, (sigma, f)
+            assert fused[f] == record_of(want.humans, topo, f), (sigma, f)
+    e.close()
+
+
+def test_blur_cold_block_skip_edges(topo):
+    """k_up_blur_tile skips blocks whose sources all lie in [0, thr (1 - 2^-10)):
+    maps built around that bound (just below / at / above it, plateaus at the
+    threshold, negative values, NaN) give the same peaks as the materialised
+    path, which skips nothing."""
+    rng = np.random.default_rng(5)
+    thr = 0.1
+    x = np.float32(thr) - np.float32(thr) * np.float32(2.0 ** -10)
+    F, K, h, w = 6, topo.n_keypoints, 46, 82
+    conf = np.zeros((F, K + 1, h, w), np.float32)
+    base = [np.float32(x) * np.float32(0.999), np.nextafter(np.float32(x), np.float32(0)), np.float32(x),
+            np.float32(thr), np.nextafter(np.float32(thr), np.float32(1))]
+    for f in range(F):
+        for k in range(K):
+            v = base[(f + k) % len(base)]
+            m = np.full((h, w), v, np.float32) * rng.uniform(0.97, 1.0, (h, w)).astype(np.float32)
+            if (f + k) % 3 == 0:
+                m[rng.integers(0, h), rng.integers(0, w)] = np.float32(thr) * 1.5      # one hot spot
+            if (f + k) % 4 == 1:
+                m[rng.integers(0, h), rng.integers(0, w)] = -0.5
+            if (f + k) % 7 == 2:
+                m[rng.integers(0, h), rng.integers(0, w)] = np.nan
+            if (f + k) % 5 == 3:
+                m[:] = np.float32(thr)                                               # plateau at thr
+            conf[f, k] = m
+    paf = np.zeros((F, 2 * topo.n_limbs, h, w), np.float32)
+    e = pf.PafParser(topo, debug=True)
+    for sigma in (1.0, 2.0):
+        params = pf.ParserParams(upsample=8, blur_sigma=sigma)
+        e.ctx.set_option(pf._native.PF_OPT_MATERIALISE, 0)
+        e.parse_arrays(conf, paf, 8, params)
+        fused = [e.peaks(f) for f in range(F)]
+        e.ctx.set_option(pf._native.PF_OPT_MATERIALISE, 1)
+        e.parse_arrays(conf, paf, 8, params)
+        assert [e.peaks(f) for f in range(F)] == fused, sigma
+        assert sum(len(p) for p in fused) > 0
+    e.close()
+
+
 def test_blur_paths(eng, topo):
     scenes = [synth.procedural_scene(29, s, 656, 368, SP) for s in range(2)]
     conf, paf = render(scenes, topo)

@@ -1,5 +1,6 @@
 """Minimal C5 driver for ncu captures: 8192 GPU-rendered frames, Mode U,
 `steps` parse calls (argv[1], default 3) on device-resident maps."""
+import os
 import sys
 
 import torch
@@ -14,6 +15,9 @@ sp = synth.SynthParams()
 scenes = [synth.procedural_scene(5, s, 656, 368, sp) for s in range(8192)]
 conf, paf = synth.render_batch_gpu(scenes, topo, sp)
 eng = pf.PafParser(topo)
+for kv in filter(None, os.environ.get("PF_OPTS", "").split(",")):   # e.g. PF_OPTS=14=0
+    k, v = kv.split("=")
+    eng.ctx.set_option(int(k), int(v))
 params = pf.ParserParams(upsample=8)
 for _ in range(steps):
     eng.parse_tensors(conf, paf, 8, params)
