@@ -159,6 +159,7 @@ struct pf_ctx {
     uint32_t *d_pk_cell = nullptr;          // split parse staging (ensure_split_ws)
     float *d_pk_score = nullptr;
     int *d_pk_base = nullptr, *d_pair_pp = nullptr, *d_npairs = nullptr, *d_cand_n = nullptr;
+    int *d_crowd_frames = nullptr;          // split parse: crowded frame list [split_frames] + its count
     long long *d_pair_base = nullptr;       // [frames + 1]: prefix, then the total
     int2 *d_ferr = nullptr;
     unsigned *d_owner = nullptr;            // overlay: draw-order owner per pixel
@@ -388,10 +389,11 @@ int ensure_split_ws(pf_ctx *ctx, size_t frames)
     if (frames <= ctx->split_frames && ctx->split_cap_frame == ctx->caps.max_peaks_per_frame) return PF_OK;
     const size_t f = frames > ctx->split_frames ? frames : ctx->split_frames;
     void *old[] = {ctx->d_pk_cell, ctx->d_pk_score, ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs,
-                   ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n};
+                   ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n, ctx->d_crowd_frames};
     for (void *q : old) cudaFree(q);
     ctx->d_pk_cell = nullptr; ctx->d_pk_score = nullptr; ctx->d_pk_base = nullptr; ctx->d_pair_pp = nullptr;
     ctx->d_npairs = nullptr; ctx->d_pair_base = nullptr; ctx->d_ferr = nullptr; ctx->d_cand_n = nullptr;
+    ctx->d_crowd_frames = nullptr;
     ctx->split_frames = 0;
     const size_t cf = (size_t)ctx->caps.max_peaks_per_frame;
     CU(dev_alloc(&ctx->d_pk_cell, f * cf));
@@ -402,6 +404,7 @@ int ensure_split_ws(pf_ctx *ctx, size_t frames)
     CU(dev_alloc(&ctx->d_pair_base, f + 1));         // + the pair total
     CU(dev_alloc(&ctx->d_ferr, f));
     CU(dev_alloc(&ctx->d_cand_n, f));
+    CU(dev_alloc(&ctx->d_crowd_frames, f + 1));
     ctx->split_frames = f;
     ctx->split_cap_frame = ctx->caps.max_peaks_per_frame;
     return PF_OK;
@@ -566,6 +569,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.rband = rows->d_bands; a.cband = cols->d_bands;
         a.rdt = rows->d_band_dt; a.cdt = cols->d_band_dt;
         a.nbr = (int)rows->bands.size(); a.nbc = (int)cols->bands.size();
+        a.max_band = std::max(rows->max_band, cols->max_band);
         a.nst = kCornerStages;
         a.chain = rows->min_step >= 0.03125 && cols->min_step >= 0.03125 && !ctx->no_chain;
         a.rrec = rows->d_rec; a.crec = cols->d_rec;
@@ -735,6 +739,9 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.pair_pp = ctx->d_pair_pp; a.n_pairs = ctx->d_npairs; a.pair_base = ctx->d_pair_base;
         a.pair_total = ctx->d_pair_base + ctx->split_frames;
         a.ferr = ctx->d_ferr; a.cand_n = ctx->d_cand_n;
+        a.crowd_frames = ctx->d_crowd_frames;
+        a.crowd_cap = (int)ctx->split_frames;
+        CU(cudaMemsetAsync(ctx->d_crowd_frames + ctx->split_frames, 0, sizeof(int), ctx->stream));
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }
     const int threads = psplit ? kParseFinThreads : kParseThreads;
@@ -989,7 +996,7 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_status, ctx->d_full, ctx->d_tmp,
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
                    ctx->d_corner_spill, ctx->d_paf_touch, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_pk_cell, ctx->d_pk_score,
-                   ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n,
+                   ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n, ctx->d_crowd_frames,
                    ctx->d_owner};
     for (void *p : dev) cudaFree(p);
     for (float *p : ctx->d_in) cudaFree(p);

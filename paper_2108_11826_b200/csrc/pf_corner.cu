@@ -1098,27 +1098,94 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
     }
 }
 
-// Crowded planes of the split path (more than kScanCrowd survivors, or the
-// survivor list overflowed): k_nms_up_scan appends them to a compact list;
-// here a whole CTA takes one such plane — survivors (from the list, or from a
-// walk of the hot cells when the list overflowed) classified across all
-// threads, candidates collected in shared memory and tested lane by lane.
+// Crowded planes of the split path (more than kScanCrowd survivors): the
+// scan appends them to a compact list; here a whole CTA takes one such plane
+// and redoes it from a shared-memory copy of the plane (when it fits):
+//   1. hot words (ballots) and the hot-cell list;
+//   2. thread per hot cell: chain pre-filter, classification; a normal cell
+//      pushes its surviving corners (exact test from the list, or on the spot
+//      when the list is full), a partial cell goes to the dense list;
+//   3. candidates: the exact 3x3 test, thread per candidate;
+//   4. dense cells, warp per cell: the exact values of the cell and its
+//      one-pixel ring are computed once into a per-warp buffer and EVERY
+//      pixel of the cell is tested from it (a superset of partial_cands'
+//      candidates; an exact test never passes a non-peak and each pixel
+//      belongs to one cell, so the peaks are the same, without duplicates).
+// Crowded scenes make most hot cells non-monotone ("partial"), where testing
+// pixel by pixel would cost nine interpolations per pixel.
 constexpr int kCrowdCands = 2048;
+constexpr int kCrowdList = 4096;     // hot cells per plane in shared memory
+constexpr int kCrowdDense = 1024;    // partial cells per plane in shared memory
+constexpr int kCrowdWarps = kFinThreads / kWarp;
+
+struct CrowdLayout {
+    size_t rb, cb, rt, ct, plane, hot, list, cand, dense, vbuf, total;
+    int vcap;            // floats per warp buffer
+    bool staged;         // the plane is copied into shared memory
+};
+
+__host__ __device__ inline CrowdLayout crowd_layout(int h, int w, int nbr, int nbc, int max_band, size_t budget)
+{
+    CrowdLayout L;
+    L.vcap = (max_band + 2) * (max_band + 2);
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 15) & ~(size_t)15; return at; };
+    L.rb = take((size_t)nbr * sizeof(int4));
+    L.cb = take((size_t)nbc * sizeof(int4));
+    L.rt = take((size_t)nbr * sizeof(BandT));
+    L.ct = take((size_t)nbc * sizeof(BandT));
+    L.hot = take((size_t)(h + 2) * ((w + 31) >> 5) * sizeof(uint32_t));
+    L.list = take((size_t)kCrowdList * sizeof(uint32_t));
+    L.cand = take((size_t)kCrowdCands * sizeof(uint32_t));
+    L.dense = take((size_t)kCrowdDense * sizeof(uint32_t));
+    L.vbuf = take((size_t)kCrowdWarps * L.vcap * sizeof(float));
+    L.plane = o;
+    L.staged = o + (size_t)h * w * sizeof(float) + 16 <= budget;
+    if (L.staged) take((size_t)h * w * sizeof(float));
+    L.total = o;
+    return L;
+}
+
+// Candidate sink of the crowded kernel: the shared list, or the exact test
+// on the spot once it is full.
+struct CrowdSink {
+    const UpCornerArgs *a;
+    const float *S;
+    uint32_t *c;
+    int *n;
+    int *npk;
+    int plane;
+    __device__ void operator()(int y, int x) const
+    {
+        const int slot = atomicAdd(n, 1);
+        if (slot < kCrowdCands) {
+            c[slot] = (uint32_t(y) << 16) | uint32_t(x);
+        } else {
+            float v;
+            if (exact_peak_all(*a, S, y, x, v)) emit_peak_c(npk, a->peaks, plane, a->cap, v, y, x);
+        }
+    }
+};
 
 #ifndef PF_CROWD_MINB
-#define PF_CROWD_MINB 6   // C3 Mode U: 1.27 ms (3 CTAs/SM), 1.14 (4), 1.08 (6), 1.07 (8, more spills)
+#define PF_CROWD_MINB 3
 #endif
 __global__ void __launch_bounds__(kFinThreads, PF_CROWD_MINB)
-k_corner_crowded(const __grid_constant__ UpCornerArgs a)
+k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
 {
     extern __shared__ __align__(16) unsigned char smf[];
-    const int nbr = a.nbr, nbc = a.nbc;
-    int4 *RB = reinterpret_cast<int4 *>(smf);
-    int4 *CB = RB + nbr;
-    BandT *RT = reinterpret_cast<BandT *>(CB + nbc);
-    BandT *CT = RT + nbr;
-    uint32_t *cand = reinterpret_cast<uint32_t *>(CT + nbc);
-    __shared__ int n_cand, n_pk;
+    const int nbr = a.nbr, nbc = a.nbc, h = a.h, w = a.w, hw = h * w;
+    int4 *RB = reinterpret_cast<int4 *>(smf + L.rb);
+    int4 *CB = reinterpret_cast<int4 *>(smf + L.cb);
+    BandT *RT = reinterpret_cast<BandT *>(smf + L.rt);
+    BandT *CT = reinterpret_cast<BandT *>(smf + L.ct);
+    uint32_t *hot = reinterpret_cast<uint32_t *>(smf + L.hot);
+    uint32_t *list = reinterpret_cast<uint32_t *>(smf + L.list);
+    uint32_t *cand = reinterpret_cast<uint32_t *>(smf + L.cand);
+    uint32_t *dense = reinterpret_cast<uint32_t *>(smf + L.dense);
+    float *vbuf = reinterpret_cast<float *>(smf + L.vbuf);
+    float *Sp = reinterpret_cast<float *>(smf + L.plane);
+    __shared__ int n_hot, n_cand, n_dense, n_pk;
     pdl_trigger();
     pdl_wait();                                          // the crowd list and the finished planes' counts
     const int nlist = min(*a.crowd_n, a.B * a.K);
@@ -1128,54 +1195,125 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a)
         else fill_band(a.cols, a.cdt, a.cband, b - nbr, CB[b - nbr], CT[b - nbr]);
     }
     const Bands bd{RB, CB, RT, CT};
-    const CandList cl{cand, &n_cand, kCrowdCands, nullptr, 0};
+    const int nws = (w + 31) >> 5, nwc = (w + 32) >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < nws; e += kFinThreads) {
+        hot[e] = 0u;                                     // guard rows -1 and h
+        hot[(h + 1) * nws + e] = 0u;
+    }
+    float *vb = vbuf + warp * L.vcap;
     for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
         const int plane = __ldcg(a.crowd_list + li);
-        if (threadIdx.x == 0) { n_cand = 0; n_pk = 0; }
-        __syncthreads();
+        if (threadIdx.x == 0) { n_hot = 0; n_cand = 0; n_dense = 0; n_pk = 0; }
         const int fb = plane / a.K, k = plane - fb * a.K;
-        const float *S = a.conf + ((size_t)fb * a.C + k) * (size_t)a.h * a.w;
-        const int ns = __ldcg(a.surv_n + plane) & 0x3fffffff;     // survivors found by k_nms_up_scan
-        const bool listed = ns <= kCornerSurv;
-        const uint32_t *sv = a.surv_out + (size_t)plane * kCornerSurv;
-        const int nwc = (nbc + 31) >> 5;
-        // pass 0: candidates into shared memory; pass 1 (overflow): inline tests
-        for (int pass = 0; pass < 2; ++pass) {
-            if (listed) {
-                for (int i = threadIdx.x; i < ns; i += kFinThreads) {
-                    const uint32_t cell = __ldcg(sv + i);
-                    if (pass == 0) process_cell(a, bd, cl, S, plane, int(cell >> 16), int(cell & 0xffffu));
-                    else classify_inline(a, bd, S, plane, &n_pk, int(cell >> 16), int(cell & 0xffffu));
-                }
-            } else {
-                for (int t = threadIdx.x; t < nbr * 32 * nwc; t += kFinThreads) {
-                    const int pj = t >> 5, bit = t & 31;
-                    const int p = pj / nwc, j = pj - p * nwc, q = (j << 5) + bit;
-                    if (q >= nbc) continue;
-                    const CellF c = cellf(S, a.w, bd.rb[p], bd.cb[q]);
-                    if (!(c.a0 >= a.thr || c.a1 >= a.thr || c.b0 >= a.thr || c.b1 >= a.thr)) continue;
-                    if (a.chain && chain_pruned(S, a.w, nbr, nbc, p, q)) continue;
-                    if (pass == 0) process_cell(a, bd, cl, S, plane, p, q);
-                    else classify_inline(a, bd, S, plane, &n_pk, p, q);
-                }
+        const float *G = a.conf + ((size_t)fb * a.C + k) * (size_t)hw;
+        const float *S = G;
+        if (L.staged) {
+            for (int e = threadIdx.x; e < hw; e += kFinThreads) Sp[e] = __ldg(G + e);
+            S = Sp;
+        }
+        __syncthreads();
+        // 1. hot words (warp per source row, one ballot per 32 columns), hot cells
+        for (int r = warp; r < h; r += kCrowdWarps) {
+            for (int j = 0; j < nws; ++j) {
+                const int c = (j << 5) + lane;
+                const uint32_t word = __ballot_sync(0xffffffffu, c < w && S[r * w + c] >= a.thr);
+                if (lane == 0) hot[(r + 1) * nws + j] = word;
             }
-            __syncthreads();
-            if (pass == 0) {
-                const int nc = n_cand;
-                if (nc <= kCrowdCands) {
-                    for (int ci = threadIdx.x; ci < nc; ci += kFinThreads) {
-                        const uint32_t yx = cand[ci];
-                        const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
-                        float v;
-                        if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk, a.peaks, plane, a.cap, v, y, x);
-                    }
-                    break;                                 // CTA-uniform
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nbr * nwc; t += kFinThreads) {
+            const int p = t / nwc, j = t - p * nwc;
+            uint32_t c = cell_word(hot, nws, p, j);
+            if (c) {
+                int slot = atomicAdd(&n_hot, __popc(c));
+                while (c) {
+                    const int q = (j << 5) + __ffs(c) - 1;
+                    c &= c - 1u;
+                    if (slot < kCrowdList) list[slot] = (uint32_t(p) << 16) | uint32_t(q);
+                    ++slot;
                 }
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0) a.counts[plane] = n_pk;
+        // 2. thread per hot cell: prune, classify, corners -> candidates,
+        // partial cells -> dense list
+        const CrowdSink sink{&a, S, cand, &n_cand, &n_pk, plane};
+        auto cell_work = [&](int p, int q) {
+            if (a.chain && chain_pruned(S, w, nbr, nbc, p, q)) return;
+            const int4 rb = bd.rb[p], cb = bd.cb[q];
+            unsigned corners;
+            const unsigned ok = classify_cell(bd, S, w, nbr, nbc, p, q, rb, cb, corners);
+            if (ok == 3u) {
+                while (corners) {
+                    const int bit = __ffs(corners) - 1;
+                    corners &= corners - 1u;
+                    const int i = bit >> 1, j = bit & 1;
+                    if (i == 1 && rb.x == rb.y) continue;
+                    if (j == 1 && cb.x == cb.y) continue;
+                    if (!corner_cross_ok(bd, S, w, i ? p - 1 : p, j ? q - 1 : q, i, j)) continue;
+                    sink(i ? rb.x : rb.y, j ? cb.x : cb.y);
+                }
+            } else if ((rb.y - rb.x + 3) * (cb.y - cb.x + 3) <= L.vcap) {
+                const int slot = atomicAdd(&n_dense, 1);
+                if (slot < kCrowdDense) dense[slot] = (uint32_t(p) << 16) | uint32_t(q);
+                else partial_cands(a, bd, sink, S, plane, p, q, ok);
+            } else {
+                partial_cands(a, bd, sink, S, plane, p, q, ok);
+            }
+        };
+        const int nh = n_hot;
+        if (nh <= kCrowdList) {
+            for (int i = threadIdx.x; i < nh; i += kFinThreads) {
+                const uint32_t pq = list[i];
+                cell_work(int(pq >> 16), int(pq & 0xffffu));
+            }
+        } else {
+            for (int t = threadIdx.x; t < nbr * nwc; t += kFinThreads) {
+                const int p = t / nwc, j = t - p * nwc;
+                uint32_t c = cell_word(hot, nws, p, j);
+                while (c) {
+                    const int q = (j << 5) + __ffs(c) - 1;
+                    c &= c - 1u;
+                    cell_work(p, q);
+                }
+            }
+        }
         __syncthreads();
+        // 3. candidates of normal cells
+        const int nc = min(n_cand, kCrowdCands);
+        for (int ci = threadIdx.x; ci < nc; ci += kFinThreads) {
+            const uint32_t yx = cand[ci];
+            const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
+            float v;
+            if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk, a.peaks, plane, a.cap, v, y, x);
+        }
+        // 4. dense cells, warp per cell
+        const int nd = min(n_dense, kCrowdDense);
+        for (int di = warp; di < nd; di += kCrowdWarps) {
+            const uint32_t pq = dense[di];
+            const int4 rb = bd.rb[int(pq >> 16)], cb = bd.cb[int(pq & 0xffffu)];
+            const int y0 = rb.x - 1, x0 = cb.x - 1;
+            const int bh = rb.y - rb.x + 3, bw = cb.y - cb.x + 3;
+            for (int e = lane; e < bh * bw; e += kWarp) {
+                const int yy = e / bw, xx = e - yy * bw;
+                vb[e] = exact_value(a, S, y0 + yy, x0 + xx);          // -inf off the grid
+            }
+            __syncwarp();
+            const int ch = bh - 2, cw = bw - 2;
+            for (int e = lane; e < ch * cw; e += kWarp) {
+                const int yy = e / cw + 1, xx = e - (yy - 1) * cw + 1;
+                const float *c = vb + yy * bw + xx;
+                const float v = c[0];
+                // paf.py:95-99: earlier neighbours strictly, later ones non-strictly
+                if (v >= a.thr && v > c[-bw - 1] && v > c[-bw] && v > c[-bw + 1] && v > c[-1] && v >= c[1] &&
+                    v >= c[bw - 1] && v >= c[bw] && v >= c[bw + 1])
+                    emit_peak_c(&n_pk, a.peaks, plane, a.cap, v, y0 + yy, x0 + xx);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) a.counts[plane] = n_pk;
     }
 }
 
@@ -1202,14 +1340,17 @@ cudaError_t launch_corner_crowded(const UpCornerArgs &a, cudaStream_t s)
 {
     const long long P = (long long)a.B * a.K;
     if (P == 0) return cudaSuccess;
-    int dev = 0, sms = 0;
+    int dev = 0, sms = 0, max_smem = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
-    const size_t smem_c = (size_t)(a.nbr + a.nbc) * (sizeof(int4) + sizeof(BandT)) + kCrowdCands * sizeof(uint32_t);
+    // stage the plane when PF_CROWD_MINB CTAs per SM still fit, else read it through L1
+    const size_t per_cta = (size_t)(228 * 1024) / PF_CROWD_MINB - 1024 - 256;
+    const CrowdLayout L = crowd_layout(a.h, a.w, a.nbr, a.nbc, a.max_band,
+                                       std::min(per_cta, (size_t)max_smem - 256));
     e = launch_pdl(kPdlCrowded, k_corner_crowded, dim3((unsigned)std::min<long long>(P, (long long)sms * PF_CROWD_MINB)),
-                   dim3(kFinThreads),
-                   smem_c, s, a);
+                   dim3(kFinThreads), L.total, s, a, L);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -105,6 +105,7 @@ struct UpCornerArgs {
     const int4 *rband, *cband;           // bands: (first, last, src0, src1)
     const double *rdt, *cdt;             // per band: min t step between adjacent outputs
     int nbr, nbc;                        // band counts (h + 1, w + 1)
+    int max_band;                        // widest band (outputs) of either axis
     int nst;                             // plane stages in shared memory
     int bulk;                            // set by the launcher: planes fetched by cp.async.bulk
     int chain;                           // chain pre-filter allowed (output t steps >= 2^-5)
@@ -184,6 +185,10 @@ struct ParseArgs {
     // (global frame index * touch_words), or null
     uint32_t *paf_touch;
     int touch_words;
+    // split parse: frames whose candidates exceed kCandSmemSplit, finished by
+    // k_parse_crowd ([crowd_cap] list + count at crowd_frames[crowd_cap]), or null
+    int *crowd_frames;
+    int crowd_cap;
 };
 #ifndef PF_CAND_SMEM
 #define PF_CAND_SMEM 256
@@ -201,11 +206,17 @@ constexpr int kParseThreads = PF_PARSE_THREADS;   // k_parse_frames CTA size
 #define PF_PARSE_FIN_THREADS 64
 #endif
 constexpr int kParseFinThreads = PF_PARSE_FIN_THREADS;   // k_parse_frames<true> (split finish) CTA size
+constexpr int kParseCrowdThreads = 512;                  // k_parse_crowd (crowded frames of the split parse)
+#ifndef PF_CAND_SMEM_CROWD
+#define PF_CAND_SMEM_CROWD 4096
+#endif
+constexpr int kCandSmemCrowd = PF_CAND_SMEM_CROWD;       // candidates in shared memory per crowded frame
+constexpr int kParseMaxThreads = kParseCrowdThreads > kParseThreads ? kParseCrowdThreads : kParseThreads;
 size_t cand_spill_bytes_per_frame(int cap_cands);
 size_t cand_record_bytes();
 enum { kCapPart = 1, kCapFrame = 2, kCapCands = 3, kCapHumans = 4, kCapPool = 5 };
 size_t parse_smem_bytes(int cap_frame, int cap_part, int cap_cands, int cap_humans, int K, int L, int n_warps,
-                        bool split);
+                        bool split, bool crowd = false);
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s);
 cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s);    // k_parse_peaks + k_pair_scan
 cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s);

@@ -253,28 +253,31 @@ __device__ __forceinline__ void neumaier_add(double &f, double &c, double v)
 // ranked by k_parse_peaks and pairs scored by k_score_pairs (all frames'
 // pairs spread over the whole GPU); this CTA takes the frame's gated
 // candidates from HBM and runs steps 4-7 (sort, greedy, assembly, scores).
-template <bool SPLIT, bool COUNT = false>
-__global__ void __launch_bounds__(SPLIT ? kParseFinThreads : kParseThreads, SPLIT ? PF_PARSE_FIN_MINB : PF_PARSE_MINB)
-k_parse_frames(const ParseArgs a)
+// CROWD (split only): a frame whose gated candidates exceed the 64-thread
+// CTA's shared store (kCandSmemSplit) is listed by k_parse_frames<true> and
+// finished here instead — 512 threads, kCandSmemCrowd candidates and their
+// connection records in shared memory — so crowded frames (C3: ~2k
+// candidates) rank per limb in shared memory instead of a bitonic sort
+// through L2 by 64 threads.
+template <bool SPLIT, bool COUNT, bool CROWD>
+__device__ __forceinline__ void parse_frame(const ParseArgs &a, const int b)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int K = a.topo.K, L = a.topo.L;
-    const int b = blockIdx.x;
     const int gframe = a.frame_base + b;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    pdl_wait();                                          // peaks / candidates of the previous kernels
     const int warp = tid / kWarp, lane = tid % kWarp, n_warps = nthr / kWarp;
 
     __shared__ int s_base[PF_MAX_KEYPOINTS + 1];
     __shared__ int s_pp[PF_MAX_LIMBS + 1];      // pair prefix per limb
     __shared__ int s_seg[PF_MAX_LIMBS + 1];     // candidate segment start per limb
     __shared__ int s_err, s_errval, s_ncand, s_nh, s_pool_base, s_nacc;
-    __shared__ int s_wacc[(kParseThreads > kParseFinThreads ? kParseThreads : kParseFinThreads) / kWarp];
+    __shared__ int s_wacc[kParseMaxThreads / kWarp];
     __shared__ int s_lcnt[PF_MAX_LIMBS], s_lcur[PF_MAX_LIMBS];
     __shared__ int s_aseg[PF_MAX_LIMBS + 1];    // accepted connections per limb, then their prefix
     // split: fewer candidates in shared memory and the peak table read from
     // the k_parse_peaks slab, so more frames stay resident per SM
-    constexpr int CS = SPLIT ? kCandSmemSplit : kCandSmem;
+    constexpr int CS = CROWD ? kCandSmemCrowd : (SPLIT ? kCandSmemSplit : kCandSmem);
     __shared__ uint16_t s_bucket[CS], s_order[CS];   // by limb; sorted within limb
     __shared__ int8_t s_la[PF_MAX_LIMBS], s_lb[PF_MAX_LIMBS];
     __shared__ int16_t s_cx[PF_MAX_LIMBS], s_cy[PF_MAX_LIMBS];
@@ -319,6 +322,7 @@ k_parse_frames(const ParseArgs a)
         if (tid == 0) {
             const int2 e = a.ferr[b];
             s_err = e.x; s_errval = e.y;
+            s_ncand = __ldcg(a.cand_n + b);
         }
     } else if (tid < K) {
         const int c = a.counts[(size_t)b * K + tid];
@@ -345,6 +349,10 @@ k_parse_frames(const ParseArgs a)
             a.frame_count[gframe] = 0;
             if (a.debug) { a.dbg_npeaks[gframe] = 0; a.dbg_nconns[gframe] = 0; }
         }
+        return;
+    }
+    if (SPLIT && !CROWD && a.crowd_frames && s_ncand > CS) {   // block-uniform: k_parse_crowd finishes it
+        if (tid == 0) a.crowd_frames[atomicAdd(a.crowd_frames + a.crowd_cap, 1)] = b;
         return;
     }
     const int P = s_base[K];
@@ -882,6 +890,25 @@ k_parse_frames(const ParseArgs a)
     }
 }
 
+template <bool SPLIT, bool COUNT = false>
+__global__ void __launch_bounds__(SPLIT ? kParseFinThreads : kParseThreads, SPLIT ? PF_PARSE_FIN_MINB : PF_PARSE_MINB)
+k_parse_frames(const ParseArgs a)
+{
+    pdl_wait();                                          // peaks / candidates of the previous kernels
+    parse_frame<SPLIT, COUNT, false>(a, blockIdx.x);
+}
+
+// Crowded frames listed by k_parse_frames<true> (persistent over the list).
+__global__ void __launch_bounds__(kParseCrowdThreads, 1)
+k_parse_crowd(const ParseArgs a)
+{
+    const int n = __ldcg(a.crowd_frames + a.crowd_cap);
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        parse_frame<true, false, true>(a, __ldcg(a.crowd_frames + i));
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Split parse (PF_OPT_PARSE_SPLIT): the per-frame CTA no longer carries the
 // gather-bound line integral.
@@ -1080,11 +1107,12 @@ k_score_pairs(const ParseArgs a, int B)
 }
 
 size_t parse_smem_bytes(int cap_frame, int cap_part, int cap_cands, int cap_humans, int K, int L, int n_warps,
-                        bool split)
+                        bool split, bool crowd)
 {
     (void)cap_cands;
     const int pm_words = (cap_part + 31) / 32;
-    size_t s = (size_t)(split ? kCandSmemSplit : kCandSmem) * sizeof(Cand);
+    const int cs = crowd ? kCandSmemCrowd : (split ? kCandSmemSplit : kCandSmem);
+    size_t s = (size_t)cs * sizeof(Cand);
     s += (size_t)cap_humans * sizeof(double);
     if (!split) s += (size_t)cap_frame * (sizeof(uint32_t) + sizeof(float));
     s += (size_t)cap_humans * (sizeof(uint32_t) + sizeof(int));
@@ -1093,7 +1121,7 @@ size_t parse_smem_bytes(int cap_frame, int cap_part, int cap_cands, int cap_huma
     s += (size_t)cap_humans * K * (sizeof(int16_t) + sizeof(int8_t));
     s += (size_t)cap_humans * 2;
     s = (s + 15) & ~size_t(15);
-    s += (size_t)(split ? kCandSmemSplit : kCandSmem) * sizeof(ConnRec);
+    s += (size_t)cs * sizeof(ConnRec);
     return (s + 15) & ~size_t(15);
 }
 
@@ -1107,7 +1135,19 @@ size_t cand_spill_bytes_per_frame(int cap_cands)
 cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t smem, cudaStream_t s)
 {
     if (B == 0) return cudaSuccess;
-    if (a.split) return launch_pdl(kPdlParseFrames, k_parse_frames<true>, dim3(B), dim3(threads), smem, s, a);
+    if (a.split) {
+        cudaError_t e = launch_pdl(kPdlParseFrames, k_parse_frames<true>, dim3(B), dim3(threads), smem, s, a);
+        if (e != cudaSuccess || !a.crowd_frames) return e;
+        // crowded frames (listed by k_parse_frames<true>): one CTA per SM
+        int dev = 0, sms = 0;
+        e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        const size_t smem_c = parse_smem_bytes(a.cap_frame, a.cap_part, a.cap_cands, a.cap_humans, a.topo.K,
+                                               a.topo.L, kParseCrowdThreads / kWarp, true, true);
+        k_parse_crowd<<<std::min(B, sms), kParseCrowdThreads, smem_c, s>>>(a);
+        return cudaGetLastError();
+    }
     if (a.paf_touch) k_parse_frames<false, true><<<B, threads, smem, s>>>(a);
     else k_parse_frames<false><<<B, threads, smem, s>>>(a);
     return cudaGetLastError();
@@ -1146,6 +1186,10 @@ cudaError_t configure_parse_kernels(int max_smem)
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_frames<true>);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_parse_frames<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_crowd);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_parse_crowd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem - (int)fa.sharedSizeBytes);
     return e;
 }

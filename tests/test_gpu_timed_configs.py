@@ -243,3 +243,38 @@ def test_paf_sector_count_instrumentation(topo):
     # every sampled pair touches at least 2 sectors (x and y channels)
     assert n1 * 32 / 48 > 1000
     eng.close()
+
+
+@pytest.mark.parametrize("grid, patch", [((46, 82), 30), ((135, 240), 72)])
+def test_crowded_plane_kernel_stress(topo, grid, patch):
+    """k_corner_crowded on adversarial planes — uniform noise patches above
+    the threshold (hundreds to thousands of hot cells, most of them
+    non-monotone, hot-list / dense-list overflow on the 135x240 grid, which
+    is also too large to stage in shared memory) and ties from quantised
+    noise — against the materialised path (resize + plane NMS over HBM maps)
+    through the default split path (32 frames)."""
+    rng = np.random.default_rng(grid[0] + patch)
+    F, K = 32, topo.n_keypoints
+    h, w = grid
+    conf = np.zeros((F, K + 1, h, w), np.float32)
+    for f in range(3):
+        for k in (0, 5, 11):
+            y0, x0 = rng.integers(0, h - patch), rng.integers(0, w - patch)
+            m = rng.random((patch, patch)).astype(np.float32)
+            if k == 5:
+                m = np.round(m * 4) / 4                  # plateaus and ties
+            conf[f, k, y0:y0 + patch, x0:x0 + patch] = m
+    paf = np.zeros((F, 2 * topo.n_limbs, h, w), np.float32)
+    e = pf.PafParser(topo, debug=True)
+    params = pf.ParserParams(upsample=8)
+    e.set_timing(True)
+    e.kernel_times(reset=True)
+    e.parse_arrays(conf, paf, 8, params)
+    kt = e.kernel_times(reset=True)
+    assert "k_nms_up_scan" in kt and "k_corner_crowded" in kt, kt
+    split = [e.peaks(f) for f in range(F)]
+    e.ctx.set_option(pf._native.PF_OPT_MATERIALISE, 1)
+    e.parse_arrays(conf, paf, 8, params)
+    assert [e.peaks(f) for f in range(F)] == split
+    assert sum(len(p) for p in split) > 1000
+    e.close()
