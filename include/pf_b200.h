@@ -173,6 +173,9 @@ int pf_set_debug(pf_ctx *ctx, int enable);
                                     (process-wide A/B; default 0 = measured fastest) */
 #define PF_OPT_COUNT_PAF 13       /* instrumented parse: count the 32-byte PAF sectors the line integral
                                     reads (one-kernel parse; read with pf_get_paf_sectors) */
+#define PF_OPT_LARGE 15           /* 1: parse through the large-frame kernel (HBM tables, 32-bit ids), the
+                                    path the context switches to by itself when a frame outgrows the
+                                    shared-memory capacities (more than 32767 peaks, ...); 0: usual path */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* With PF_OPT_COUNT_PAF on: distinct 32-byte PAF sectors the last parse call
@@ -182,7 +185,7 @@ int pf_get_paf_sectors(pf_ctx *ctx, long long *sectors);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch
  * counts accumulated since the last reset; ids index pf_kernel_name(). */
-#define PF_N_KERNELS 15
+#define PF_N_KERNELS 16
 const char *pf_kernel_name(int id);
 int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset);
 int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,

@@ -30,7 +30,8 @@ PF_OPT_PARSE_SPLIT = 10
 PF_OPT_CONF_ZERO_COPY = 11
 PF_OPT_PDL = 12
 PF_OPT_COUNT_PAF = 13
-PF_N_KERNELS = 15
+PF_OPT_LARGE = 15
+PF_N_KERNELS = 16
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (

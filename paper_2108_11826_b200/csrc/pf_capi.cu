@@ -212,6 +212,13 @@ struct pf_ctx {
     int no_chain = 0;
     int paf_zero_copy = 1;
     int count_paf = 0;                      // PF_OPT_COUNT_PAF: instrumented one-kernel parse
+    int large = 0;                          // parse through k_parse_large (set when a capacity outgrows
+                                            // shared memory, or PF_OPT_LARGE)
+    LargeWs lws{};                          // its per-frame workspace
+    size_t lws_frames = 0;
+    int large_auto = 0;                     // switched by grow_cap (per call: the next call starts on
+    pf_caps caps_usual{};                   //   the usual path again, with these caps)
+    int replaying = 0;
     uint32_t *d_paf_touch = nullptr;        // [batch][touch_words] sampled-sector bitmaps
     size_t touch_cap = 0, touch_used = 0;
     int conf_zero_copy = 0;
@@ -261,12 +268,13 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
 
 enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
                 kNmsUpWin, kNmsUpCorner, kCornerFinish, kCornerCrowded, kNmsUpScan, kParsePeaks, kScorePairs,
-                kUpBlur };
+                kUpBlur, kParseLarge };
 const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
                                           "k_resize_planes", "k_blur_rows", "k_blur_cols",
                                           "k_preprocess", "k_nms_up_win", "k_nms_up_corner",
                                           "k_corner_finish", "k_corner_crowded", "k_nms_up_scan",
-                                          "k_parse_peaks", "k_score_pairs", "k_up_blur_nms"};
+                                          "k_parse_peaks", "k_score_pairs", "k_up_blur_nms",
+                                          "k_parse_large"};
 
 cudaEvent_t take_event(pf_ctx *ctx)
 {
@@ -407,6 +415,51 @@ int ensure_split_ws(pf_ctx *ctx, size_t frames)
     CU(dev_alloc(&ctx->d_crowd_frames, f + 1));
     ctx->split_frames = f;
     ctx->split_cap_frame = ctx->caps.max_peaks_per_frame;
+    return PF_OK;
+}
+
+// Per-frame HBM workspace of k_parse_large, sized by the current caps.
+size_t large_bytes_per_frame(const pf_ctx *ctx)
+{
+    const pf_caps &c = ctx->caps;
+    const size_t K = (size_t)ctx->topo.K, L = (size_t)ctx->topo.L;
+    const size_t pw = ((size_t)c.max_peaks_per_part + 31) / 32;
+    return (size_t)c.max_peaks_per_frame * 12 + (size_t)c.max_candidates * large_cand_bytes() + L * 2 * pw * 4 +
+           (size_t)c.max_humans_per_frame * (K * 5 + 2 + 4 + 8 + 4);
+}
+
+int ensure_large_ws(pf_ctx *ctx, size_t frames)
+{
+    LargeWs &w = ctx->lws;
+    const pf_caps &c = ctx->caps;
+    const int pw = (c.max_peaks_per_part + 31) / 32;
+    if (frames <= ctx->lws_frames && w.cap_peaks == c.max_peaks_per_frame && w.cap_cands == c.max_candidates &&
+        w.cap_humans == c.max_humans_per_frame && w.part_words == pw)
+        return PF_OK;
+    void *old[] = {w.pk_cell, w.pk_score, w.owner, w.cand, w.used, w.h_parts, w.h_order, w.h_n, w.h_alive,
+                   w.h_mask, w.h_score, w.h_pos};
+    for (void *q : old) cudaFree(q);
+    w = LargeWs{};
+    ctx->lws_frames = 0;
+    const size_t f = frames, K = (size_t)ctx->topo.K;
+    w.cap_peaks = c.max_peaks_per_frame;
+    w.cap_cands = c.max_candidates;
+    w.cap_humans = c.max_humans_per_frame;
+    w.part_words = pw;
+    w.used_words = ctx->topo.L * 2 * pw;
+    CU(dev_alloc(&w.pk_cell, f * w.cap_peaks));
+    CU(dev_alloc(&w.pk_score, f * w.cap_peaks));
+    CU(dev_alloc(&w.owner, f * w.cap_peaks));
+    CU(dev_alloc(reinterpret_cast<char **>(&w.cand), f * w.cap_cands * large_cand_bytes()));
+    CU(dev_alloc(&w.used, f * (size_t)w.used_words));
+    CU(dev_alloc(&w.h_parts, f * w.cap_humans * K));
+    CU(dev_alloc(&w.h_order, f * w.cap_humans * K));
+    CU(dev_alloc(&w.h_n, f * w.cap_humans));
+    CU(dev_alloc(&w.h_alive, f * w.cap_humans));
+    CU(dev_alloc(&w.h_mask, f * w.cap_humans));
+    CU(dev_alloc(&w.h_score, f * w.cap_humans));
+    CU(dev_alloc(&w.h_pos, f * w.cap_humans));
+    ctx->lws_frames = f;
     return PF_OK;
 }
 
@@ -726,6 +779,13 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     a.dbg_npeaks = ctx->d_dbg_np; a.dbg_peaks = ctx->d_dbg_peaks;
     a.dbg_nconns = ctx->d_dbg_nc; a.dbg_conn_i = ctx->d_dbg_ci; a.dbg_conn_d = ctx->d_dbg_cd;
     a.cand_spill = ctx->d_spill;
+    if (ctx->large) {                                // frames past the shared-memory capacities
+        int rc = ensure_large_ws(ctx, (size_t)n);
+        if (rc) return rc;
+        KernelTimer kt(ctx, kParseLarge);
+        CU(launch_parse_large(a, ctx->lws, n, s));
+        return PF_OK;
+    }
     const bool psplit = !ctx->count_paf && (ctx->parse_split == 2 || (ctx->parse_split == 1 && n >= kSplitMinFrames));
     if (ctx->count_paf && L > 0) {
         a.paf_touch = ctx->d_paf_touch;
@@ -828,6 +888,9 @@ bool grow_cap(pf_ctx *ctx, const Status &st)
     if (!((ctx->auto_caps >> st.what) & 1)) return false;
     pf_caps c = ctx->caps;
     const long long need = st.value > 0 ? st.value : 1;
+    // shared-memory / 16-bit bound limits of k_parse_frames; past them the
+    // context parses through k_parse_large (HBM workspace, 32-bit indices)
+    bool large = ctx->large != 0;
     switch (st.what) {
     case kCapPool:
         if ((long long)st.pool_used <= ctx->pool_need) return false;
@@ -836,45 +899,61 @@ bool grow_cap(pf_ctx *ctx, const Status &st)
     case kCapPart: {
         long long v = c.max_peaks_per_part;
         while (v < need) v *= 2;
-        c.max_peaks_per_part = (int)(v > (1 << 20) ? (1 << 20) : v);
+        if (v > (1 << 20)) return false;
+        c.max_peaks_per_part = (int)v;
         if (c.max_peaks_per_part > c.max_peaks_per_frame && ((ctx->auto_caps >> kCapFrame) & 1))
-            c.max_peaks_per_frame = c.max_peaks_per_part < 32767 ? c.max_peaks_per_part : 32767;
+            c.max_peaks_per_frame = c.max_peaks_per_part;
         break;
     }
     case kCapCands: {
         long long v = c.max_candidates;
         while (v < need) v *= 2;
-        if (v > (1 << 24)) return false;
+        if (v > (1 << 26)) return false;
         c.max_candidates = (int)v;
         break;
     }
     case kCapFrame: {
         long long v = c.max_peaks_per_frame;
         while (v < need) v *= 2;
-        if (v > 32767) v = 32767;
-        if (v < need) return false;
+        if (v > (1 << 26)) return false;
         c.max_peaks_per_frame = (int)v;
         break;
     }
     case kCapHumans: {
         long long v = c.max_humans_per_frame * 2LL;
-        if (v > 32767) return false;
+        if (v > (1 << 24)) return false;
         c.max_humans_per_frame = (int)v;
         break;
     }
     default:
         return false;
     }
+    if (c.max_peaks_per_frame > 32767 || c.max_humans_per_frame > 32767 || c.max_candidates > (1 << 24)) large = true;
     const size_t smem = parse_smem_bytes(c.max_peaks_per_frame, c.max_peaks_per_part, c.max_candidates,
                                          c.max_humans_per_frame, PF_MAX_KEYPOINTS, PF_MAX_LIMBS,
                                          std::max(kParseThreads, kParseFinThreads) / 32, false) + 2048;
-    if (smem > (size_t)ctx->max_smem) return false;
+    if (smem > (size_t)ctx->max_smem) large = true;
     if (c.max_peaks_per_part == ctx->caps.max_peaks_per_part && c.max_candidates == ctx->caps.max_candidates &&
         c.max_peaks_per_frame == ctx->caps.max_peaks_per_frame &&
-        c.max_humans_per_frame == ctx->caps.max_humans_per_frame)
+        c.max_humans_per_frame == ctx->caps.max_humans_per_frame && large == (ctx->large != 0))
         return false;
+    if (large && !ctx->large) {
+        ctx->large_auto = 1;
+        ctx->caps_usual = ctx->caps;
+    }
     ctx->caps = c;
+    ctx->large = large ? 1 : 0;
     return true;
+}
+
+// A new call (not a capacity replay) after an automatic switch to the
+// large-frame path starts on the usual path again.
+void reset_large(pf_ctx *ctx)
+{
+    if (ctx->replaying || !ctx->large_auto) return;
+    ctx->caps = ctx->caps_usual;
+    ctx->large = 0;
+    ctx->large_auto = 0;
 }
 
 int prepare_axes(pf_ctx *ctx, int h, int w, const pf_params *p, AxisCache **rows, AxisCache **cols)
@@ -901,6 +980,13 @@ int chunk_for(pf_ctx *ctx, const pf_params *p, int h, int w)
         if (lim < 1) lim = 1;
         if ((size_t)chunk > lim) chunk = (int)lim;
     }
+    // bound the per-frame parse workspace (NMS slab, candidate lists, and
+    // k_parse_large's tables) to ~4 GiB per chunk
+    size_t per = (size_t)ctx->topo.K * ctx->caps.max_peaks_per_part * 8 +
+                 (size_t)ctx->caps.max_candidates * cand_record_bytes();
+    if (ctx->large) per += large_bytes_per_frame(ctx);
+    const size_t lim = std::max<size_t>(1, ((size_t)4 << 30) / std::max<size_t>(per, 1));
+    if ((size_t)chunk > lim) chunk = (int)lim;
     return chunk;
 }
 
@@ -929,9 +1015,9 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
     int pc = 1;
     while (pc < c.max_candidates) pc <<= 1;
     c.max_candidates = pc;
-    if (c.max_peaks_per_frame > 32767)
-        return fail(nullptr, PF_ERR_CONFIG, "max_peaks_per_frame must be <= 32767");
-    if (c.max_humans_per_frame > 32767) return fail(nullptr, PF_ERR_CONFIG, "max_humans_per_frame > 32767");
+    if (c.max_peaks_per_frame > (1 << 26)) return fail(nullptr, PF_ERR_CONFIG, "max_peaks_per_frame > 2^26");
+    if (c.max_humans_per_frame > (1 << 24)) return fail(nullptr, PF_ERR_CONFIG, "max_humans_per_frame > 2^24");
+    if (c.max_candidates > (1 << 26)) return fail(nullptr, PF_ERR_CONFIG, "max_candidates > 2^26");
     pf_ctx *ctx = new pf_ctx();
     ctx->device = device;
     ctx->caps = c;
@@ -970,6 +1056,15 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
         return bail(PF_ERR_CUDA);
     const int max_smem = prop.sharedMemPerBlockOptin;
     ctx->max_smem = max_smem;
+    {
+        // explicit caps past k_parse_frames' shared-memory bounds: large path from the start
+        const pf_caps &cc = ctx->caps;
+        if (cc.max_peaks_per_frame > 32767 || cc.max_humans_per_frame > 32767 || cc.max_candidates > (1 << 24) ||
+            parse_smem_bytes(cc.max_peaks_per_frame, cc.max_peaks_per_part, cc.max_candidates, cc.max_humans_per_frame,
+                             PF_MAX_KEYPOINTS, PF_MAX_LIMBS, std::max(kParseThreads, kParseFinThreads) / 32, false) +
+                    2048 > (size_t)max_smem)
+            ctx->large = 1;
+    }
     if (cu(configure_nms_kernels(max_smem), "configure k_nms_up") ||
         cu(configure_corner_kernels(max_smem), "configure k_nms_up_corner") ||
         cu(configure_parse_kernels(max_smem), "configure k_parse_frames") ||
@@ -999,6 +1094,12 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n, ctx->d_crowd_frames,
                    ctx->d_owner};
     for (void *p : dev) cudaFree(p);
+    {
+        LargeWs &w = ctx->lws;
+        void *lw[] = {w.pk_cell, w.pk_score, w.owner, w.cand, w.used, w.h_parts, w.h_order, w.h_n, w.h_alive,
+                      w.h_mask, w.h_score, w.h_pos};
+        for (void *p : lw) cudaFree(p);
+    }
     for (float *p : ctx->d_in) cudaFree(p);
     void *host[] = {ctx->h_frame_first, ctx->h_frame_count, ctx->h_hscore, ctx->h_hnparts,
                     ctx->h_kpx, ctx->h_kpy, ctx->h_kps, ctx->h_kpp, ctx->h_status};
@@ -1101,6 +1202,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_PARSE_SPLIT: ctx->parse_split = (value >= 0 && value <= 2) ? value : 1; return PF_OK;
     case PF_OPT_PDL: g_pdl_mask = value; return PF_OK;
     case PF_OPT_COUNT_PAF: ctx->count_paf = value ? 1 : 0; return PF_OK;
+    case PF_OPT_LARGE: ctx->large = value ? 1 : 0; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }
@@ -1137,6 +1239,7 @@ int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch,
     if (rc) return rc;
     rc = set_device(ctx);
     if (rc) return rc;
+    reset_large(ctx);
     const int K = ctx->topo.K, L = ctx->topo.L;
     const int pool = pool_cap_for(ctx, batch);
     rc = begin_call(ctx, batch, pool);
@@ -1200,8 +1303,10 @@ int pf_get_results(pf_ctx *ctx, pf_results *out)
             // grown to the need and the call is replayed (inputs must stay
             // valid until results are fetched)
             const auto L = ctx->last;
+            ctx->replaying = 1;
             rc = L.kind == 1 ? pf_parse_device(ctx, L.conf, L.paf, L.batch, L.h, L.w, L.stride, &L.p)
                              : pf_parse_host(ctx, L.conf, L.paf, L.batch, L.h, L.w, L.stride, &L.p, nullptr);
+            ctx->replaying = 0;
             if (rc) return rc;
             return pf_get_results(ctx, out);
         }
@@ -1246,6 +1351,7 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     if (rc) return rc;
     rc = set_device(ctx);
     if (rc) return rc;
+    reset_large(ctx);
     const int K = ctx->topo.K, L = ctx->topo.L;
     if (batch == 0 || grid_h == 0 || grid_w == 0) {
         rc = pf_parse_device(ctx, nullptr, nullptr, batch, grid_h, grid_w, stride, p);

@@ -55,7 +55,7 @@
 
 namespace pf {
 
-#ifdef PF_CORNER_PROF
+#if defined(PF_CORNER_PROF) || defined(PF_FIN_PROF)
 __device__ unsigned long long g_corner_prof[16];  // cycles per phase [0, 12) (thread 0 of each CTA), planes, hot, survivors, candidates
 #endif
 
@@ -303,6 +303,9 @@ __device__ __forceinline__ void partial_cands(const UpCornerArgs &a, const Bands
                 const float e = sl_v(c, (float)__dsub_rn(1.0, tx), (float)tx);
                 if (fabsf(e) * rdt > n && y != (e > 0.f ? rb.y : rb.x)) continue;
             }
+#ifdef PF_FIN_PROF
+            atomicAdd(g_corner_prof + 4, 1ull);
+#endif
             cl(y, x);
         }
     }
@@ -368,6 +371,10 @@ __device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands 
     const int4 rb = bd.rb[pr], cb = bd.cb[q];
     unsigned corners;
     const unsigned ok = classify_cell(bd, S, a.w, a.nbr, a.nbc, pr, q, rb, cb, corners);
+#ifdef PF_FIN_PROF
+    atomicAdd(g_corner_prof + (ok == 3u ? 1 : 2), 1ull);
+    if (ok != 3u) atomicAdd(g_corner_prof + 6 + ok, 1ull);
+#endif
     if (ok == 3u) {
         while (corners) {
             const int bit = __ffs(corners) - 1;
@@ -376,6 +383,9 @@ __device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands 
             if (i == 1 && rb.x == rb.y) continue;     // a 1-row band's pixel is visited once
             if (j == 1 && cb.x == cb.y) continue;
             if (!corner_cross_ok(bd, S, a.w, i ? pr - 1 : pr, j ? q - 1 : q, i, j)) continue;
+#ifdef PF_FIN_PROF
+            atomicAdd(g_corner_prof + 3, 1ull);
+#endif
             cl(i ? rb.x : rb.y, j ? cb.x : cb.y);
         }
     } else {
@@ -1066,6 +1076,9 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
     for (int plane = blockIdx.x * kFinGroups + grp; plane < P; plane += gridDim.x * kFinGroups) {
         const int ns = __ldcg(a.surv_n + plane);
         if (ns < 0) continue;   // -1: k_nms_up_corner finished it; -2: crowded (k_corner_crowded); group-uniform
+#ifdef PF_FIN_PROF
+        if (gl == 0) { atomicAdd(g_corner_prof + 12, 1ull); atomicAdd(g_corner_prof + 0, (unsigned long long)ns); }
+#endif
         if (gl == 0) { n_cand[grp] = 0; n_pk[grp] = 0; }
         __syncwarp(gmask);
         const int fb = plane / a.K, k = plane - fb * a.K;
@@ -1455,7 +1468,7 @@ cudaError_t configure_corner_kernels(int max_smem)
 
 }  // namespace pf
 
-#ifdef PF_CORNER_PROF
+#if defined(PF_CORNER_PROF) || defined(PF_FIN_PROF)
 // development builds only: read (and reset) the per-phase cycle counters
 extern "C" int pf_corner_prof_read(unsigned long long *out, int reset)
 {

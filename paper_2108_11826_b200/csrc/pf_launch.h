@@ -222,6 +222,26 @@ cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s);    //
 cudaError_t launch_score_pairs(const ParseArgs &a, int B, cudaStream_t s);
 cudaError_t configure_parse_kernels(int max_smem);
 
+// pf_large.cu: frames past the shared-memory capacities of k_parse_frames
+// (per-frame HBM workspace, 32-bit indices; see pf_large.cu)
+struct LargeWs {
+    int cap_peaks, cap_cands, cap_humans;    // per frame
+    int part_words, used_words;              // bitmap words per part side / per frame (L * 2 * part_words)
+    uint32_t *pk_cell;                       // [B][cap_peaks]
+    float *pk_score;
+    int *owner;
+    void *cand;                              // [B][cap_cands] records of large_cand_bytes()
+    uint32_t *used;                          // [B][used_words]
+    int *h_parts;                            // [B][cap_humans][K]
+    int8_t *h_order;                         // [B][cap_humans][K]
+    int8_t *h_n, *h_alive;                   // [B][cap_humans]
+    uint32_t *h_mask;
+    double *h_score;
+    int *h_pos;
+};
+size_t large_cand_bytes();
+cudaError_t launch_parse_large(const ParseArgs &a, const LargeWs &ws, int B, cudaStream_t s);
+
 // pf_render.cu
 struct RenderArgs {
     Topo topo;
