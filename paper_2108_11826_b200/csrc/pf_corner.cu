@@ -101,12 +101,19 @@ __device__ __forceinline__ Ax ax_load(const AxisRec *tab, int o, int n_out)
 }
 
 
+// Source accessor of a low-res plane (global or shared memory).
+struct PlaneSrc {
+    const float *S;
+    int w;
+    __device__ float operator()(int r, int c) const { return S[r * w + c]; }
+};
+
 // Exact upsampled value (operators.py:104-107 op order); -inf off-grid.
-__device__ __forceinline__ float up_val(const float *S, int w, const Ax &ry, const Ax &cx)
+template <class Src>
+__device__ __forceinline__ float up_val(const Src &S, const Ax &ry, const Ax &cx)
 {
     if (!(ry.in && cx.in)) return -INFINITY;
-    return bilerp(S[ry.i0 * w + cx.i0], S[ry.i0 * w + cx.i1], S[ry.i1 * w + cx.i0], S[ry.i1 * w + cx.i1],
-                  cx.t, cx.omt, ry.t, ry.omt);
+    return bilerp(S(ry.i0, cx.i0), S(ry.i0, cx.i1), S(ry.i1, cx.i0), S(ry.i1, cx.i1), cx.t, cx.omt, ry.t, ry.omt);
 }
 
 // The reference predicate (paf.py:87-99) on exactly computed values; each row
@@ -115,30 +122,60 @@ __device__ __noinline__ bool exact_peak(const UpCornerArgs &a, const float *S, i
 {
     const Ax ym = ax_load(a.rrec, y - 1, a.H), yc = ax_load(a.rrec, y, a.H), yp = ax_load(a.rrec, y + 1, a.H);
     const Ax xm = ax_load(a.crec, x - 1, a.W), xc = ax_load(a.crec, x, a.W), xp = ax_load(a.crec, x + 1, a.W);
-    v = up_val(S, a.w, yc, xc);
+    const PlaneSrc src{S, a.w};
+    v = up_val(src, yc, xc);
     if (!(v >= a.thr)) return false;
     // earlier neighbours: strictly greater; later: greater or equal
-    if (!(v > up_val(S, a.w, ym, xm))) return false;
-    if (!(v > up_val(S, a.w, ym, xc))) return false;
-    if (!(v > up_val(S, a.w, ym, xp))) return false;
-    if (!(v > up_val(S, a.w, yc, xm))) return false;
-    if (!(v >= up_val(S, a.w, yc, xp))) return false;
-    if (!(v >= up_val(S, a.w, yp, xm))) return false;
-    if (!(v >= up_val(S, a.w, yp, xc))) return false;
-    return v >= up_val(S, a.w, yp, xp);
+    if (!(v > up_val(src, ym, xm))) return false;
+    if (!(v > up_val(src, ym, xc))) return false;
+    if (!(v > up_val(src, ym, xp))) return false;
+    if (!(v > up_val(src, yc, xm))) return false;
+    if (!(v >= up_val(src, yc, xp))) return false;
+    if (!(v >= up_val(src, yp, xm))) return false;
+    if (!(v >= up_val(src, yp, xc))) return false;
+    return v >= up_val(src, yp, xp);
 }
 
-// The same predicate without early exits: all nine values are gathered at
-// once (one load round trip), for gather-latency-bound callers.
-__device__ __forceinline__ bool exact_peak_all(const UpCornerArgs &a, const float *S, int y, int x, float &v)
+// Horizontal lerps of source row r at three output columns (operators.py:104-105).
+template <class Src>
+__device__ __forceinline__ void hlerp3(const Src &S, int r, const Ax *xs, double *o)
+{
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o[c] = dadd(dmul(S(r, xs[c].i0), xs[c].omt), dmul(S(r, xs[c].i1), xs[c].t));
+}
+
+// The same predicate without early exits: all nine values at once (one
+// load round trip).  A horizontal lerp depends only on its source row and
+// output column, so the three output rows share them: an output row in the
+// same band as the previous one reuses both, one in the next band reuses
+// the previous bottom row as its top (canonical bands: i0 = previous i1).
+// Every value is the same fp64 expression as up_val.
+template <class Src>
+__device__ __forceinline__ bool exact_peak_all(const UpCornerArgs &a, const Src &S, int y, int x, float &v)
 {
     const Ax ys[3] = {ax_load(a.rrec, y - 1, a.H), ax_load(a.rrec, y, a.H), ax_load(a.rrec, y + 1, a.H)};
     const Ax xs[3] = {ax_load(a.crec, x - 1, a.W), ax_load(a.crec, x, a.W), ax_load(a.crec, x + 1, a.W)};
     float n[9];
+    double T[3], B[3];
+    hlerp3(S, ys[0].i0, xs, T);
+    hlerp3(S, ys[0].i1, xs, B);
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+    for (int r = 0; r < 3; ++r) {
+        if (r > 0 && !(ys[r].i0 == ys[r - 1].i0 && ys[r].i1 == ys[r - 1].i1)) {
+            if (ys[r].i0 == ys[r - 1].i1) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) n[3 * r + c] = up_val(S, a.w, ys[r], xs[c]);
+                for (int c = 0; c < 3; ++c) T[c] = B[c];
+            } else {
+                hlerp3(S, ys[r].i0, xs, T);
+            }
+            hlerp3(S, ys[r].i1, xs, B);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            n[3 * r + c] = (ys[r].in && xs[c].in)
+                               ? __double2float_rn(dadd(dmul(T[c], ys[r].omt), dmul(B[c], ys[r].t)))
+                               : -INFINITY;
+    }
     v = n[4];
     // paf.py:95-99: earlier neighbours strictly, later ones non-strictly
     return v >= a.thr && v > n[0] && v > n[1] && v > n[2] && v > n[3] && v >= n[5] && v >= n[6] && v >= n[7] &&
@@ -396,7 +433,7 @@ __device__ __forceinline__ void process_cell(const UpCornerArgs &a, const Bands 
 // Exact value of output pixel (y, x); -inf off the grid (paf.py:87-93 pads).
 __device__ __forceinline__ float exact_value(const UpCornerArgs &a, const float *S, int y, int x)
 {
-    return up_val(S, a.w, ax_load(a.rrec, y, a.H), ax_load(a.crec, x, a.W));
+    return up_val(PlaneSrc{S, a.w}, ax_load(a.rrec, y, a.H), ax_load(a.crec, x, a.W));
 }
 
 // ---- mbarrier + 1-D bulk copy (TMA) helpers
@@ -677,13 +714,7 @@ k_nms_up_corner(const __grid_constant__ UpCornerArgs a)
         PROF_MARK(8);
         __syncthreads();
         PROF_MARK(9);
-        // split mode: hand the survivors to k_corner_finish (no shared plane
-        // needed there) unless this plane took a crowded path
-        const bool handed = a.surv_out && n_hot <= kCornerList && n_surv <= kCornerSurv;
-        if (handed) {
-            for (int i = threadIdx.x; i < n_surv; i += kCornerThreads)
-                a.surv_out[(size_t)plane * kCornerSurv + i] = surv[i];
-        } else if (n_hot > kCornerList) {
+        if (n_hot > kCornerList) {
             // done above
         } else if (n_surv <= kCornerSurv) {
             const int ns = n_surv;
@@ -708,7 +739,7 @@ k_nms_up_corner(const __grid_constant__ UpCornerArgs a)
 
         // ---- (C2) the exact 3x3 test, 9 lanes per candidate (one pixel each),
         // three candidates per warp, gathered by shuffles
-        if (!handed) {
+        {
             const int nc = min(n_cand, kCornerCands + cl.spill_cap);
             const int grp = lane / 9, nb = lane - grp * 9;
             const int src = min(grp, 2) * 9;
@@ -749,8 +780,7 @@ k_nms_up_corner(const __grid_constant__ UpCornerArgs a)
         }
         __syncthreads();                                     // stage + list free again
         if (threadIdx.x == 0) {
-            if (a.surv_out) a.surv_n[plane] = handed ? n_surv : -1;
-            if (!handed) a.counts[plane] = n_pk;             // handed: k_corner_finish writes it
+            a.counts[plane] = n_pk;
             n_hot = 0;
             n_cand = 0;
             n_surv = 0;
@@ -1031,7 +1061,7 @@ struct InlineSink {
     __device__ void operator()(int y, int x) const
     {
         float v;
-        if (exact_peak_all(*a, S, y, x, v)) emit_peak_c(npk, a->peaks, plane, a->cap, v, y, x);
+        if (exact_peak_all(*a, PlaneSrc{S, a->w}, y, x, v)) emit_peak_c(npk, a->peaks, plane, a->cap, v, y, x);
     }
 };
 
@@ -1095,7 +1125,7 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
                 const uint32_t yx = wc[ci];
                 const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
                 float v;
-                if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
+                if (exact_peak_all(a, PlaneSrc{S, a.w}, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
             }
         } else {
             // candidate overflow: classify again and test each candidate on
@@ -1175,7 +1205,7 @@ struct CrowdSink {
             c[slot] = (uint32_t(y) << 16) | uint32_t(x);
         } else {
             float v;
-            if (exact_peak_all(*a, S, y, x, v)) emit_peak_c(npk, a->peaks, plane, a->cap, v, y, x);
+            if (exact_peak_all(*a, PlaneSrc{S, a->w}, y, x, v)) emit_peak_c(npk, a->peaks, plane, a->cap, v, y, x);
         }
     }
 };
@@ -1299,7 +1329,7 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
             const uint32_t yx = cand[ci];
             const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
             float v;
-            if (exact_peak_all(a, S, y, x, v)) emit_peak_c(&n_pk, a.peaks, plane, a.cap, v, y, x);
+            if (exact_peak_all(a, PlaneSrc{S, a.w}, y, x, v)) emit_peak_c(&n_pk, a.peaks, plane, a.cap, v, y, x);
         }
         // 4. dense cells, warp per cell
         const int nd = min(n_dense, kCrowdDense);
