@@ -139,6 +139,37 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch,
                   int grid_h, int grid_w, int stride, const pf_params *p,
                   pf_results *out);
 
+/* Caller-owned results of pf_parse_batch: device (or
+ * mapped pinned) arrays the caller allocates for max_humans slots per frame,
+ * humans of frame f in slots [f][0 .. n_humans[f]) in the reference output
+ * order (paf.py:288).  kp_xy holds cell_to_pixel (x, y) (types.py:233-235),
+ * kp_score the peak value, kp_present 1 where the keypoint exists.
+ * status[0]: PF_OK, or PF_ERR_CAPACITY when a frame had more than max_humans
+ * humans (n_humans[f] is still its true count, only max_humans slots are
+ * written) or an internal capacity overflowed (all n_humans 0); status[1]:
+ * the smallest such frame, -1 if none. */
+typedef struct pf_out {
+    int32_t max_humans;      /* slots per frame (Hmax) */
+    int32_t *n_humans;       /* [B] */
+    double *human_score;     /* [B][Hmax] */
+    int32_t *n_parts;        /* [B][Hmax] */
+    double *kp_xy;           /* [B][Hmax][K][2] */
+    float *kp_score;         /* [B][Hmax][K] */
+    uint8_t *kp_present;     /* [B][Hmax][K] */
+    int32_t *status;         /* [2] */
+} pf_out;
+
+/* The batch entry point of the §8(b) boundary: parse `batch` device-resident
+ * frames (layout as pf_parse_device) into the caller-owned `out`, enqueued on
+ * `cuda_stream` (cudaStream_t as void*; NULL = the context's stream) and
+ * asynchronous: `out` is valid, and the maps may be released, once that
+ * stream reaches this point.  Nothing is replayed (capacity overflows are
+ * reported in out->status instead); errors raised before any work are
+ * returned, as the reference raises before work (paf.py:295). */
+int pf_parse_batch(pf_ctx *ctx, const float *conf, const float *paf, int batch,
+                   int grid_h, int grid_w, int stride, const pf_params *p,
+                   const pf_out *out, void *cuda_stream);
+
 /* Wait for the last parse and expose its results (D2H of the compact pool). */
 int pf_get_results(pf_ctx *ctx, pf_results *out);
 
@@ -185,7 +216,7 @@ int pf_get_paf_sectors(pf_ctx *ctx, long long *sectors);
 
 /* Per-kernel device time (ms, CUDA events on the launching stream) and launch
  * counts accumulated since the last reset; ids index pf_kernel_name(). */
-#define PF_N_KERNELS 16
+#define PF_N_KERNELS 17
 const char *pf_kernel_name(int id);
 int pf_get_kernel_times(pf_ctx *ctx, double *ms, int64_t *launches, int reset);
 int pf_get_peaks(pf_ctx *ctx, int frame, int *n_peaks, int32_t *part, int32_t *row,

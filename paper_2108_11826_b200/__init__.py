@@ -28,7 +28,7 @@ from .errors import (
     PoseflowError,
 )
 from .hpt import read_ppm, read_ppm_u8, read_tensor, write_ppm, write_tensor
-from .parser import BatchResult, PafParser, ParserParams, parse, parse_arrays, parse_batch
+from .parser import BatchResult, PafParser, ParserParams, PoseSlots, parse, parse_arrays, parse_batch
 from .pipeline_ops import (
     OperatorSpec,
     Packet,

@@ -31,7 +31,7 @@ PF_OPT_CONF_ZERO_COPY = 11
 PF_OPT_PDL = 12
 PF_OPT_COUNT_PAF = 13
 PF_OPT_LARGE = 15
-PF_N_KERNELS = 16
+PF_N_KERNELS = 17
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (
@@ -42,7 +42,7 @@ EXPORTED_SYMBOLS = (
     "pf_get_kernel_times", "pf_get_peaks", "pf_get_connections",
     "pf_preprocess_device", "pf_preprocess_f32_device", "pf_resize_device", "pf_host_alloc", "pf_host_free",
     "pf_launch_count", "pf_gaussian_taps", "pf_format_records", "pf_format_float", "pf_render_maps",
-    "pf_overlay", "pf_get_paf_sectors",
+    "pf_overlay", "pf_get_paf_sectors", "pf_parse_batch",
 )
 
 
@@ -87,6 +87,20 @@ class PfResults(ctypes.Structure):
     ]
 
 
+class PfOut(ctypes.Structure):
+    """pf_out: caller-owned [B][max_humans] result slots (device pointers)."""
+    _fields_ = [
+        ("max_humans", ctypes.c_int32),
+        ("n_humans", ctypes.c_void_p),
+        ("human_score", ctypes.c_void_p),
+        ("n_parts", ctypes.c_void_p),
+        ("kp_xy", ctypes.c_void_p),
+        ("kp_score", ctypes.c_void_p),
+        ("kp_present", ctypes.c_void_p),
+        ("status", ctypes.c_void_p),
+    ]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -118,6 +132,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pf_parse_host.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int,
                                       ctypes.POINTER(PfParams), ctypes.POINTER(PfResults)]
         lib.pf_get_results.argtypes = [vp, ctypes.POINTER(PfResults)]
+        lib.pf_parse_batch.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, ctypes.POINTER(PfParams),
+                                       ctypes.POINTER(PfOut), vp]
         lib.pf_sync.argtypes = [vp]
         lib.pf_set_debug.argtypes = [vp, c_int]
         lib.pf_set_option.argtypes = [vp, c_int, c_int]

@@ -268,13 +268,13 @@ int fail(pf_ctx *c, int code, const char *fmt, ...)
 
 enum KernelId { kNmsPlane = 0, kNmsUp, kParseFrames, kResize, kBlurRows, kBlurCols, kPreprocess,
                 kNmsUpWin, kNmsUpCorner, kCornerFinish, kCornerCrowded, kNmsUpScan, kParsePeaks, kScorePairs,
-                kUpBlur, kParseLarge };
+                kUpBlur, kParseLarge, kScatterOut };
 const char *kKernelNames[PF_N_KERNELS] = {"k_nms_plane", "k_nms_up", "k_parse_frames",
                                           "k_resize_planes", "k_blur_rows", "k_blur_cols",
                                           "k_preprocess", "k_nms_up_win", "k_nms_up_corner",
                                           "k_corner_finish", "k_corner_crowded", "k_nms_up_scan",
                                           "k_parse_peaks", "k_score_pairs", "k_up_blur_nms",
-                                          "k_parse_large"};
+                                          "k_parse_large", "k_scatter_out"};
 
 cudaEvent_t take_event(pf_ctx *ctx)
 {
@@ -1460,6 +1460,81 @@ int pf_get_paf_sectors(pf_ctx *ctx, long long *sectors)
     long long n = 0;
     for (uint32_t v : bm) n += __builtin_popcount(v);
     *sectors = n;
+    return PF_OK;
+}
+
+// pf_parse_batch's scatter: warp per frame, the frame's humans from the
+// context pool (frame_first / frame_count) into the caller's [B][Hmax] slots.
+__global__ void k_scatter_out(const Status *__restrict__ st, int B, int K, const int *__restrict__ first,
+                              const int *__restrict__ count, const double *__restrict__ hs,
+                              const int *__restrict__ hn, const double *__restrict__ kx,
+                              const double *__restrict__ ky, const float *__restrict__ ks,
+                              const int *__restrict__ kp, pf_out o)
+{
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int code = st->code;
+    if (code != 0 && warp == 0 && lane == 0) {                 // internal capacity: nothing is valid
+        atomicMax(o.status, code);
+        atomicMin(reinterpret_cast<unsigned *>(o.status + 1), (unsigned)st->frame);
+    }
+    for (int f = warp; f < B; f += nwarps) {
+        const int n = code != 0 ? 0 : count[f];
+        if (lane == 0) {
+            o.n_humans[f] = n;
+            if (n > o.max_humans) {
+                atomicMax(o.status, PF_ERR_CAPACITY);
+                atomicMin(reinterpret_cast<unsigned *>(o.status + 1), (unsigned)f);
+            }
+        }
+        const int nh = min(n, o.max_humans), h0 = first[f];
+        const size_t slot0 = (size_t)f * o.max_humans;
+        for (int h = lane; h < nh; h += kWarp) {
+            o.human_score[slot0 + h] = hs[h0 + h];
+            o.n_parts[slot0 + h] = hn[h0 + h];
+        }
+        for (int e = lane; e < nh * K; e += kWarp) {
+            const size_t src = (size_t)h0 * K + e, dst = slot0 * K + e;
+            const bool present = kp[src] >= 0;
+            o.kp_xy[2 * dst] = present ? kx[src] : 0.0;
+            o.kp_xy[2 * dst + 1] = present ? ky[src] : 0.0;
+            o.kp_score[dst] = present ? ks[src] : 0.f;
+            o.kp_present[dst] = present ? 1 : 0;
+        }
+    }
+}
+
+int pf_parse_batch(pf_ctx *ctx, const float *conf, const float *paf, int batch, int grid_h, int grid_w,
+                   int stride, const pf_params *p, const pf_out *out, void *cuda_stream)
+{
+    if (!ctx) return PF_ERR_CONTRACT;
+    if (!out || !out->status) return fail(ctx, PF_ERR_CONTRACT, "pf_parse_batch: null output / status");
+    if (out->max_humans < 0) return fail(ctx, PF_ERR_CONTRACT, "pf_parse_batch: max_humans must be >= 0");
+    if (batch > 0 && (!out->n_humans || (out->max_humans > 0 && (!out->human_score || !out->n_parts ||
+                                                                  !out->kp_xy || !out->kp_score ||
+                                                                  !out->kp_present))))
+        return fail(ctx, PF_ERR_CONTRACT, "pf_parse_batch: null output array");
+    struct Restore {
+        pf_ctx *c;
+        cudaStream_t s;
+        ~Restore() { c->stream = s; }
+    } restore{ctx, ctx->stream};
+    if (cuda_stream) ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    int rc = pf_parse_device(ctx, conf, paf, batch, grid_h, grid_w, stride, p);
+    ctx->last.kind = 0;                                  // never replayed: inputs only for the call
+    if (rc) return rc;
+    CU(cudaMemsetAsync(out->status, 0, sizeof(int32_t), ctx->stream));
+    CU(cudaMemsetAsync(out->status + 1, 0xff, sizeof(int32_t), ctx->stream));   // -1: no frame
+    if (batch == 0) return PF_OK;
+    const int threads = 256;
+    const int blocks = std::min((batch * kWarp + threads - 1) / threads, ctx->sms * 8);
+    {
+        KernelTimer kt(ctx, kScatterOut);
+        k_scatter_out<<<blocks, threads, 0, ctx->stream>>>(ctx->d_status, batch, ctx->topo.K, ctx->d_frame_first,
+                                                            ctx->d_frame_count, ctx->d_hscore, ctx->d_hnparts,
+                                                            ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp, *out);
+        CU(cudaGetLastError());
+    }
     return PF_OK;
 }
 

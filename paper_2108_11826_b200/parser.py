@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _native
 from .core import FeatureMaps, HumanPose, Keypoint, SkeletonTopology
-from .errors import ConfigError, ContractError
+from .errors import CapacityError, ConfigError, ContractError, DeviceError
 
 
 @dataclass
@@ -225,6 +225,42 @@ class PafParser:
         self.parse_device(conf.data_ptr(), paf.data_ptr(), b, h, w, stride, params)
         self._inflight = (conf, paf)
 
+    def parse_into(self, conf, paf, stride: int, params: ParserParams, max_humans: int = 64,
+                   out: Optional["PoseSlots"] = None, stream=None) -> "PoseSlots":
+        """The §8(b) batch entry point (``pf_parse_batch``): torch CUDA maps
+        in, caller-owned device slots out (``PoseSlots``, allocated here
+        unless ``out`` is given), enqueued on ``stream`` (default: torch's
+        current stream) with no host synchronisation.  Valid once that stream
+        reaches this point; the maps are needed only until then (no replay:
+        capacity overflows land in ``out.status``)."""
+        import torch
+
+        params = _params_of(params)
+        params.validate()
+        self._check_arrays(tuple(conf.shape), tuple(paf.shape), stride)
+        if conf.dtype != torch.float32 or paf.dtype != torch.float32:
+            raise ContractError("maps must be float32")
+        if not (conf.is_cuda and paf.is_cuda):
+            raise ContractError("parse_into needs CUDA tensors")
+        conf = conf.contiguous()
+        paf = paf.contiguous()
+        b, _, h, w = conf.shape
+        if out is None:
+            out = PoseSlots.empty(b, int(max_humans), self.topo.n_keypoints, conf.device)
+        elif out.n_humans.shape[0] != b or out.kp_present.shape[2] != self.topo.n_keypoints:
+            raise ContractError("output slots do not match the batch / keypoint count")
+        st = stream if stream is not None else torch.cuda.current_stream(conf.device)
+        p = params.to_native()
+        native_out = out.native()
+        self.ctx.check(self.ctx.lib.pf_parse_batch(
+            self.ctx.handle, ctypes.c_void_p(conf.data_ptr()), ctypes.c_void_p(paf.data_ptr()), int(b),
+            int(h), int(w), int(stride), ctypes.byref(p), ctypes.byref(native_out),
+            ctypes.c_void_p(st.cuda_stream)))
+        # the caching allocator must not reuse the maps before the stream is done with them
+        conf.record_stream(st)
+        paf.record_stream(st)
+        return out
+
     def results(self) -> BatchResult:
         res = _native.PfResults()
         try:
@@ -262,6 +298,57 @@ class PafParser:
 
     def close(self) -> None:
         self.ctx.close()
+
+
+class PoseSlots:
+    """Caller-owned result slots of ``parse_into`` (torch device tensors,
+    the ``pf_out`` SoA): frame f's humans in slots [f, :n_humans[f]], in
+    the reference output order (paf.py:288)."""
+
+    def __init__(self, n_humans, human_score, n_parts, kp_xy, kp_score, kp_present, status):
+        self.n_humans, self.human_score, self.n_parts = n_humans, human_score, n_parts
+        self.kp_xy, self.kp_score, self.kp_present, self.status = kp_xy, kp_score, kp_present, status
+
+    @classmethod
+    def empty(cls, batch: int, max_humans: int, n_keypoints: int, device) -> "PoseSlots":
+        import torch
+
+        if max_humans < 0:
+            raise ContractError("max_humans must be >= 0")
+        z = dict(device=device)
+        return cls(torch.empty(batch, dtype=torch.int32, **z),
+                   torch.empty(batch, max_humans, dtype=torch.float64, **z),
+                   torch.empty(batch, max_humans, dtype=torch.int32, **z),
+                   torch.empty(batch, max_humans, n_keypoints, 2, dtype=torch.float64, **z),
+                   torch.empty(batch, max_humans, n_keypoints, dtype=torch.float32, **z),
+                   torch.empty(batch, max_humans, n_keypoints, dtype=torch.uint8, **z),
+                   torch.empty(2, dtype=torch.int32, **z))
+
+    def native(self) -> "_native.PfOut":
+        return _native.PfOut(int(self.human_score.shape[1]), self.n_humans.data_ptr(),
+                             self.human_score.data_ptr(), self.n_parts.data_ptr(), self.kp_xy.data_ptr(),
+                             self.kp_score.data_ptr(), self.kp_present.data_ptr(), self.status.data_ptr())
+
+    def check(self) -> None:
+        """Synchronise on the slots and raise CapacityError if a frame did not fit."""
+        code, frame = (int(v) for v in self.status.cpu())
+        if code == _native.PF_ERR_CAPACITY:
+            raise CapacityError(f"frame {frame} exceeds a capacity of pf_parse_batch "
+                                f"(max_humans {self.human_score.shape[1]} or an internal cap)")
+        if code != 0:
+            raise DeviceError(f"pf_parse_batch status {code}")
+
+    def poses(self, frame: int) -> List[HumanPose]:
+        """Host HumanPose list of one frame (reference types, types.py:208-230)."""
+        n = int(self.n_humans[frame])
+        sc = self.human_score[frame, :n].cpu().tolist()
+        npart = self.n_parts[frame, :n].cpu().tolist()
+        xy = self.kp_xy[frame, :n].cpu().tolist()
+        ks = self.kp_score[frame, :n].cpu().tolist()
+        pr = self.kp_present[frame, :n].cpu().tolist()
+        return [HumanPose(keypoints=tuple(Keypoint(x=xy[i][k][0], y=xy[i][k][1], score=ks[i][k]) if pr[i][k] else None
+                                          for k in range(len(pr[i]))),
+                          score=sc[i], n_parts=npart[i]) for i in range(n)]
 
 
 _tls = threading.local()
