@@ -207,6 +207,10 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_LARGE 15           /* 1: parse through the large-frame kernel (HBM tables, 32-bit ids), the
                                     path the context switches to by itself when a frame outgrows the
                                     shared-memory capacities (more than 32767 peaks, ...); 0: usual path */
+#define PF_OPT_HOST_OVERLAP 16    /* pf_parse_host (default 1): the NMS stage of chunk c+1 on the context
+                                    stream beside the parse of chunk c on a second stream (the in-place
+                                    PAF parse waits on PCIe read requests, the NMS stage on the SMs);
+                                    0: one compute stream */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* With PF_OPT_COUNT_PAF on: distinct 32-byte PAF sectors the last parse call

@@ -132,6 +132,14 @@ cudaError_t host_alloc(T **p, size_t n)
 #endif
 constexpr int kHostSlots = PF_HOST_SLOTS;   // device input slots of pf_parse_host (copy / compute overlap)
 
+// Streams of one run_chunk: the NMS stage (upsample / blur / peaks) on
+// `nms`, the parse stage on `parse`, NMS slab set `set`.  Serial: both the
+// context stream, set 0.
+struct Sched {
+    cudaStream_t nms, parse;
+    int set;
+};
+
 struct pf_ctx {
     int device = 0;
     int sms = 148;
@@ -146,8 +154,15 @@ struct pf_ctx {
     int64_t launches = 0;
 
     // NMS workspace (chunk-sized)
-    int *d_counts = nullptr;
-    uint2 *d_peaks = nullptr;
+    // NMS slabs (peak counts + records per plane); a second set while
+    // pf_parse_host overlaps the NMS stage of one chunk with the parse of the last
+    int *d_counts = nullptr, *d_counts2 = nullptr;
+    uint2 *d_peaks = nullptr, *d_peaks2 = nullptr;
+    int ws_sets = 0;
+    cudaStream_t parse_stream = nullptr;    // pf_parse_host: the parse stage beside the NMS stage
+    cudaEvent_t ev_nms[2] = {}, ev_parsed[2] = {}, ev_join = nullptr;
+    int host_overlap = 1;                   // PF_OPT_HOST_OVERLAP
+    int prio_low = 0, prio_high = 0;
     void *d_spill = nullptr;     // candidate spill slab for crowded frames
     uint32_t *d_corner_spill = nullptr;   // k_nms_up_corner candidate overflow (per resident CTA)
     uint32_t *d_surv = nullptr;           // split corner path: survivors per plane
@@ -294,11 +309,13 @@ struct KernelTimer {
     int id;
     int n;
     cudaEvent_t a = nullptr;
-    KernelTimer(pf_ctx *c, int kid, int launches = 1) : ctx(c), id(kid), n(launches)
+    cudaStream_t st;
+    KernelTimer(pf_ctx *c, int kid, int launches = 1, cudaStream_t s = nullptr)
+        : ctx(c), id(kid), n(launches), st(s ? s : c->stream)
     {
         if (ctx->timing) {
             a = take_event(ctx);
-            cudaEventRecord(a, ctx->stream);
+            cudaEventRecord(a, st);
         }
     }
     ~KernelTimer()
@@ -307,7 +324,7 @@ struct KernelTimer {
         ctx->kernel_launches[id] += n;
         if (a) {
             cudaEvent_t b = take_event(ctx);
-            cudaEventRecord(b, ctx->stream);
+            cudaEventRecord(b, st);
             ctx->pending.push_back({id, {a, b}});
         }
     }
@@ -364,24 +381,35 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
     return PF_OK;
 }
 
-int ensure_nms_ws(pf_ctx *ctx, size_t frames, int K)
+int ensure_nms_ws(pf_ctx *ctx, size_t frames, int K, int sets = 1)
 {
     if (frames <= ctx->ws_frames && K <= ctx->ws_K && ctx->ws_cap_part == ctx->caps.max_peaks_per_part &&
-        ctx->ws_cap_cands == ctx->caps.max_candidates)
+        ctx->ws_cap_cands == ctx->caps.max_candidates && sets <= ctx->ws_sets)
         return PF_OK;
+    CU(cudaDeviceSynchronize());                         // the old slabs may still be in use
     ctx->ws_cap_part = ctx->caps.max_peaks_per_part;
     ctx->ws_cap_cands = ctx->caps.max_candidates;
     cudaFree(ctx->d_counts);
     cudaFree(ctx->d_peaks);
+    cudaFree(ctx->d_counts2);
+    cudaFree(ctx->d_peaks2);
     cudaFree(ctx->d_spill);
-    ctx->d_counts = nullptr;
-    ctx->d_peaks = nullptr;
+    ctx->d_counts = ctx->d_counts2 = nullptr;
+    ctx->d_peaks = ctx->d_peaks2 = nullptr;
     ctx->d_spill = nullptr;
+    ctx->ws_sets = 0;
     const size_t f = frames > ctx->ws_frames ? frames : ctx->ws_frames;
     const int k = K > ctx->ws_K ? K : ctx->ws_K;
+    const int ns = sets > ctx->ws_sets ? sets : 1;
     CU(dev_alloc(&ctx->d_counts, f * k));
     CU(cudaMemset(ctx->d_counts, 0, f * k * sizeof(int)));
     CU(dev_alloc(&ctx->d_peaks, f * k * (size_t)ctx->caps.max_peaks_per_part));
+    if (ns > 1) {
+        CU(dev_alloc(&ctx->d_counts2, f * k));
+        CU(cudaMemset(ctx->d_counts2, 0, f * k * sizeof(int)));
+        CU(dev_alloc(&ctx->d_peaks2, f * k * (size_t)ctx->caps.max_peaks_per_part));
+    }
+    ctx->ws_sets = ns;
     // [f][cap_cands] records: the one-kernel parse uses it as the spill past the
     // shared candidates, the split parse as the whole per-frame candidate list
     CU(dev_alloc(reinterpret_cast<char **>(&ctx->d_spill),
@@ -581,7 +609,7 @@ bool fused_blur(const pf_ctx *ctx, const pf_params *p, int W)
 
 int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame_base,
               int h, int w, int stride, const pf_params *p, AxisCache *rows, AxisCache *cols,
-              int pool_cap)
+              int pool_cap, Sched sc)
 {
     const int K = ctx->topo.K, L = ctx->topo.L;
     const int C = K + 1;
@@ -590,12 +618,16 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     const int half = p->nms_window / 2;
     const float thr = (float)p->conf_threshold;   // numpy NEP 50: fp32 compare
     const bool blur = p->blur_sigma > 0.0;
-    cudaStream_t s = ctx->stream;
+    const bool two = sc.nms != sc.parse;
+    int *const counts = sc.set ? ctx->d_counts2 : ctx->d_counts;
+    uint2 *const peaks = sc.set ? ctx->d_peaks2 : ctx->d_peaks;
+    cudaStream_t s = sc.nms;                       // the NMS stage
+    if (two) CU(cudaStreamWaitEvent(s, ctx->ev_parsed[sc.set], 0));   // this slab set consumed
 
     if (!blur && up == 1) {
-        KernelTimer kt(ctx, kNmsPlane);
+        KernelTimer kt(ctx, kNmsPlane, 1, s);
         CU(launch_nms_plane(conf, n, C, K, h, w, thr, half, ctx->caps.max_peaks_per_part,
-                            ctx->d_counts, ctx->d_peaks, s));
+                            counts, peaks, s));
     } else if (fused_blur(ctx, p, W)) {
         // fused upsample -> blur -> 3x3 NMS (nothing full-resolution in HBM)
         UpBlurArgs a{};
@@ -604,8 +636,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.up = up;
         make_taps(p->blur_sigma, a.taps);
         a.thr = thr; a.cap = ctx->caps.max_peaks_per_part;
-        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
-        KernelTimer kt(ctx, kUpBlur);
+        a.counts = counts; a.peaks = peaks;
+        KernelTimer kt(ctx, kUpBlur, 1, s);
         CU(launch_up_blur_nms(a, s));
     } else if (!blur && half == 1 && !ctx->materialise && !ctx->generic_fused && ctx->win_variant == 4 &&
                rows->canonical && cols->canonical && h + 1 <= 256 && w + 1 <= 256 &&
@@ -617,7 +649,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         UpCornerArgs a{};
         a.conf = conf; a.B = n; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
         a.thr = thr; a.cap = ctx->caps.max_peaks_per_part;
-        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+        a.counts = counts; a.peaks = peaks;
         a.rows = rows->dev(); a.cols = cols->dev();
         a.rband = rows->d_bands; a.cband = cols->d_bands;
         a.rdt = rows->d_band_dt; a.cdt = cols->d_band_dt;
@@ -651,18 +683,18 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             CU(cudaMemsetAsync(a.crowd_n, 0, sizeof(int), s));
         }
         if (csplit) {
-            KernelTimer kt(ctx, kNmsUpScan);                          // streaming half
+            KernelTimer kt(ctx, kNmsUpScan, 1, s);                          // streaming half
             CU(launch_nms_up_scan(a, s));
         } else {
-            KernelTimer kt(ctx, kNmsUpCorner);                        // one-kernel path
+            KernelTimer kt(ctx, kNmsUpCorner, 1, s);                        // one-kernel path
             CU(launch_nms_up_corner(a, s));
         }
         if (csplit) {
             {
-                KernelTimer kt(ctx, kCornerFinish);
+                KernelTimer kt(ctx, kCornerFinish, 1, s);
                 CU(launch_corner_finish(a, s));
             }
-            KernelTimer kt(ctx, kCornerCrowded);
+            KernelTimer kt(ctx, kCornerCrowded, 1, s);
             CU(launch_corner_crowded(a, s));
         }
     } else if (!blur && (half == 1 || half == 2) && !ctx->materialise && !ctx->generic_fused &&
@@ -672,19 +704,19 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.ry = (double)h / (double)H;
         a.rx = (double)w / (double)W;
         a.thr = thr; a.half = half; a.cap = ctx->caps.max_peaks_per_part;
-        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+        a.counts = counts; a.peaks = peaks;
         a.first_out = rows->d_first; a.last_out = rows->d_last;
         a.variant = ctx->win_variant;
         a.rows = rows->dev(); a.cols = cols->dev(); a.gend = rows->d_gend; a.tw = rows->d_tw;
         a.stage = 0;   // measured: staging the plane in smem is slower than L1-cached reads
-        KernelTimer kt(ctx, kNmsUpWin);
+        KernelTimer kt(ctx, kNmsUpWin, 1, s);
         CU(launch_nms_up_win(a, n, s));
     } else if (!blur && half <= kMaxFusedHalf && !ctx->materialise) {
         UpArgs a{};
         a.conf = conf; a.C = C; a.K = K; a.h = h; a.w = w; a.H = H; a.W = W;
         a.rows = rows->dev(); a.cols = cols->dev();
         a.thr = thr; a.half = half; a.cap = ctx->caps.max_peaks_per_part;
-        a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+        a.counts = counts; a.peaks = peaks;
         // band height: keep the fp64 staging of the source rows <= 48 KB
         int band = H;
         auto src_rows = [&](int b0, int b1) {
@@ -704,7 +736,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             if (ns > max_src) max_src = ns;
         }
         const size_t smem = nms_up_smem(max_src, w, half, band, W);
-        KernelTimer kt(ctx, kNmsUp);
+        KernelTimer kt(ctx, kNmsUp, 1, s);
         CU(launch_nms_up(a, n, smem, s));
     } else {
         // materialised: resize (if up > 1) -> blur (if sigma > 0) -> NMS
@@ -717,7 +749,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         int nms_C = C;
         long long src_frame = (long long)C * h * w;
         if (up > 1) {
-            KernelTimer kt(ctx, kResize);
+            KernelTimer kt(ctx, kResize, 1, s);
             CU(launch_resize_planes(conf, (long long)C * h * w, K, (long long)n * K, h, w, ctx->d_full, H, W,
                                     rows->d_rec, cols->d_rec, s));
             nms_src = ctx->d_full;
@@ -727,17 +759,22 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         if (blur) {
             BlurTaps taps;
             make_taps(p->blur_sigma, taps);
-            KernelTimer kt(ctx, kBlurRows, 2);   // rows + cols pass, timed together
+            KernelTimer kt(ctx, kBlurRows, 2, s);   // rows + cols pass, timed together
             CU(launch_blur(nms_src, src_frame, ctx->d_tmp, ctx->d_full, (long long)frame_full, n, K,
                            H, W, taps, ctx->sms, s));
             nms_src = ctx->d_full;
             nms_C = K;
         }
-        KernelTimer kt(ctx, kNmsPlane);
+        KernelTimer kt(ctx, kNmsPlane, 1, s);
         CU(launch_nms_plane(nms_src, n, nms_C, K, H, W, thr, half, ctx->caps.max_peaks_per_part,
-                            ctx->d_counts, ctx->d_peaks, s));
+                            counts, peaks, s));
     }
 
+    if (two) {                                      // the parse stage on its own stream
+        CU(cudaEventRecord(ctx->ev_nms[sc.set], sc.nms));
+        CU(cudaStreamWaitEvent(sc.parse, ctx->ev_nms[sc.set], 0));
+    }
+    s = sc.parse;
     ParseArgs a{};
     a.topo = ctx->topo;
     a.paf = paf; a.h = h; a.w = w; a.up = up;
@@ -764,7 +801,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     }
     a.min_score = p->min_human_score;
     a.min_parts = p->min_parts;
-    a.counts = ctx->d_counts; a.peaks = ctx->d_peaks;
+    a.counts = counts; a.peaks = peaks;
     a.cap_part = ctx->caps.max_peaks_per_part;
     a.cap_frame = ctx->caps.max_peaks_per_frame;
     a.cap_cands = ctx->caps.max_candidates;
@@ -782,8 +819,11 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
     if (ctx->large) {                                // frames past the shared-memory capacities
         int rc = ensure_large_ws(ctx, (size_t)n);
         if (rc) return rc;
-        KernelTimer kt(ctx, kParseLarge);
-        CU(launch_parse_large(a, ctx->lws, n, s));
+        {
+            KernelTimer kt(ctx, kParseLarge, 1, s);
+            CU(launch_parse_large(a, ctx->lws, n, s));
+        }
+        if (two) CU(cudaEventRecord(ctx->ev_parsed[sc.set], s));
         return PF_OK;
     }
     const bool psplit = !ctx->count_paf && (ctx->parse_split == 2 || (ctx->parse_split == 1 && n >= kSplitMinFrames));
@@ -801,7 +841,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.ferr = ctx->d_ferr; a.cand_n = ctx->d_cand_n;
         a.crowd_frames = ctx->d_crowd_frames;
         a.crowd_cap = (int)ctx->split_frames;
-        CU(cudaMemsetAsync(ctx->d_crowd_frames + ctx->split_frames, 0, sizeof(int), ctx->stream));
+        CU(cudaMemsetAsync(ctx->d_crowd_frames + ctx->split_frames, 0, sizeof(int), s));
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }
     const int threads = psplit ? kParseFinThreads : kParseThreads;
@@ -809,14 +849,17 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         parse_smem_bytes(a.cap_frame, a.cap_part, a.cap_cands, a.cap_humans, K, ctx->topo.L, threads / 32, psplit);
     if (a.split) {
         {
-            KernelTimer kt(ctx, kParsePeaks, 2);   // k_parse_peaks + k_pair_scan
+            KernelTimer kt(ctx, kParsePeaks, 2, s);   // k_parse_peaks + k_pair_scan
             CU(launch_parse_peaks(a, n, s));
         }
-        KernelTimer kt(ctx, kScorePairs);
+        KernelTimer kt(ctx, kScorePairs, 1, s);
         CU(launch_score_pairs(a, n, s));
     }
-    KernelTimer kt(ctx, kParseFrames);
-    CU(launch_parse_frames(a, n, threads, smem, s));
+    {
+        KernelTimer kt(ctx, kParseFrames, 1, s);
+        CU(launch_parse_frames(a, n, threads, smem, s));
+    }
+    if (two) CU(cudaEventRecord(ctx->ev_parsed[sc.set], s));
     return PF_OK;
 }
 
@@ -1043,8 +1086,17 @@ int pf_create(pf_ctx **out, int device, const pf_caps *caps)
         return e != cudaSuccess;
     };
     if (cu(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream") ||
-        cu(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream"))
+        cu(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream") ||
+        cu(cudaDeviceGetStreamPriorityRange(&ctx->prio_low, &ctx->prio_high), "stream priorities") ||
+        // the parse stream first: its latency-bound CTAs are dispatched ahead of the next NMS stage's
+        cu(cudaStreamCreateWithPriority(&ctx->parse_stream, cudaStreamNonBlocking, ctx->prio_high), "parse stream") ||
+        cu(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event"))
         return bail(PF_ERR_CUDA);
+    for (int k = 0; k < 2; ++k) {
+        if (cu(cudaEventCreateWithFlags(&ctx->ev_nms[k], cudaEventDisableTiming), "event") ||
+            cu(cudaEventCreateWithFlags(&ctx->ev_parsed[k], cudaEventDisableTiming), "event"))
+            return bail(PF_ERR_CUDA);
+    }
     ctx->stream = ctx->own_stream;
     for (int k = 0; k < kHostSlots; ++k) {
         if (cu(cudaEventCreateWithFlags(&ctx->ev_copied[k], cudaEventDisableTiming), "event") ||
@@ -1086,7 +1138,7 @@ void pf_destroy(pf_ctx *ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    void *dev[] = {ctx->d_counts, ctx->d_peaks, ctx->d_spill, ctx->d_frame_first, ctx->d_frame_count,
+    void *dev[] = {ctx->d_counts, ctx->d_peaks, ctx->d_counts2, ctx->d_peaks2, ctx->d_spill, ctx->d_frame_first, ctx->d_frame_count,
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp,
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
@@ -1117,8 +1169,14 @@ void pf_destroy(pf_ctx *ctx)
         if (ctx->ev_copied[k]) cudaEventDestroy(ctx->ev_copied[k]);
         if (ctx->ev_free[k]) cudaEventDestroy(ctx->ev_free[k]);
     }
+    for (int k = 0; k < 2; ++k) {
+        if (ctx->ev_nms[k]) cudaEventDestroy(ctx->ev_nms[k]);
+        if (ctx->ev_parsed[k]) cudaEventDestroy(ctx->ev_parsed[k]);
+    }
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->parse_stream) cudaStreamDestroy(ctx->parse_stream);
     delete ctx;
 }
 
@@ -1203,6 +1261,7 @@ int pf_set_option(pf_ctx *ctx, int option, int value)
     case PF_OPT_PDL: g_pdl_mask = value; return PF_OK;
     case PF_OPT_COUNT_PAF: ctx->count_paf = value ? 1 : 0; return PF_OK;
     case PF_OPT_LARGE: ctx->large = value ? 1 : 0; return PF_OK;
+    case PF_OPT_HOST_OVERLAP: ctx->host_overlap = value ? 1 : 0; return PF_OK;
     default: return fail(ctx, PF_ERR_CONFIG, "unknown option %d", option);
     }
 }
@@ -1275,7 +1334,7 @@ int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch,
     for (int f0 = 0; f0 < batch; f0 += chunk) {
         const int n = batch - f0 < chunk ? batch - f0 : chunk;
         rc = run_chunk(ctx, conf + (size_t)f0 * conf_frame, paf + (size_t)f0 * paf_frame, n, f0,
-                       grid_h, grid_w, stride, p, rows, cols, pool);
+                       grid_h, grid_w, stride, p, rows, cols, pool, Sched{ctx->stream, ctx->stream, 0});
         if (rc) return rc;
     }
     return PF_OK;
@@ -1396,7 +1455,12 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
             conf_dev = static_cast<const float *>(pa.devicePointer);
         cudaGetLastError();
     }
-    rc = ensure_nms_ws(ctx, chunk, K);
+    // PF_OPT_HOST_OVERLAP: the NMS stage of chunk c+1 runs on ctx->stream
+    // beside the parse of chunk c on parse_stream (two NMS slab sets); the
+    // in-place PAF parse is bound by the PCIe read-request rate, the NMS
+    // stage by the SMs, so they overlap
+    const bool ov = ctx->host_overlap && !ctx->count_paf && !ctx->large && batch > chunk;
+    rc = ensure_nms_ws(ctx, chunk, K, ov ? 2 : 1);
     if (rc) return rc;
     const size_t plane = (size_t)grid_h * grid_w;
     const size_t conf_frame = (size_t)(K + 1) * plane, paf_frame = (size_t)2 * L * plane;
@@ -1420,6 +1484,22 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
     } restore{ctx, saved_split};
     // slots start free
     for (int k = 0; k < kHostSlots; ++k) CU(cudaEventRecord(ctx->ev_free[k], ctx->stream));
+    struct Join {                       // the parse stream rejoins ctx->stream on every exit
+        pf_ctx *c;
+        bool on;
+        void now()
+        {
+            if (on && cudaEventRecord(c->ev_join, c->parse_stream) == cudaSuccess)
+                cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+            on = false;
+        }
+        ~Join() { now(); }
+    } join{ctx, ov};
+    if (ov) {
+        CU(cudaEventRecord(ctx->ev_join, ctx->stream));
+        CU(cudaStreamWaitEvent(ctx->parse_stream, ctx->ev_join, 0));
+        for (int k = 0; k < 2; ++k) CU(cudaEventRecord(ctx->ev_parsed[k], ctx->parse_stream));
+    }
     int ci = 0;
     for (int f0 = 0; f0 < batch; f0 += chunk, ++ci) {
         const int n = batch - f0 < chunk ? batch - f0 : chunk;
@@ -1439,10 +1519,14 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[sl], 0));
         rc = run_chunk(ctx, conf_dev ? conf_dev + (size_t)f0 * conf_frame : dconf,
                        paf_dev ? paf_dev + (size_t)f0 * paf_frame : dpaf, n, f0, grid_h, grid_w,
-                       stride, p, rows, cols, pool);
+                       stride, p, rows, cols, pool,
+                       ov ? Sched{ctx->stream, ctx->parse_stream, ci & 1} : Sched{ctx->stream, ctx->stream, 0});
         if (rc) return rc;
-        CU(cudaEventRecord(ctx->ev_free[sl], ctx->stream));
+        // the slot is free once its last reader is done: the NMS stage, or the
+        // parse when the PAF was copied into the slot
+        CU(cudaEventRecord(ctx->ev_free[sl], ov && !paf_dev ? ctx->parse_stream : ctx->stream));
     }
+    join.now();
     return out ? pf_get_results(ctx, out) : PF_OK;
 }
 
