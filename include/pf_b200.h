@@ -190,7 +190,7 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_TIMING 2
 #define PF_OPT_MATERIALISE 3
 #define PF_OPT_GENERIC_FUSED 4   /* use the shared-memory tile kernel for Mode U */
-#define PF_OPT_WIN_VARIANT 5     /* Mode U 3x3 kernel: 4 corner-pruned (default), 3/2/1 strip kernels */
+#define PF_OPT_WIN_VARIANT 5     /* Mode U 3x3 kernel: 4 corner-pruned (default); 1-3: the strip kernel */
 #define PF_OPT_NO_CHAIN 6        /* corner kernel: disable the chain pre-filter (A/B parity checks) */
 #define PF_OPT_CORNER_SPLIT 9    /* Mode U 3x3: survivors classified by a second kernel;
                                     0 off, 1 auto (batches of >= 32 frames, or planes too large

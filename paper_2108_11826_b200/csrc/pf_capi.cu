@@ -53,8 +53,7 @@ struct AxisCache {
     bool canonical = false;                     // band b reads sources (b-1, b) clipped: b = 0..in_n
     int4 *d_bands = nullptr;
     double *d_band_dt = nullptr;
-    int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr, *d_gend = nullptr;
-    double2 *d_tw = nullptr;
+    int32_t *d_i0 = nullptr, *d_i1 = nullptr, *d_first = nullptr, *d_last = nullptr;
     AxisRec *d_rec = nullptr;
     double *d_t = nullptr, *d_omt = nullptr;
     AxisTab dev() const { return AxisTab{d_i0, d_i1, d_t, d_omt}; }
@@ -352,10 +351,6 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
         CU(cudaMemcpy(a.d_t, a.t.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(a.d_omt, a.omt.data(), out_n * sizeof(double), cudaMemcpyHostToDevice));
         {
-            std::vector<double2> tw(out_n);
-            for (int o = 0; o < out_n; ++o) tw[o] = make_double2(a.t[o], a.omt[o]);
-            CU(dev_alloc(&a.d_tw, out_n));
-            CU(cudaMemcpy(a.d_tw, tw.data(), out_n * sizeof(double2), cudaMemcpyHostToDevice));
             std::vector<AxisRec> rec(out_n);
             for (int o = 0; o < out_n; ++o) {
                 rec[o].i01 = a.i0[o] | (a.i1[o] << 16);
@@ -369,8 +364,6 @@ int get_axis(pf_ctx *ctx, int in_n, int out_n, AxisCache **out)
         CU(cudaMemcpy(a.d_bands, a.bands.data(), a.bands.size() * sizeof(int4), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_band_dt, a.band_dt.size()));
         CU(cudaMemcpy(a.d_band_dt, a.band_dt.data(), a.band_dt.size() * sizeof(double), cudaMemcpyHostToDevice));
-        CU(dev_alloc(&a.d_gend, out_n));
-        CU(cudaMemcpy(a.d_gend, a.gend.data(), out_n * sizeof(int32_t), cudaMemcpyHostToDevice));
         CU(dev_alloc(&a.d_first, in_n));
         CU(dev_alloc(&a.d_last, in_n));
         CU(cudaMemcpy(a.d_first, a.first_out.data(), in_n * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -706,9 +699,6 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.thr = thr; a.half = half; a.cap = ctx->caps.max_peaks_per_part;
         a.counts = counts; a.peaks = peaks;
         a.first_out = rows->d_first; a.last_out = rows->d_last;
-        a.variant = ctx->win_variant;
-        a.rows = rows->dev(); a.cols = cols->dev(); a.gend = rows->d_gend; a.tw = rows->d_tw;
-        a.stage = 0;   // measured: staging the plane in smem is slower than L1-cached reads
         KernelTimer kt(ctx, kNmsUpWin, 1, s);
         CU(launch_nms_up_win(a, n, s));
     } else if (!blur && half <= kMaxFusedHalf && !ctx->materialise) {
@@ -1159,7 +1149,7 @@ void pf_destroy(pf_ctx *ctx)
     for (auto &kv : ctx->axes) {
         cudaFree(kv.second.d_i0); cudaFree(kv.second.d_i1);
         cudaFree(kv.second.d_t); cudaFree(kv.second.d_omt);
-        cudaFree(kv.second.d_first); cudaFree(kv.second.d_last); cudaFree(kv.second.d_gend); cudaFree(kv.second.d_tw);
+        cudaFree(kv.second.d_first); cudaFree(kv.second.d_last);
         cudaFree(kv.second.d_rec);
         cudaFree(kv.second.d_bands); cudaFree(kv.second.d_band_dt);
     }

@@ -75,11 +75,6 @@ struct UpWinArgs {
     int *counts;
     uint2 *peaks;
     const int32_t *first_out, *last_out;   // [h]: output rows reading source row r
-    int variant;         // 3 (default), 2: two columns per lane; 1: one column per lane
-    AxisTab rows, cols;  // host-built operators.py:86-96 tables (variant 3)
-    const int32_t *gend; // [H]: last output row sharing row y's source pair (variant 3)
-    const double2 *tw;   // [H]: (t, 1 - t) per output row, packed for one 16-byte load
-    int stage;           // 1: low-res plane staged in shared memory (variant 3)
 };
 size_t nms_up_win_smem(int h, int w, int H, int threads);
 

@@ -234,21 +234,25 @@ cudaError_t launch_nms_up(const UpArgs &a, int B, size_t smem, cudaStream_t s)
 }
 
 // ---------------------------------------------------------------------------
-// k_nms_up_win<HALF> — register-window fused upsample + NMS (windows 3 and 5).
+// k_nms_up_win2<HALF> — register-window fused upsample + NMS (windows 3 and 5):
+// the strip path for maps the corner kernels do not take (wider than 255
+// cells per axis, non-canonical bands, window 5, or PF_OPT_WIN_VARIANT != 4).
 //
 // One CTA (4 warps) per (frame, part) plane.
 //  phase 1: the low-res plane is streamed once (16-byte loads) and turned into
 //           per-row "cell >= thr" bitmasks in shared memory (the compulsory
 //           HBM read of the path; later reads hit L1).  The output-row
 //           interpolation parameters (operators.py:87-96) go to a shared table.
-//  phase 2: a warp owns a strip of 32 - 2*HALF output columns (one lane per
-//           column, HALF halo lanes each side).  From the bitmasks it derives
-//           the strip's hot source rows and walks only the output rows whose
-//           values can reach thr (+/- HALF halo rows), top to bottom.  Each
-//           lane keeps the horizontal interpolant of its two current source
-//           rows (the reference's `top`/`bot`, operators.py:104-105 — they
-//           depend on the source row only, so reuse is bit-exact) and spends
-//           2 DMUL + 1 DADD + 1 F2F per output.
+//  phase 2: a warp owns a strip of 60 output columns, two per lane (lanes 0
+//           and 31 carry the NMS halo).  From the bitmasks it derives the
+//           strip's hot source rows and walks only the output rows whose
+//           values can reach thr (+/- HALF halo rows), top to bottom, with an
+//           inner row loop per source-row pair: each lane keeps the
+//           horizontal interpolants of the pair's two source rows (the
+//           reference's `top`/`bot`, operators.py:104-105 — they depend on the
+//           source row only, so reuse is bit-exact) and per output row spends
+//           one broadcast LDS.128 (the row weights), 4 DMUL + 2 DADD + 2 F2F
+//           for its two outputs, 2*HALF shuffles and a few maxima.
 //  NMS (paf.py:87-99) as two maxima: the centre must beat max(earlier
 //           neighbours) strictly and max(later neighbours) non-strictly.  The
 //           maxima propagate NaN (max.NaN.f32), so a NaN neighbour suppresses
@@ -277,352 +281,6 @@ __device__ __forceinline__ float max_nan(float a, float b)
 }
 
 // ---------------------------------------------------------------------------
-// k_nms_up_win2<HALF>: the same algorithm with two output columns per lane
-// (strips of 60 useful columns; lanes 0 and 31 carry the NMS halo) and an
-// inner row loop per source-row pair, so the interpolant refresh and all
-// row-invariant work leave the hot loop: per output row a lane spends one
-// broadcast LDS.128 (the row weights), 4 DMUL + 2 DADD + 2 F2F for its two
-// outputs, 2*HALF shuffles and a handful of NaN-propagating maxima.
-// ---------------------------------------------------------------------------
-// ---------------------------------------------------------------------------
-// k_nms_up_win3<HALF>: win2 with the per-plane setup stripped down.
-//  * row tables (source pair, weights, last row of each pair) are built once
-//    per context on the host and read through L1 (warp-uniform loads);
-//  * the "cell >= thr" bits come straight out of the 16-byte plane loads
-//    (a nibble per lane, OR-combined across 8 lanes with shuffles) into a
-//    flat bitmap — no byte array, no per-row ballots;
-//  * no per-row test-range predicate: rows outside a run's tested range are
-//    halo rows whose values are < thr (their sources are cold), so the
-//    threshold compare rejects them, and un-filled window slots are -inf;
-//  * -inf padding rows below the grid are handled after the hot loop;
-//  * the interpolant of a source row is reused when it moves from the lower
-//    to the upper position of the pair.
-// ---------------------------------------------------------------------------
-template <int HALF>
-__device__ __forceinline__ void win3_row(const float v0, const float v1, const bool use0, const bool use1,
-                                         float (&full)[2][2 * HALF + 1], float (&cv)[2][2 * HALF + 1],
-                                         float (&lm)[2][2 * HALF + 1], float (&rm)[2][2 * HALF + 1],
-                                         const UpWinArgs &a, int plane, int yc, const int (&xc)[2])
-{
-    constexpr int WIN = 2 * HALF + 1;
-    const float v[2] = {v0, v1};
-    const float l1 = __shfl_up_sync(0xffffffffu, v1, 1);
-    const float r1 = __shfl_down_sync(0xffffffffu, v0, 1);
-    float lmx[2], rmx[2];
-    if (HALF == 1) {
-        lmx[0] = l1;   rmx[0] = v1;
-        lmx[1] = v0;   rmx[1] = r1;
-    } else {
-        const float l2 = __shfl_up_sync(0xffffffffu, v0, 1);
-        const float r2 = __shfl_down_sync(0xffffffffu, v1, 1);
-        lmx[0] = max_nan(l1, l2);   rmx[0] = max_nan(v1, r1);
-        lmx[1] = max_nan(v0, l1);   rmx[1] = max_nan(r1, r2);
-    }
-    const bool use[2] = {use0, use1};
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-#pragma unroll
-        for (int t = 0; t < WIN - 1; ++t) {
-            full[c][t] = full[c][t + 1]; cv[c][t] = cv[c][t + 1];
-            lm[c][t] = lm[c][t + 1]; rm[c][t] = rm[c][t + 1];
-        }
-        full[c][WIN - 1] = max_nan(max_nan(lmx[c], v[c]), rmx[c]);
-        cv[c][WIN - 1] = v[c]; lm[c][WIN - 1] = lmx[c]; rm[c][WIN - 1] = rmx[c];
-        float earlier = lm[c][HALF], later = rm[c][HALF];
-#pragma unroll
-        for (int t = 0; t < HALF; ++t) {
-            earlier = max_nan(earlier, full[c][t]);
-            later = max_nan(later, full[c][HALF + 1 + t]);
-        }
-        const float cc = cv[c][HALF];
-        const bool pk = use[c] && cc >= a.thr && cc > earlier && cc >= later;
-        if (__any_sync(0xffffffffu, pk)) {            // rare: keep packing out of the row loop
-            if (pk) emit_peak(a.counts, a.peaks, plane, a.cap, cc, yc, xc[c]);
-        }
-    }
-}
-
-// 3x3 window, two columns per lane (x0 = 2*(lane-1)+c): minimal carried state.
-// After row y-1:  c0, c1 = centre values (row y-1) of the lane's columns,
-// cl = value at x0-1 (lane-1's col 1), cr = value at x1+1 (lane+1's col 0),
-// f0, f1 = max over the 3 columns around x0 / x1 of row y-2.
-struct Win1 {
-    float c0, c1, cl, cr, f0, f1;
-};
-
-__device__ __forceinline__ void win1_init(Win1 &s)
-{
-    s.c0 = s.c1 = s.cl = s.cr = s.f0 = s.f1 = -INFINITY;
-}
-
-// Consume row y (values n0, n1); test the centre row y-1 (paf.py:87-99).
-__device__ __forceinline__ void win1_row(Win1 &s, float n0, float n1, float thr, bool use0, bool use1,
-                                         const UpWinArgs &a, int plane, int yc, int x0)
-{
-    const float nl = __shfl_up_sync(0xffffffffu, n1, 1);
-    const float nr = __shfl_down_sync(0xffffffffu, n0, 1);
-    const float fn0 = max_nan(max_nan(nl, n0), n1);      // row y maxima around x0, x1
-    const float fn1 = max_nan(max_nan(n0, n1), nr);
-    // earlier neighbours: row y-2 (3 cells) + left cell of row y-1; later: right cell + row y
-    const bool p0 = use0 && s.c0 >= thr && s.c0 > max_nan(s.f0, s.cl) && s.c0 >= max_nan(s.c1, fn0);
-    const bool p1 = use1 && s.c1 >= thr && s.c1 > max_nan(s.f1, s.c0) && s.c1 >= max_nan(s.cr, fn1);
-    if (__any_sync(0xffffffffu, p0 || p1)) {             // rare
-        if (p0) emit_peak(a.counts, a.peaks, plane, a.cap, s.c0, yc, x0);
-        if (p1) emit_peak(a.counts, a.peaks, plane, a.cap, s.c1, yc, x0 + 1);
-    }
-    s.f0 = max_nan(max_nan(s.cl, s.c0), s.c1);
-    s.f1 = max_nan(max_nan(s.c0, s.c1), s.cr);
-    s.c0 = n0; s.c1 = n1; s.cl = nl; s.cr = nr;
-}
-
-// Low-res source values: shared-memory copy of the plane (SMEM) or L1-cached global.
-template <bool SMEM>
-__device__ __forceinline__ float ldsrc(const float *src, int idx)
-{
-    return SMEM ? src[idx] : __ldg(src + idx);
-}
-
-template <bool EDGE, bool SMEM>
-__device__ __forceinline__ void win1_run(const UpWinArgs &a, const float *__restrict__ p, int plane,
-                                         int run_lo, int run_hi, const int (&xc)[2], const int (&j0)[2],
-                                         const int (&j1)[2], const double (&tx)[2], const double (&omtx)[2],
-                                         const bool (&in_grid)[2], const bool (&useful)[2])
-{
-    const int w = a.w, H = a.H;
-    const float thr = a.thr;
-    Win1 s;
-    win1_init(s);
-    double hA0 = 0.0, hA1 = 0.0, hB0 = 0.0, hB1 = 0.0;
-    int ci1 = -1;
-    int y = run_lo;
-    while (y <= run_hi) {
-        const int i0 = __ldg(a.rows.i0 + y), i1 = __ldg(a.rows.i1 + y);
-        if (i0 == ci1) {                     // warp-uniform: last pair's upper row
-            hA0 = hB0;
-            hA1 = hB1;
-        } else {
-            hA0 = dadd(dmul((double)ldsrc<SMEM>(p, i0 * w + j0[0]), omtx[0]), dmul((double)ldsrc<SMEM>(p, i0 * w + j1[0]), tx[0]));
-            hA1 = dadd(dmul((double)ldsrc<SMEM>(p, i0 * w + j0[1]), omtx[1]), dmul((double)ldsrc<SMEM>(p, i0 * w + j1[1]), tx[1]));
-        }
-        hB0 = dadd(dmul((double)ldsrc<SMEM>(p, i1 * w + j0[0]), omtx[0]), dmul((double)ldsrc<SMEM>(p, i1 * w + j1[0]), tx[0]));
-        hB1 = dadd(dmul((double)ldsrc<SMEM>(p, i1 * w + j0[1]), omtx[1]), dmul((double)ldsrc<SMEM>(p, i1 * w + j1[1]), tx[1]));
-        ci1 = i1;
-        const int yend = min(__ldg(a.gend + y), run_hi);
-        for (; y <= yend; ++y) {
-            const double2 wt = __ldg(a.tw + y);
-            float v0 = __double2float_rn(dadd(dmul(hA0, wt.y), dmul(hB0, wt.x)));
-            float v1 = __double2float_rn(dadd(dmul(hA1, wt.y), dmul(hB1, wt.x)));
-            if (EDGE) {
-                v0 = in_grid[0] ? v0 : -INFINITY;
-                v1 = in_grid[1] ? v1 : -INFINITY;
-            }
-            win1_row(s, v0, v1, thr, useful[0], useful[1], a, plane, y - 1, xc[0]);
-        }
-    }
-    if (run_hi == H - 1)                     // -inf padding row below the grid
-        win1_row(s, -INFINITY, -INFINITY, thr, useful[0], useful[1], a, plane, H - 1, xc[0]);
-}
-
-// Rows [y, run_hi] of one run for one strip; EDGE strips mask out-of-grid
-// columns to -inf (the reference's padding), interior strips skip the select.
-template <int HALF, bool EDGE>
-__device__ __forceinline__ void win3_run(const UpWinArgs &a, const float *__restrict__ p, int plane,
-                                         int run_lo, int run_hi, const int (&xc)[2], const int (&j0)[2],
-                                         const int (&j1)[2], const double (&tx)[2], const double (&omtx)[2],
-                                         const bool (&in_grid)[2], const bool (&useful)[2])
-{
-    constexpr int WIN = 2 * HALF + 1;
-    const int w = a.w, H = a.H;
-    float full[2][WIN], cv[2][WIN], lm[2][WIN], rm[2][WIN];
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int t = 0; t < WIN; ++t) full[c][t] = cv[c][t] = lm[c][t] = rm[c][t] = -INFINITY;
-    double hA[2] = {0.0, 0.0}, hB[2] = {0.0, 0.0};
-    int ci1 = -1;
-    int y = run_lo;
-    while (y <= run_hi) {
-        const int i0 = __ldg(a.rows.i0 + y), i1 = __ldg(a.rows.i1 + y);
-        if (i0 == ci1) {                   // warp-uniform: the upper row of the last pair
-            hA[0] = hB[0];
-            hA[1] = hB[1];
-        } else {
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-                hA[c] = dadd(dmul((double)__ldg(p + i0 * w + j0[c]), omtx[c]),
-                             dmul((double)__ldg(p + i0 * w + j1[c]), tx[c]));
-        }
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-            hB[c] = dadd(dmul((double)__ldg(p + i1 * w + j0[c]), omtx[c]),
-                         dmul((double)__ldg(p + i1 * w + j1[c]), tx[c]));
-        ci1 = i1;
-        const int yend = min(__ldg(a.gend + y), run_hi);
-        for (; y <= yend; ++y) {
-            const double2 wt = __ldg(a.tw + y);          // (t, 1 - t) of output row y
-            float v[2];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const float val = __double2float_rn(dadd(dmul(hA[c], wt.y), dmul(hB[c], wt.x)));
-                v[c] = (EDGE && !in_grid[c]) ? -INFINITY : val;
-            }
-            win3_row<HALF>(v[0], v[1], useful[0], useful[1], full, cv, lm, rm, a, plane, y - HALF, xc);
-        }
-    }
-    if (run_hi == H - 1) {                 // -inf padding rows below the grid
-#pragma unroll
-        for (int t = 1; t <= HALF; ++t)
-            win3_row<HALF>(-INFINITY, -INFINITY, useful[0], useful[1], full, cv, lm, rm, a, plane,
-                           H - 1 + t - HALF, xc);
-    }
-}
-
-template <int HALF>
-__global__ void __launch_bounds__(128, 8)
-k_nms_up_win3(const UpWinArgs a)
-{
-    constexpr int SW = 2 * (kWarp - 2);
-    constexpr int WIN = 2 * HALF + 1;
-    extern __shared__ __align__(16) uint32_t sm[];
-    const int plane = blockIdx.x;
-    const int b = plane / a.K, k = plane - b * a.K;
-    const float *p = a.conf + ((size_t)b * a.C + k) * (size_t)a.h * a.w;
-    const int h = a.h, w = a.w, H = a.H;
-    const int hw = h * w;
-    const int n_bw = ((hw + 127) & ~127) >> 5;   // words of the flat hot bitmap (128-cell padded)
-    const int n_rw = (h + 31) >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_warps = blockDim.x >> 5;
-    uint32_t *hotbits = sm;                                  // [n_bw]
-    uint32_t *srcmask = sm + n_bw + warp * n_rw;             // per warp [n_rw]
-    float *plane_s = reinterpret_cast<float *>(sm + n_bw + 4 * n_rw);   // [h*w] if a.stage (16B aligned)
-
-    // ---- phase 1: stream the plane -> flat bitmap of cells >= thr ----
-    // all 16-byte loads of a thread are issued before any is consumed
-    if ((hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-        const float4 *p4 = reinterpret_cast<const float4 *>(p);
-        const int n4 = hw >> 2, n4_pad = (n4 + 31) & ~31;               // whole warps per pass
-        constexpr int U = 8;
-        for (int e0 = threadIdx.x; e0 < n4_pad; e0 += U * blockDim.x) {
-            float4 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                v[u] = e < n4 ? __ldg(p4 + e) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-            }
-            if (a.stage) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = e0 + u * blockDim.x;
-                    if (e < n4) reinterpret_cast<float4 *>(plane_s)[e] = v[u];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                if (e - lane >= n4_pad) break;                             // warp-uniform tail
-                uint32_t nib = uint32_t(v[u].x >= a.thr) | (uint32_t(v[u].y >= a.thr) << 1) |
-                               (uint32_t(v[u].z >= a.thr) << 2) | (uint32_t(v[u].w >= a.thr) << 3);
-                nib = (e < n4 ? nib : 0u) << (4 * (lane & 7));
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
-                if ((lane & 7) == 0) hotbits[e >> 3] = nib;
-            }
-        }
-    } else {
-        for (int q = threadIdx.x; q < n_bw; q += blockDim.x) hotbits[q] = 0u;
-        __syncthreads();
-        for (int e = threadIdx.x; e < hw; e += blockDim.x) {
-            const float v = __ldg(p + e);
-            if (a.stage) plane_s[e] = v;
-            if (v >= a.thr) atomicOr(hotbits + (e >> 5), 1u << (e & 31));
-        }
-    }
-    __syncthreads();
-
-    // ---- phase 2: strips of SW columns, two per lane ----
-    const int n_strips = (a.W + SW - 1) / SW;
-    for (int s = warp; s < n_strips; s += n_warps) {
-        const int x0 = s * SW;
-        int xc[2], j0[2], j1[2];
-        double tx[2], omtx[2];
-        bool in_grid[2], useful[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            xc[c] = x0 + 2 * (lane - 1) + c;
-            in_grid[c] = xc[c] >= 0 && xc[c] < a.W;
-            useful[c] = lane >= 1 && lane <= kWarp - 2 && in_grid[c];
-            const int xx = min(max(xc[c], 0), a.W - 1);
-            j0[c] = __ldg(a.cols.i0 + xx);
-            j1[c] = __ldg(a.cols.i1 + xx);
-            tx[c] = __ldg(a.cols.t + xx);
-            omtx[c] = __ldg(a.cols.omt + xx);
-        }
-        const int cj0 = __ldg(a.cols.i0 + x0);
-        const int cj1 = __ldg(a.cols.i1 + min(x0 + SW, a.W) - 1);
-        const bool edge = x0 - 2 < 0 || x0 + SW + 2 > a.W;      // strip has out-of-grid lanes
-        // hot source rows of this strip: any bit in [r*w + cj0, r*w + cj1]
-        for (int r0 = 0; r0 < h; r0 += 32) {
-            const int r = r0 + lane;
-            bool any = false;
-            if (r < h) {
-                const int bit0 = r * w + cj0, bit1 = r * w + cj1;
-                for (int q = bit0 >> 5; q <= (bit1 >> 5) && !any; ++q) {
-                    const int lo = max(bit0 - (q << 5), 0), hi = min(bit1 - (q << 5), 31);
-                    const uint32_t span = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
-                    any = (hotbits[q] & span) != 0u;
-                }
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, any);
-            if (lane == 0) srcmask[r0 >> 5] = bal;
-        }
-        __syncwarp();
-
-        int run_lo = -1, run_hi = -2;
-        for (int q = 0; q <= n_rw; ++q) {
-            uint32_t m = q < n_rw ? srcmask[q] : 0u;
-            bool flush_final = q == n_rw;
-            while (m || flush_final) {
-                int lo = 0, hi = -1;
-                if (m) {
-                    const int r = (q << 5) + __ffs(m) - 1;
-                    m &= m - 1u;
-                    lo = max(__ldg(a.first_out + r) - HALF, 0);
-                    hi = min(__ldg(a.last_out + r) + HALF, H - 1);
-                    if (run_hi >= run_lo && lo <= run_hi + 1) {
-                        run_hi = max(run_hi, hi);
-                        continue;
-                    }
-                } else {
-                    flush_final = false;
-                }
-                if (run_hi >= run_lo) {
-                    if (HALF == 1) {
-                        if (a.stage) {
-                            if (edge)
-                                win1_run<true, true>(a, plane_s, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
-                            else
-                                win1_run<false, true>(a, plane_s, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
-                        } else if (edge) {
-                            win1_run<true, false>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
-                        } else {
-                            win1_run<false, false>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
-                        }
-                    } else if (edge) {
-                        win3_run<HALF, true>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
-                    } else {
-                        win3_run<HALF, false>(a, p, plane, run_lo, run_hi, xc, j0, j1, tx, omtx, in_grid, useful);
-                    }
-                }
-                if (hi >= lo) { run_lo = lo; run_hi = hi; }
-                else { run_lo = -1; run_hi = -2; }
-            }
-        }
-        __syncwarp();
-    }
-}
-
 template <int HALF>
 __global__ void __launch_bounds__(128)
 k_nms_up_win2(const UpWinArgs a)
@@ -824,175 +482,6 @@ k_nms_up_win2(const UpWinArgs a)
     }
 }
 
-template <int HALF>
-__global__ void __launch_bounds__(128)
-k_nms_up_win(const UpWinArgs a)
-{
-    constexpr int SW = kWarp - 2 * HALF;     // useful columns per strip
-    constexpr int WIN = 2 * HALF + 1;
-    extern __shared__ __align__(16) uint32_t sm[];
-    const int plane = blockIdx.x;
-    const int b = plane / a.K, k = plane - b * a.K;
-    const float *p = a.conf + ((size_t)b * a.C + k) * (size_t)a.h * a.w;
-    const int h = a.h, w = a.w, H = a.H;
-    const int n_cw = (w + 31) >> 5;          // column words per low-res row
-    const int n_rw = (h + 31) >> 5;          // row words per strip mask
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_warps = blockDim.x >> 5;
-    // shared layout: row weights (ty, 1-ty) [H] | row source indices [H] |
-    //                hot bytes [h*w] | row masks [h][n_cw] | strip masks [warps][n_rw]
-    double2 *rt_w = reinterpret_cast<double2 *>(sm);
-    uint32_t *rt_idx = reinterpret_cast<uint32_t *>(rt_w + H);
-    uint8_t *hot = reinterpret_cast<uint8_t *>(rt_idx + H);
-    uint32_t *rowmask = reinterpret_cast<uint32_t *>(hot + ((h * w + 15) & ~15));
-    uint32_t *srcmask = rowmask + h * n_cw + warp * n_rw;
-
-    // ---- phase 1: stream the plane -> hot bytes; row table ----
-    const int hw = h * w;
-    if ((hw & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-        const float4 *p4 = reinterpret_cast<const float4 *>(p);
-        uchar4 *hot4 = reinterpret_cast<uchar4 *>(hot);
-        for (int e = threadIdx.x; e < (hw >> 2); e += blockDim.x) {
-            const float4 v = __ldg(p4 + e);
-            hot4[e] = make_uchar4(v.x >= a.thr, v.y >= a.thr, v.z >= a.thr, v.w >= a.thr);
-        }
-    } else {
-        for (int e = threadIdx.x; e < hw; e += blockDim.x) hot[e] = __ldg(p + e) >= a.thr;
-    }
-    for (int y = threadIdx.x; y < H; y += blockDim.x) {
-        int i0, i1;
-        double t, omt;
-        axis_at(y, a.ry, h, i0, i1, t, omt);
-        rt_w[y] = make_double2(t, omt);
-        rt_idx[y] = uint32_t(i0) | (uint32_t(i1) << 16);
-    }
-    __syncthreads();
-    for (int r = warp; r < h; r += n_warps) {
-        for (int q = 0; q < n_cw; ++q) {
-            const int col = (q << 5) + lane;
-            const uint32_t m = __ballot_sync(0xffffffffu, col < w && hot[r * w + col]);
-            if (lane == 0) rowmask[r * n_cw + q] = m;
-        }
-    }
-    __syncthreads();
-
-    // ---- phase 2: strips ----
-    const int n_strips = (a.W + SW - 1) / SW;
-    for (int s = warp; s < n_strips; s += n_warps) {
-        const int x0 = s * SW;
-        const int x = x0 - HALF + lane;                 // this lane's output column
-        const bool in_grid = x >= 0 && x < a.W;
-        const bool useful = lane >= HALF && lane < kWarp - HALF && in_grid;
-        int j0, j1;
-        double tx, omtx;
-        axis_at(min(max(x, 0), a.W - 1), a.rx, w, j0, j1, tx, omtx);
-        // source-column span of the strip's useful columns (lanes HALF and last useful)
-        const int last_useful = min(x0 + SW, a.W) - 1 - (x0 - HALF);
-        const int cj0 = __shfl_sync(0xffffffffu, j0, HALF);
-        const int cj1 = __shfl_sync(0xffffffffu, j1, last_useful);
-        // hot source rows of this strip -> srcmask
-        for (int r0 = 0; r0 < h; r0 += 32) {
-            const int r = r0 + lane;
-            bool any = false;
-            if (r < h) {
-                for (int q = cj0 >> 5; q <= (cj1 >> 5) && !any; ++q) {
-                    const uint32_t m = rowmask[r * n_cw + q];
-                    const int lo = max(cj0 - (q << 5), 0), hi = min(cj1 - (q << 5), 31);
-                    const uint32_t span = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
-                    any = (m & span) != 0u;
-                }
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, any);
-            if (lane == 0) srcmask[r0 >> 5] = bal;
-        }
-        __syncwarp();
-
-        // walk runs of needed output rows (warp-uniform control flow)
-        int run_lo = -1, run_hi = -2;
-        for (int q = 0; q <= n_rw; ++q) {
-            uint32_t m = q < n_rw ? srcmask[q] : 0u;
-            bool flush_final = q == n_rw;
-            while (m || flush_final) {
-                int lo = 0, hi = -1;
-                if (m) {
-                    const int r = (q << 5) + __ffs(m) - 1;
-                    m &= m - 1u;
-                    lo = max(__ldg(a.first_out + r) - HALF, 0);
-                    hi = min(__ldg(a.last_out + r) + HALF, H - 1);
-                    if (run_hi >= run_lo && lo <= run_hi + 1) {   // extend current run
-                        run_hi = max(run_hi, hi);
-                        continue;
-                    }
-                } else {
-                    flush_final = false;
-                }
-                if (run_hi >= run_lo) {
-                    // ---- evaluate rows [run_lo, run_hi] ----
-                    // window index 0 = oldest row; HALF = centre; 2*HALF = newest
-                    float full[WIN], cv[WIN], lm[WIN], rm[WIN];
-#pragma unroll
-                    for (int t = 0; t < WIN; ++t) { full[t] = cv[t] = lm[t] = rm[t] = -INFINITY; }
-                    int ci0 = -1, ci1 = -1;
-                    double hA = 0.0, hB = 0.0;
-                    const int test_lo = run_lo == 0 ? 0 : run_lo + HALF;
-                    const int test_hi = run_hi == H - 1 ? H - 1 : run_hi - HALF;
-                    const int last_eval = run_hi == H - 1 ? run_hi + HALF : run_hi;
-                    for (int y = run_lo; y <= last_eval; ++y) {
-                        float v = -INFINITY;
-                        if (y < H) {
-                            const uint32_t idx = rt_idx[y];
-                            const double2 wy = rt_w[y];
-                            const int i0 = int(idx & 0xffffu), i1 = int(idx >> 16);
-                            if (i0 != ci0) {
-                                hA = (i0 == ci1) ? hB
-                                                 : dadd(dmul((double)__ldg(p + i0 * w + j0), omtx),
-                                                        dmul((double)__ldg(p + i0 * w + j1), tx));
-                                ci0 = i0;
-                            }
-                            if (i1 != ci1) {
-                                hB = (i1 == ci0) ? hA
-                                                 : dadd(dmul((double)__ldg(p + i1 * w + j0), omtx),
-                                                        dmul((double)__ldg(p + i1 * w + j1), tx));
-                                ci1 = i1;
-                            }
-                            const float val = __double2float_rn(dadd(dmul(hA, wy.y), dmul(hB, wy.x)));
-                            v = in_grid ? val : -INFINITY;
-                        }
-                        // row maxima from the neighbouring lanes
-                        float lmax = -INFINITY, rmax = -INFINITY;
-#pragma unroll
-                        for (int d = 1; d <= HALF; ++d) {
-                            lmax = max_nan(lmax, __shfl_up_sync(0xffffffffu, v, d));
-                            rmax = max_nan(rmax, __shfl_down_sync(0xffffffffu, v, d));
-                        }
-#pragma unroll
-                        for (int t = 0; t < WIN - 1; ++t) {
-                            full[t] = full[t + 1]; cv[t] = cv[t + 1];
-                            lm[t] = lm[t + 1]; rm[t] = rm[t + 1];
-                        }
-                        full[WIN - 1] = max_nan(max_nan(lmax, v), rmax);
-                        cv[WIN - 1] = v; lm[WIN - 1] = lmax; rm[WIN - 1] = rmax;
-                        // test the centre row
-                        float earlier = lm[HALF], later = rm[HALF];
-#pragma unroll
-                        for (int t = 0; t < HALF; ++t) {
-                            earlier = max_nan(earlier, full[t]);
-                            later = max_nan(later, full[HALF + 1 + t]);
-                        }
-                        const float c = cv[HALF];
-                        const int yc = y - HALF;
-                        const bool peak = useful && yc >= test_lo && yc <= test_hi && c >= a.thr &&
-                                          c > earlier && c >= later;
-                        if (peak) emit_peak(a.counts, a.peaks, plane, a.cap, c, yc, x);
-                    }
-                }
-                if (hi >= lo) { run_lo = lo; run_hi = hi; }
-                else { run_lo = -1; run_hi = -2; }
-            }
-        }
-        __syncwarp();
-    }
-}
 
 size_t nms_up_win_smem(int h, int w, int H, int threads)
 {
@@ -1006,22 +495,9 @@ cudaError_t launch_nms_up_win(const UpWinArgs &a, int B, cudaStream_t s)
     const long long grid = (long long)B * a.K;
     if (grid == 0) return cudaSuccess;
     const size_t smem = nms_up_win_smem(a.h, a.w, a.H, 128);
-    if (a.variant == 3) {
-        size_t smem3 = (size_t)(((a.h * a.w + 127) & ~127) >> 5) * 4 + (size_t)4 * ((a.h + 31) >> 5) * 4;
-        smem3 = (smem3 + 15) & ~size_t(15);
-        if (a.stage) smem3 += (size_t)a.h * a.w * sizeof(float);
-        if (a.half == 1) k_nms_up_win3<1><<<(unsigned)grid, 128, smem3, s>>>(a);
-        else if (a.half == 2) k_nms_up_win3<2><<<(unsigned)grid, 128, smem3, s>>>(a);
-        else return cudaErrorInvalidValue;
-    } else if (a.variant == 1) {
-        if (a.half == 1) k_nms_up_win<1><<<(unsigned)grid, 128, smem, s>>>(a);
-        else if (a.half == 2) k_nms_up_win<2><<<(unsigned)grid, 128, smem, s>>>(a);
-        else return cudaErrorInvalidValue;
-    } else {
-        if (a.half == 1) k_nms_up_win2<1><<<(unsigned)grid, 128, smem, s>>>(a);
-        else if (a.half == 2) k_nms_up_win2<2><<<(unsigned)grid, 128, smem, s>>>(a);
-        else return cudaErrorInvalidValue;
-    }
+    if (a.half == 1) k_nms_up_win2<1><<<(unsigned)grid, 128, smem, s>>>(a);
+    else if (a.half == 2) k_nms_up_win2<2><<<(unsigned)grid, 128, smem, s>>>(a);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
@@ -1039,12 +515,8 @@ cudaError_t configure_nms_kernels(int max_smem)
 {
     {
         cudaError_t e;
-        if ((e = raise_smem_limit(k_nms_up_win<1>, max_smem)) != cudaSuccess) return e;
-        if ((e = raise_smem_limit(k_nms_up_win<2>, max_smem)) != cudaSuccess) return e;
         if ((e = raise_smem_limit(k_nms_up_win2<1>, max_smem)) != cudaSuccess) return e;
         if ((e = raise_smem_limit(k_nms_up_win2<2>, max_smem)) != cudaSuccess) return e;
-        if ((e = raise_smem_limit(k_nms_up_win3<1>, max_smem)) != cudaSuccess) return e;
-        if ((e = raise_smem_limit(k_nms_up_win3<2>, max_smem)) != cudaSuccess) return e;
     }
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k_nms_up);

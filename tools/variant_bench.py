@@ -14,7 +14,7 @@ paf = torch.from_numpy(paf_h).cuda()[idx.cuda()].contiguous()
 params = pf.ParserParams(upsample=8)
 e = pf.PafParser(topo)
 ref = None
-for variant in [int(v) for v in os.environ.get("VARIANTS", "1,2,3,4").split(",")]:
+for variant in [int(v) for v in os.environ.get("VARIANTS", "2,4").split(",")]:
     e.ctx.set_option(_native.PF_OPT_WIN_VARIANT, variant)
     for _ in range(2):
         e.parse_tensors(conf, paf, 8, params)
