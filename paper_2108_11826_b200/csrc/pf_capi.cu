@@ -666,14 +666,14 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
                 ctx->surv_planes = 0;
                 CU(dev_alloc(&ctx->d_surv, planes * corner_surv_entries_per_plane()));
                 CU(dev_alloc(&ctx->d_surv_n, planes));
-                CU(dev_alloc(&ctx->d_crowd, planes + 1));
+                CU(dev_alloc(&ctx->d_crowd, planes + 2));   // + count + hand-out counter
                 ctx->surv_planes = planes;
             }
             a.surv_out = ctx->d_surv;
             a.surv_n = ctx->d_surv_n;
             a.crowd_list = ctx->d_crowd;
             a.crowd_n = ctx->d_crowd + ctx->surv_planes;
-            CU(cudaMemsetAsync(a.crowd_n, 0, sizeof(int), s));
+            CU(cudaMemsetAsync(a.crowd_n, 0, 2 * sizeof(int), s));
         }
         if (csplit) {
             KernelTimer kt(ctx, kNmsUpScan, 1, s);                          // streaming half

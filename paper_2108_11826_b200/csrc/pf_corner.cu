@@ -1245,7 +1245,10 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
         hot[(h + 1) * nws + e] = 0u;
     }
     float *vb = vbuf + warp * L.vcap;
-    for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
+    // planes handed out dynamically (crowded planes differ widely in cost):
+    // the first by CTA index, the rest from a counter (crowd_n[1])
+    __shared__ int s_next;
+    for (int li = blockIdx.x; li < nlist;) {
         const int plane = __ldcg(a.crowd_list + li);
         if (threadIdx.x == 0) { n_hot = 0; n_cand = 0; n_dense = 0; n_pk = 0; }
         const int fb = plane / a.K, k = plane - fb * a.K;
@@ -1356,7 +1359,12 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
             __syncwarp();
         }
         __syncthreads();
-        if (threadIdx.x == 0) a.counts[plane] = n_pk;
+        if (threadIdx.x == 0) {
+            a.counts[plane] = n_pk;
+            s_next = (int)gridDim.x + atomicAdd(a.crowd_n + 1, 1);
+        }
+        __syncthreads();
+        li = s_next;
     }
 }
 
