@@ -173,6 +173,27 @@ int pf_parse_batch(pf_ctx *ctx, const float *conf, const float *paf, int batch,
 /* Wait for the last parse and expose its results (D2H of the compact pool). */
 int pf_get_results(pf_ctx *ctx, pf_results *out);
 
+/* Caller-owned host results: the same as pf_get_results, with the D2H copies
+ * going straight into the caller's arrays (pinned for full speed) instead of
+ * the context's buffers, so they outlive the next call.  frame_first /
+ * frame_count hold n_frames entries, the human arrays `capacity` humans
+ * (kp_* capacity * K).  If the call produced more than `capacity` humans the
+ * function returns PF_ERR_CAPACITY with *total_humans set to the need and
+ * nothing else written; call again with larger arrays (the parse is not
+ * repeated). */
+typedef struct pf_host_out {
+    int32_t capacity;
+    int32_t *frame_first;          /* [n_frames] */
+    int32_t *frame_count;          /* [n_frames] */
+    double *human_score;           /* [capacity] */
+    int32_t *human_n_parts;        /* [capacity] */
+    double *kp_x;                  /* [capacity * K] */
+    double *kp_y;                  /* [capacity * K] */
+    float *kp_score;               /* [capacity * K] */
+    int32_t *kp_peak;              /* [capacity * K] */
+} pf_host_out;
+int pf_get_results_into(pf_ctx *ctx, const pf_host_out *dst, int32_t *n_frames, int32_t *total_humans);
+
 /* Wait for all work on the context stream. */
 int pf_sync(pf_ctx *ctx);
 

@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = (
     "pf_get_kernel_times", "pf_get_peaks", "pf_get_connections",
     "pf_preprocess_device", "pf_preprocess_f32_device", "pf_resize_device", "pf_host_alloc", "pf_host_free",
     "pf_launch_count", "pf_gaussian_taps", "pf_format_records", "pf_format_float", "pf_render_maps",
-    "pf_overlay", "pf_get_paf_sectors", "pf_parse_batch",
+    "pf_overlay", "pf_get_paf_sectors", "pf_parse_batch", "pf_get_results_into",
 )
 
 
@@ -85,6 +85,21 @@ class PfResults(ctypes.Structure):
         ("kp_y", ctypes.POINTER(ctypes.c_double)),
         ("kp_score", ctypes.POINTER(ctypes.c_float)),
         ("kp_peak", ctypes.POINTER(ctypes.c_int32)),
+    ]
+
+
+class PfHostOut(ctypes.Structure):
+    """pf_host_out: caller-owned host arrays for pf_get_results_into."""
+    _fields_ = [
+        ("capacity", ctypes.c_int32),
+        ("frame_first", ctypes.c_void_p),
+        ("frame_count", ctypes.c_void_p),
+        ("human_score", ctypes.c_void_p),
+        ("human_n_parts", ctypes.c_void_p),
+        ("kp_x", ctypes.c_void_p),
+        ("kp_y", ctypes.c_void_p),
+        ("kp_score", ctypes.c_void_p),
+        ("kp_peak", ctypes.c_void_p),
     ]
 
 
@@ -133,6 +148,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.pf_parse_host.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int,
                                       ctypes.POINTER(PfParams), ctypes.POINTER(PfResults)]
         lib.pf_get_results.argtypes = [vp, ctypes.POINTER(PfResults)]
+        lib.pf_get_results_into.argtypes = [vp, ctypes.POINTER(PfHostOut), ctypes.POINTER(i32),
+                                            ctypes.POINTER(i32)]
         lib.pf_parse_batch.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, ctypes.POINTER(PfParams),
                                        ctypes.POINTER(PfOut), vp]
         lib.pf_sync.argtypes = [vp]

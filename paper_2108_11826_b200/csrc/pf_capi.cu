@@ -244,6 +244,7 @@ struct pf_ctx {
     int last_batch = 0;
     int last_K = 0;
     bool results_ready = false;
+    bool status_ready = false;              // h_status holds the last call's final status
 
     // the last parse call, replayed once with a larger output pool when the
     // default pool (64 humans/frame) overflows and no fixed cap was requested
@@ -900,6 +901,7 @@ int begin_call(pf_ctx *ctx, int batch, int pool_cap)
     *ctx->h_status = init;
     CU(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, ctx->stream));
     ctx->results_ready = false;
+    ctx->status_ready = false;
     return PF_OK;
 }
 
@@ -1609,6 +1611,52 @@ int pf_parse_batch(pf_ctx *ctx, const float *conf, const float *paf, int batch, 
                                                             ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp, *out);
         CU(cudaGetLastError());
     }
+    return PF_OK;
+}
+
+int pf_get_results_into(pf_ctx *ctx, const pf_host_out *dst, int32_t *n_frames, int32_t *total_humans)
+{
+    if (!ctx || !dst || !n_frames || !total_humans) return PF_ERR_CONTRACT;
+    if (dst->capacity < 0) return fail(ctx, PF_ERR_CONTRACT, "pf_get_results_into: negative capacity");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    // the status (and, on a capacity overflow, the grow + replay) as pf_get_results
+    if (!ctx->results_ready && !ctx->status_ready) {
+        CU(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        const Status st = *ctx->h_status;
+        if (st.code == PF_ERR_CAPACITY) {
+            pf_results tmp;                      // grows, replays and reports exactly like pf_get_results
+            rc = pf_get_results(ctx, &tmp);
+            if (rc) return rc;
+        }
+        ctx->status_ready = true;
+    }
+    const int B = ctx->last_batch;
+    const int K = ctx->last_K;
+    const int total = ctx->h_status->pool_used;
+    *n_frames = B;
+    *total_humans = total;
+    if (total > dst->capacity) return PF_ERR_CAPACITY;   // no message: the caller grows its arrays
+    if (B > 0 && (!dst->frame_first || !dst->frame_count))
+        return fail(ctx, PF_ERR_CONTRACT, "pf_get_results_into: null frame arrays");
+    if (total > 0 && (!dst->human_score || !dst->human_n_parts || !dst->kp_x || !dst->kp_y || !dst->kp_score ||
+                      !dst->kp_peak))
+        return fail(ctx, PF_ERR_CONTRACT, "pf_get_results_into: null human arrays");
+    if (B > 0) {
+        CU(cudaMemcpyAsync(dst->frame_first, ctx->d_frame_first, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(dst->frame_count, ctx->d_frame_count, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (total > 0) {
+        const size_t t = (size_t)total;
+        CU(cudaMemcpyAsync(dst->human_score, ctx->d_hscore, sizeof(double) * t, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(dst->human_n_parts, ctx->d_hnparts, sizeof(int) * t, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(dst->kp_x, ctx->d_kpx, sizeof(double) * t * K, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(dst->kp_y, ctx->d_kpy, sizeof(double) * t * K, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(dst->kp_score, ctx->d_kps, sizeof(float) * t * K, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(dst->kp_peak, ctx->d_kpp, sizeof(int) * t * K, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
     return PF_OK;
 }
 

@@ -115,6 +115,28 @@ class BatchResult:
                                  n_parts=int(self.human_n_parts[h])))
         return out
 
+    @classmethod
+    def _from_block(cls, block: "_HostBlock", n: int, total: int, k: int) -> "BatchResult":
+        """Views into a pinned block that pf_get_results_into filled (no copy);
+        the block returns to its pool once every view of it is gone."""
+        self = cls.__new__(cls)
+        self.n_frames, self.total_humans, self.n_keypoints = n, total, k
+        buf = block.buffer()
+        off = block.offsets(n, block.capacity, k)
+
+        def view(name, count, dtype):
+            return np.frombuffer(buf, dtype=dtype, count=count, offset=off[name])
+
+        self.frame_first = view("ff", n, np.int32)
+        self.frame_count = view("fc", n, np.int32)
+        self.human_score = view("hs", total, np.float64)
+        self.human_n_parts = view("hn", total, np.int32)
+        self.kp_x = view("kx", total * k, np.float64).reshape(total, k)
+        self.kp_y = view("ky", total * k, np.float64).reshape(total, k)
+        self.kp_score = view("ks", total * k, np.float32).reshape(total, k)
+        self.kp_peak = view("kp", total * k, np.int32).reshape(total, k)
+        return self
+
     def all_poses(self) -> List[List[HumanPose]]:
         return [self.poses(f) for f in range(self.n_frames)]
 
@@ -122,6 +144,74 @@ class BatchResult:
         """``pose_record(seq_base + f, poses(f), topo)`` for every frame, built
         natively from the SoA arrays (byte-identical; no HumanPose objects)."""
         return format_records(self, topo, seq_base)
+
+
+class _HostBlock:
+    """One pinned host block holding a parse_arrays result (pf_host_out)."""
+
+    def __init__(self, pool: "_HostPool", ptr: int, nbytes: int, frames: int, capacity: int, k: int):
+        self.pool, self.ptr, self.nbytes = pool, ptr, nbytes
+        self.frames, self.capacity, self.k = frames, capacity, k
+
+    @staticmethod
+    def offsets(frames: int, capacity: int, k: int) -> dict:
+        off, o = {}, 0
+        for name, size in (("ff", 4 * frames), ("fc", 4 * frames), ("hs", 8 * capacity), ("hn", 4 * capacity),
+                           ("kx", 8 * capacity * k), ("ky", 8 * capacity * k), ("ks", 4 * capacity * k),
+                           ("kp", 4 * capacity * k)):
+            off[name] = o
+            o += (size + 63) & ~63
+        off["_total"] = o
+        return off
+
+    def native(self) -> "_native.PfHostOut":
+        off = self.offsets(self.frames, self.capacity, self.k)
+        p = self.ptr
+        return _native.PfHostOut(self.capacity, p + off["ff"], p + off["fc"], p + off["hs"], p + off["hn"],
+                                 p + off["kx"], p + off["ky"], p + off["ks"], p + off["kp"])
+
+    def buffer(self):
+        """A fresh ctypes view of the block; the block goes back to the pool
+        when it (and every numpy array built on it) is collected."""
+        import weakref
+
+        buf = (ctypes.c_char * self.nbytes).from_address(self.ptr)
+        weakref.finalize(buf, self.pool.give, self.ptr, self.nbytes)
+        return buf
+
+
+class _HostPool:
+    """Recycled pinned blocks for parse_arrays results (pf_host_alloc): the
+    device-to-host copies land in the result's own memory (no host copy), and
+    a block is reused only after its BatchResult and all views are gone."""
+
+    def __init__(self, lib, keep: int = 3):
+        self.lib, self.keep = lib, keep
+        self.free: List[tuple] = []
+        self.lock = threading.Lock()
+
+    def take(self, frames: int, capacity: int, k: int) -> _HostBlock:
+        need = _HostBlock.offsets(frames, capacity, k)["_total"]
+        with self.lock:
+            fit = [b for b in self.free if b[1] >= need]
+            if fit:
+                best = min(fit, key=lambda b: b[1])
+                self.free.remove(best)
+                ptr, nbytes = best
+            else:
+                nbytes = need
+                ptr = self.lib.pf_host_alloc(nbytes)
+                if not ptr:
+                    raise DeviceError(f"pf_host_alloc({nbytes}) failed")
+        return _HostBlock(self, ptr, nbytes, frames, capacity, k)
+
+    def give(self, ptr: int, nbytes: int) -> None:
+        with self.lock:
+            self.free.append((ptr, nbytes))
+            while len(self.free) > self.keep:
+                p, _ = min(self.free, key=lambda b: b[1])
+                self.free.remove((p, _))
+                self.lib.pf_host_free(p)
 
 
 class PafParser:
@@ -141,6 +231,8 @@ class PafParser:
         # temporaries): pf_get_results may replay the call from them when an
         # automatic capacity grows, so they stay alive until results() returns
         self._inflight = None
+        self._host_pool = _HostPool(self.ctx.lib)
+        self._host_cap = 0
         if debug:
             self.set_debug(True)
 
@@ -184,14 +276,32 @@ class PafParser:
         conf = np.ascontiguousarray(conf, dtype=np.float32)
         paf = np.ascontiguousarray(paf, dtype=np.float32)
         self._check_arrays(conf.shape, paf.shape, stride)
-        res = _native.PfResults()
         p = params.to_native()
         b, _, h, w = conf.shape
         self.ctx.check(self.ctx.lib.pf_parse_host(
             self.ctx.handle, conf.ctypes.data if conf.size else None,
             paf.ctypes.data if paf.size else None, b, h, w, int(stride),
-            ctypes.byref(p), ctypes.byref(res)))
-        return BatchResult(res)
+            ctypes.byref(p), None))
+        return self._host_results(b)
+
+    def _host_results(self, frames: int) -> BatchResult:
+        """pf_get_results_into a pooled pinned block sized for the call."""
+        k = self.topo.n_keypoints
+        cap = max(self._host_cap, 4 * frames, 16)
+        n_frames, total = ctypes.c_int32(), ctypes.c_int32()
+        while True:
+            block = self._host_pool.take(frames, cap, k)
+            dst = block.native()
+            rc = self.ctx.lib.pf_get_results_into(self.ctx.handle, ctypes.byref(dst), ctypes.byref(n_frames),
+                                                  ctypes.byref(total))
+            if rc == _native.PF_ERR_CAPACITY and total.value > cap:
+                self._host_pool.give(block.ptr, block.nbytes)
+                cap = self._host_cap = max(total.value, 2 * cap)
+                continue
+            if rc:
+                self._host_pool.give(block.ptr, block.nbytes)
+                self.ctx.check(rc)
+            return BatchResult._from_block(block, n_frames.value, total.value, k)
 
     def parse_device(self, conf_ptr: int, paf_ptr: int, batch: int, grid_h: int, grid_w: int,
                      stride: int, params: ParserParams) -> None:
@@ -297,6 +407,10 @@ class PafParser:
                 for q in range(n.value)]
 
     def close(self) -> None:
+        with self._host_pool.lock:
+            for ptr, _ in self._host_pool.free:
+                self.ctx.lib.pf_host_free(ptr)
+            self._host_pool.free.clear()
         self.ctx.close()
 
 
