@@ -835,7 +835,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         CU(cudaMemsetAsync(ctx->d_crowd_frames + ctx->split_frames, 0, sizeof(int), s));
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }
-    const int threads = psplit ? kParseFinThreads : kParseThreads;
+    const int threads = psplit ? kParseFinThreads
+                               : (n <= kParseWideFrames && !ctx->count_paf ? kParseWideThreads : kParseThreads);
     const size_t smem =
         parse_smem_bytes(a.cap_frame, a.cap_part, a.cap_cands, a.cap_humans, K, ctx->topo.L, threads / 32, psplit);
     if (a.split) {

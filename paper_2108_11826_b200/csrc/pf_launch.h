@@ -202,11 +202,20 @@ constexpr int kParseThreads = PF_PARSE_THREADS;   // k_parse_frames CTA size
 #endif
 constexpr int kParseFinThreads = PF_PARSE_FIN_THREADS;   // k_parse_frames<true> (split finish) CTA size
 constexpr int kParseCrowdThreads = 512;                  // k_parse_crowd (crowded frames of the split parse)
+#ifndef PF_PARSE_WIDE_THREADS
+#define PF_PARSE_WIDE_THREADS 512
+#endif
+constexpr int kParseWideThreads = PF_PARSE_WIDE_THREADS;  // k_parse_frames_wide (small one-kernel batches)
+#ifndef PF_PARSE_WIDE_FRAMES
+#define PF_PARSE_WIDE_FRAMES 31   // device calls from 32 frames take the split parse
+#endif
+constexpr int kParseWideFrames = PF_PARSE_WIDE_FRAMES;    // batches up to this many frames take it
 #ifndef PF_CAND_SMEM_CROWD
 #define PF_CAND_SMEM_CROWD 4096
 #endif
 constexpr int kCandSmemCrowd = PF_CAND_SMEM_CROWD;       // candidates in shared memory per crowded frame
 constexpr int kParseMaxThreads = kParseCrowdThreads > kParseThreads ? kParseCrowdThreads : kParseThreads;
+static_assert(kParseWideThreads <= kParseMaxThreads, "per-thread tables are sized for kParseMaxThreads");
 size_t cand_spill_bytes_per_frame(int cap_cands);
 size_t cand_record_bytes();
 enum { kCapPart = 1, kCapFrame = 2, kCapCands = 3, kCapHumans = 4, kCapPool = 5 };

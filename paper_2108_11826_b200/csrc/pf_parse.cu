@@ -780,6 +780,16 @@ k_parse_frames(const ParseArgs a)
     parse_frame<SPLIT, COUNT, false>(a, blockIdx.x);
 }
 
+// Small batches (fewer frames than SMs): the one-kernel parse with a wide
+// CTA per frame, so the line integrals of a frame's pairs run in one round
+// instead of several (single-frame latency; same function, same results).
+__global__ void __launch_bounds__(kParseWideThreads, 1)
+k_parse_frames_wide(const ParseArgs a)
+{
+    pdl_wait();
+    parse_frame<false, false, false>(a, blockIdx.x);
+}
+
 // Crowded frames listed by k_parse_frames<true> (persistent over the list).
 __global__ void __launch_bounds__(kParseCrowdThreads, 1)
 k_parse_crowd(const ParseArgs a)
@@ -1031,6 +1041,7 @@ cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t s
         return cudaGetLastError();
     }
     if (a.paf_touch) k_parse_frames<false, true><<<B, threads, smem, s>>>(a);
+    else if (threads == kParseWideThreads) k_parse_frames_wide<<<B, threads, smem, s>>>(a);
     else k_parse_frames<false><<<B, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -1068,6 +1079,10 @@ cudaError_t configure_parse_kernels(int max_smem)
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_frames<true>);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_parse_frames<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_frames_wide);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_parse_frames_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem - (int)fa.sharedSizeBytes);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_parse_crowd);
     if (e == cudaSuccess)
