@@ -222,7 +222,8 @@ int pf_set_debug(pf_ctx *ctx, int enable);
 #define PF_OPT_PAF_ZERO_COPY 8   /* pf_parse_host (default 1): a pinned host PAF is read in place by the
                                     parse kernel, so only the sampled cells cross PCIe; 0: copy it whole */
 #define PF_OPT_PDL 12             /* bitmask: programmatic dependent launch per split-kernel launch site
-                                    (process-wide A/B; default 0 = measured fastest) */
+                                    (process-wide A/B; default: only the small-batch wide parse, bit 6 --
+                                    every edge of the big-batch split path measured slower) */
 #define PF_OPT_COUNT_PAF 13       /* instrumented parse: count the 32-byte PAF sectors the line integral
                                     reads (one-kernel parse; read with pf_get_paf_sectors) */
 #define PF_OPT_LARGE 15           /* 1: parse through the large-frame kernel (HBM tables, 32-bit ids), the

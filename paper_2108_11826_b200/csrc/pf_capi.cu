@@ -24,7 +24,10 @@
 using namespace pf;
 
 namespace pf {
-int g_pdl_mask = 0;
+#ifndef PF_PDL_DEFAULT
+#define PF_PDL_DEFAULT (1 << kPdlParseWide)   // small batches: the parse launch overlaps the NMS tail
+#endif
+int g_pdl_mask = PF_PDL_DEFAULT;
 }
 
 #ifndef PF_CORNER_SPLIT_DEFAULT

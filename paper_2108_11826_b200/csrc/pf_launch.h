@@ -21,7 +21,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // 1.99 ms/step against 1.40 ms with none (the early-resident dependents slow
 // the running grid), so the default is 0.
 extern int g_pdl_mask;
-enum PdlSite { kPdlFinish = 0, kPdlCrowded, kPdlParsePeaks, kPdlPairScan, kPdlScorePairs, kPdlParseFrames };
+enum PdlSite { kPdlFinish = 0, kPdlCrowded, kPdlParsePeaks, kPdlPairScan, kPdlScorePairs, kPdlParseFrames,
+               kPdlParseWide };
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(int site, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -1041,7 +1041,8 @@ cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t s
         return cudaGetLastError();
     }
     if (a.paf_touch) k_parse_frames<false, true><<<B, threads, smem, s>>>(a);
-    else if (threads == kParseWideThreads) k_parse_frames_wide<<<B, threads, smem, s>>>(a);
+    else if (threads == kParseWideThreads)
+        return launch_pdl(kPdlParseWide, k_parse_frames_wide, dim3(B), dim3(threads), smem, s, a);
     else k_parse_frames<false><<<B, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
