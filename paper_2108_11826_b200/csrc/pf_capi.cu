@@ -40,6 +40,10 @@ int g_pdl_mask = PF_PDL_DEFAULT;
 #define PF_SPLIT_MIN_FRAMES 32   // C4 (32 frames of 135x240 maps): 136k frames/s split vs 131k
 #endif
 constexpr int kSplitMinFrames = PF_SPLIT_MIN_FRAMES;   // split option 1 (auto): batches of at least this many frames
+#ifndef PF_CORNER_SPLIT_MIN_FRAMES
+#define PF_CORNER_SPLIT_MIN_FRAMES 256   // measured: one-kernel corner faster up to 128 frames (C2 64: 113 -> 98 us), equal at 256
+#endif
+constexpr int kCornerSplitMinFrames = PF_CORNER_SPLIT_MIN_FRAMES;   // the same for the Mode U scan + finish split
 
 namespace {
 
@@ -659,7 +663,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
             CU(dev_alloc(&ctx->d_corner_spill, nms_up_corner_spill_entries(ctx->sms * 16)));
         a.cand_spill = ctx->d_corner_spill;
         // split kernels pay off on batches; a few frames take the one-kernel path (fewer launches)
-        const bool csplit = ctx->corner_split == 2 || (ctx->corner_split == 1 && (n >= kSplitMinFrames || big));
+        const bool csplit = ctx->corner_split == 2 || (ctx->corner_split == 1 && (n >= kCornerSplitMinFrames || big || two));
+        // (beside the parse stream the split kernels measured 1 % faster on 128-frame chunks)
         if (csplit) {
             const size_t planes = (size_t)n * K;
             if (planes > ctx->surv_planes) {

@@ -252,7 +252,8 @@ def test_crowded_plane_kernel_stress(topo, grid, patch):
     non-monotone, hot-list / dense-list overflow on the 135x240 grid, which
     is also too large to stage in shared memory) and ties from quantised
     noise — against the materialised path (resize + plane NMS over HBM maps)
-    through the default split path (32 frames)."""
+    through the split path (forced: 32 frames of 46x82 maps would take the
+    one-kernel corner form by default)."""
     rng = np.random.default_rng(grid[0] + patch)
     F, K = 32, topo.n_keypoints
     h, w = grid
@@ -266,6 +267,7 @@ def test_crowded_plane_kernel_stress(topo, grid, patch):
             conf[f, k, y0:y0 + patch, x0:x0 + patch] = m
     paf = np.zeros((F, 2 * topo.n_limbs, h, w), np.float32)
     e = pf.PafParser(topo, debug=True)
+    e.ctx.set_option(pf._native.PF_OPT_CORNER_SPLIT, 2)
     params = pf.ParserParams(upsample=8)
     e.set_timing(True)
     e.kernel_times(reset=True)

@@ -23,8 +23,12 @@ del conf_d, paf_d
 params = pf.ParserParams(upsample=8)
 eng = pf.PafParser(topo)
 ref = None
+import os
+CS = [int(x) for x in os.environ.get("CORNER_SPLIT", "1").split(",")]
 for zc in (1, 0):
     for ov in (0, 1):
+      for cs in CS:
+        eng.ctx.set_option(_native.PF_OPT_CORNER_SPLIT, cs)
         eng.ctx.set_option(_native.PF_OPT_PAF_ZERO_COPY, zc)
         eng.ctx.set_option(_native.PF_OPT_HOST_OVERLAP, ov)
         r = eng.parse_arrays(pin_conf.array, pin_paf.array, 8, params)
@@ -36,5 +40,5 @@ for zc in (1, 0):
             for _ in range(3):
                 eng.parse_arrays(pin_conf.array, pin_paf.array, 8, params)
             best = min(best, (time.perf_counter() - t0) / 3)
-        print(f"paf_zero_copy={zc} host_overlap={ov}: {E / best:.0f} frames/s ({best * 1e3:.2f} ms)  digest {dg} "
+        print(f"paf_zero_copy={zc} host_overlap={ov} corner_split={cs}: {E / best:.0f} frames/s ({best * 1e3:.2f} ms)  digest {dg} "
               f"{'OK' if dg == ref else 'DIFFERS'}", flush=True)
