@@ -36,10 +36,12 @@ int g_pdl_mask = PF_PDL_DEFAULT;
 #ifndef PF_PARSE_SPLIT_DEFAULT
 #define PF_PARSE_SPLIT_DEFAULT 1
 #endif
-#ifndef PF_SPLIT_MIN_FRAMES
-#define PF_SPLIT_MIN_FRAMES 32   // C4 (32 frames of 135x240 maps): 136k frames/s split vs 131k
-#endif
-constexpr int kSplitMinFrames = PF_SPLIT_MIN_FRAMES;   // split option 1 (auto): batches of at least this many frames
+// Parse split option 1 (auto): batches with more frames than SMs take the
+// split parse; up to one frame per SM, the one-kernel parse with a wide
+// (512-thread) CTA per frame runs them in one wave and measured faster
+// (C2 64 frames 98.9 -> 80.4 us per call, C4 147k -> 185k frames/s, equal
+// just past the SM count; the 128-thread one-kernel form needed the split
+// parse from 32 frames).
 #ifndef PF_CORNER_SPLIT_MIN_FRAMES
 #define PF_CORNER_SPLIT_MIN_FRAMES 256   // measured: one-kernel corner faster up to 128 frames (C2 64: 113 -> 98 us), equal at 256
 #endif
@@ -144,6 +146,7 @@ constexpr int kHostSlots = PF_HOST_SLOTS;   // device input slots of pf_parse_ho
 struct Sched {
     cudaStream_t nms, parse;
     int set;
+    bool wide;      // small batches may take the wide one-kernel parse (device-resident PAF)
 };
 
 struct pf_ctx {
@@ -825,7 +828,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         if (two) CU(cudaEventRecord(ctx->ev_parsed[sc.set], s));
         return PF_OK;
     }
-    const bool psplit = !ctx->count_paf && (ctx->parse_split == 2 || (ctx->parse_split == 1 && n >= kSplitMinFrames));
+    const bool psplit = !ctx->count_paf && (ctx->parse_split == 2 || (ctx->parse_split == 1 && n > ctx->sms));
     if (ctx->count_paf && L > 0) {
         a.paf_touch = ctx->d_paf_touch;
         a.touch_words = (int)(((size_t)2 * L * h * w + 255) / 256);   // 8 floats per sector, 32 sectors per word
@@ -844,7 +847,10 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }
     const int threads = psplit ? kParseFinThreads
-                               : (n <= kParseWideFrames && !ctx->count_paf ? kParseWideThreads : kParseThreads);
+                               : (n <= ctx->sms && !ctx->count_paf && sc.wide ? kParseWideThreads : kParseThreads);
+    // (the host path keeps the 128-thread form: its PAF read in place over PCIe
+    // is request-rate bound, and beside the overlapped NMS stream the narrow
+    // CTAs leave room for the next chunk's kernels -- 137-140k vs 131-137k e2e)
     const size_t smem =
         parse_smem_bytes(a.cap_frame, a.cap_part, a.cap_cands, a.cap_humans, K, ctx->topo.L, threads / 32, psplit);
     if (a.split) {
@@ -1335,7 +1341,7 @@ int pf_parse_device(pf_ctx *ctx, const float *conf, const float *paf, int batch,
     for (int f0 = 0; f0 < batch; f0 += chunk) {
         const int n = batch - f0 < chunk ? batch - f0 : chunk;
         rc = run_chunk(ctx, conf + (size_t)f0 * conf_frame, paf + (size_t)f0 * paf_frame, n, f0,
-                       grid_h, grid_w, stride, p, rows, cols, pool, Sched{ctx->stream, ctx->stream, 0});
+                       grid_h, grid_w, stride, p, rows, cols, pool, Sched{ctx->stream, ctx->stream, 0, true});
         if (rc) return rc;
     }
     return PF_OK;
@@ -1521,7 +1527,8 @@ int pf_parse_host(pf_ctx *ctx, const float *conf, const float *paf, int batch, i
         rc = run_chunk(ctx, conf_dev ? conf_dev + (size_t)f0 * conf_frame : dconf,
                        paf_dev ? paf_dev + (size_t)f0 * paf_frame : dpaf, n, f0, grid_h, grid_w,
                        stride, p, rows, cols, pool,
-                       ov ? Sched{ctx->stream, ctx->parse_stream, ci & 1} : Sched{ctx->stream, ctx->stream, 0});
+                       ov ? Sched{ctx->stream, ctx->parse_stream, ci & 1, false}
+                          : Sched{ctx->stream, ctx->stream, 0, false});
         if (rc) return rc;
         // the slot is free once its last reader is done: the NMS stage, or the
         // parse when the PAF was copied into the slot

@@ -207,10 +207,7 @@ constexpr int kParseCrowdThreads = 512;                  // k_parse_crowd (crowd
 #define PF_PARSE_WIDE_THREADS 512
 #endif
 constexpr int kParseWideThreads = PF_PARSE_WIDE_THREADS;  // k_parse_frames_wide (small one-kernel batches)
-#ifndef PF_PARSE_WIDE_FRAMES
-#define PF_PARSE_WIDE_FRAMES 31   // device calls from 32 frames take the split parse
-#endif
-constexpr int kParseWideFrames = PF_PARSE_WIDE_FRAMES;    // batches up to this many frames take it
+
 #ifndef PF_CAND_SMEM_CROWD
 #define PF_CAND_SMEM_CROWD 4096
 #endif

@@ -349,7 +349,7 @@ def test_pinned_paf_read_in_place(topo, up):
     scenes = [synth.procedural_scene(12, s, 656, 368, SP) for s in range(5)] + [synth.crowd_scene(4, 0)]
     conf, paf = render(scenes, topo)
     reps = 46                                          # 276 frames: host chunks of 128, 128 and 20 frames
-                                                       # (the last below the split threshold: one-kernel NMS)
+                                                       # (a partial chunk at the end)
     pc = pf._native.PinnedArray((len(scenes) * reps,) + conf.shape[1:])
     pp = pf._native.PinnedArray((len(scenes) * reps,) + paf.shape[1:])
     pc.array[:] = np.concatenate([conf] * reps)

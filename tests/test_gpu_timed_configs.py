@@ -1,10 +1,11 @@
 """Parity on exactly the kernel paths the benchmark times.
 
-The bench times large batches (C3: 256 crowded frames, C4: 32 frames of
-135x240 maps, C5: 8192 frames), which take the split kernels
-(``k_nms_up_scan`` -> ``k_corner_finish`` / ``k_corner_crowded`` and
-``k_parse_peaks`` -> ``k_score_pairs`` -> ``k_parse_frames<true>``), not
-the one-kernel forms that small test batches take.  Every frame here is
+The bench times C3 (256 crowded frames) and C5 (8192 frames), which take the
+split kernels (``k_nms_up_scan`` -> ``k_corner_finish`` / ``k_corner_crowded``
+and ``k_parse_peaks`` -> ``k_score_pairs`` -> ``k_parse_frames<true>``), and
+C4 (32 frames of 135x240 maps: the split NMS kernels, the wide one-kernel
+parse — at most one frame per SM), not the forms that small test batches
+take.  Every frame here is
 compared with the oracle (``paf.py:292-305`` composed with
 ``operators.py:79-107`` for Mode U), and the launch counters prove which
 kernels ran.  Also: a 32-keypoint topology through the split parse (the
@@ -88,9 +89,12 @@ def test_c3_mode_r_256_crowded_split_path(topo):
     eng.close()
 
 
+@pytest.mark.parametrize("parse_split", [1, 2])
 @pytest.mark.parametrize("people", [6, 40])
-def test_c4_mode_u_batch32_split_path(topo, people):
-    """BASELINE configs[3] as timed: 32 frames of 135x240 maps, Mode U (-> 1080x1920)."""
+def test_c4_mode_u_batch32_split_path(topo, people, parse_split):
+    """BASELINE configs[3] as timed: 32 frames of 135x240 maps, Mode U (-> 1080x1920):
+    the split NMS kernels with the default (wide one-kernel) parse and with
+    the split parse forced."""
     if people == 6:
         scenes = [synth.GroundTruthScene(synth.crowd_scene(9, s, 1920, 1080, 6, (300.0, 500.0)).humans, 1920, 1080)
                   for s in range(32)]
@@ -100,9 +104,11 @@ def test_c4_mode_u_batch32_split_path(topo, people):
     assert conf.shape == (32, 19, 135, 240)
     params = pf.ParserParams(upsample=8)
     eng = pf.PafParser(topo)
+    eng.ctx.set_option(pf._native.PF_OPT_PARSE_SPLIT, parse_split)
     device_parse(eng, conf, paf, params)
     res, launches = device_parse(eng, conf, paf, params)
-    assert launches.get("k_nms_up_scan", 0) >= 1 and launches.get("k_score_pairs", 0) >= 1, launches
+    assert launches.get("k_nms_up_scan", 0) >= 1, launches
+    assert (launches.get("k_score_pairs", 0) >= 1) == (parse_split == 2), launches
     assert records(res, topo) == oracle_records(conf, paf, topo, params)
     eng.close()
 
@@ -133,16 +139,19 @@ def _chain_scenes(k, frames, seed, w=656, h=368):
     return scenes
 
 
+@pytest.mark.parametrize("parse_split", [2, 1])
 @pytest.mark.parametrize("k", [32, 31])
 @pytest.mark.parametrize("up", [1, 8])
-def test_max_keypoints_topology_split_parse(k, up):
-    """PF_MAX_KEYPOINTS = 32 parts through the split parse (>= 32 frames)."""
+def test_max_keypoints_topology_split_parse(k, up, parse_split):
+    """PF_MAX_KEYPOINTS = 32 parts through the split parse (forced) and the
+    default (wide one-kernel) parse of 40 frames."""
     topo = _chain_topology(k)
     conf, paf = synth.render_batch(_chain_scenes(k, 40, 100 + k), topo, SP)
     params = pf.ParserParams(upsample=up, min_parts=4)
     eng = pf.PafParser(topo)
+    eng.ctx.set_option(pf._native.PF_OPT_PARSE_SPLIT, parse_split)
     res, launches = device_parse(eng, conf, paf, params)
-    assert launches.get("k_parse_peaks", 0) >= 1, launches
+    assert (launches.get("k_parse_peaks", 0) >= 1) == (parse_split == 2), launches
     assert records(res, topo) == oracle_records(conf, paf, topo, params)
     assert res.total_humans >= 40
     eng.close()
