@@ -36,6 +36,9 @@ int g_pdl_mask = PF_PDL_DEFAULT;
 #ifndef PF_PARSE_SPLIT_DEFAULT
 #define PF_PARSE_SPLIT_DEFAULT 1
 #endif
+#ifndef PF_WIDE_FRAMES_PER_SM
+#define PF_WIDE_FRAMES_PER_SM 1
+#endif
 // Parse split option 1 (auto): batches with more frames than SMs take the
 // split parse; up to one frame per SM, the one-kernel parse with a wide
 // (512-thread) CTA per frame runs them in one wave and measured faster
@@ -828,7 +831,7 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         if (two) CU(cudaEventRecord(ctx->ev_parsed[sc.set], s));
         return PF_OK;
     }
-    const bool psplit = !ctx->count_paf && (ctx->parse_split == 2 || (ctx->parse_split == 1 && n > ctx->sms));
+    const bool psplit = !ctx->count_paf && (ctx->parse_split == 2 || (ctx->parse_split == 1 && n > ctx->sms * PF_WIDE_FRAMES_PER_SM));
     if (ctx->count_paf && L > 0) {
         a.paf_touch = ctx->d_paf_touch;
         a.touch_words = (int)(((size_t)2 * L * h * w + 255) / 256);   // 8 floats per sector, 32 sectors per word
@@ -847,7 +850,8 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         a.cand_g = reinterpret_cast<Cand *>(ctx->d_spill);
     }
     const int threads = psplit ? kParseFinThreads
-                               : (n <= ctx->sms && !ctx->count_paf && sc.wide ? kParseWideThreads : kParseThreads);
+                               : (n <= ctx->sms * PF_WIDE_FRAMES_PER_SM && !ctx->count_paf && sc.wide ? kParseWideThreads
+                                                                                    : kParseThreads);
     // (the host path keeps the 128-thread form: its PAF read in place over PCIe
     // is request-rate bound, and beside the overlapped NMS stream the narrow
     // CTAs leave room for the next chunk's kernels -- 137-140k vs 131-137k e2e)
