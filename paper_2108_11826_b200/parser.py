@@ -189,6 +189,7 @@ class _HostPool:
         self.lib, self.keep = lib, keep
         self.free: List[tuple] = []
         self.lock = threading.Lock()
+        self.closed = False
 
     def take(self, frames: int, capacity: int, k: int) -> _HostBlock:
         need = _HostBlock.offsets(frames, capacity, k)["_total"]
@@ -207,6 +208,9 @@ class _HostPool:
 
     def give(self, ptr: int, nbytes: int) -> None:
         with self.lock:
+            if self.closed:                      # the parser is gone: nothing will reuse it
+                self.lib.pf_host_free(ptr)
+                return
             self.free.append((ptr, nbytes))
             while len(self.free) > self.keep:
                 p, _ = min(self.free, key=lambda b: b[1])
@@ -411,6 +415,7 @@ class PafParser:
             for ptr, _ in self._host_pool.free:
                 self.ctx.lib.pf_host_free(ptr)
             self._host_pool.free.clear()
+            self._host_pool.closed = True        # blocks of live results are freed when they die
         self.ctx.close()
 
 
