@@ -45,11 +45,25 @@ __device__ __forceinline__ void emit_peak(int *counts, uint2 *peaks, int plane, 
     if (slot < cap) peaks[(size_t)plane * cap + slot] = pack_peak(v, i, j);
 }
 
+// The same with the plane's counter in shared memory (one CTA per plane).
+__device__ __forceinline__ void emit_peak_s(int *npk, uint2 *peaks, int plane, int cap, float v, int i, int j)
+{
+    const int slot = atomicAdd(npk, 1);
+    if (slot < cap) peaks[(size_t)plane * cap + slot] = pack_peak(v, i, j);
+}
+
 // conf: [B][C][H][W]; planes are (b, k) for k < K; plane index = b*K + k.
+// One CTA per plane: the peak count lives in shared memory (crowded planes
+// emit tens of peaks; a global atomic each serialised them) and is stored
+// once at the end.
 __global__ void __launch_bounds__(256)
 k_nms_plane(const float *__restrict__ conf, int C, int K, int H, int W, float thr, int half,
             int cap, int *__restrict__ counts, uint2 *__restrict__ peaks)
 {
+    __shared__ int s_npk;
+    if (threadIdx.x == 0) s_npk = 0;
+    __syncthreads();
+    int *const npk = &s_npk;
     const int plane = blockIdx.x;
     const int b = plane / K, k = plane - b * K;
     const float *p = conf + ((size_t)b * C + k) * (size_t)H * W;
@@ -94,7 +108,7 @@ k_nms_plane(const float *__restrict__ conf, int C, int K, int H, int W, float th
                         const float r = j == W - 1 ? -INFINITY : (q < 3 ? vs[q + 1] : rgt);
                         if ((have_l && !(vs[q] > l)) || (have_r && !(vs[q] >= r))) continue;
                     }
-                    if (plane_is_peak(p, H, W, i, j, vs[q], half)) emit_peak(counts, peaks, plane, cap, vs[q], i, j);
+                    if (plane_is_peak(p, H, W, i, j, vs[q], half)) emit_peak_s(npk, peaks, plane, cap, vs[q], i, j);
                 }
             }
         }
@@ -103,9 +117,11 @@ k_nms_plane(const float *__restrict__ conf, int C, int K, int H, int W, float th
             const float v = __ldg(p + e);
             if (!(v >= thr)) continue;
             const int i = e / W, j = e - i * W;
-            if (plane_is_peak(p, H, W, i, j, v, half)) emit_peak(counts, peaks, plane, cap, v, i, j);
+            if (plane_is_peak(p, H, W, i, j, v, half)) emit_peak_s(npk, peaks, plane, cap, v, i, j);
         }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) counts[plane] = s_npk;
 }
 
 constexpr int kTH = 8;    // tile rows
