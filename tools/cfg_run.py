@@ -26,6 +26,9 @@ elif name == "c4u":
     params = pf.ParserParams(upsample=8)
 conf, paf = synth.render_batch_gpu(scenes, topo, sp)
 eng = pf.PafParser(topo)
+for kv in filter(None, __import__("os").environ.get("PF_OPTS", "").split(",")):   # e.g. PF_OPTS=9=0
+    k, v = kv.split("=")
+    eng.ctx.set_option(int(k), int(v))
 for _ in range(2):
     eng.parse_tensors(conf, paf, 8, params)
     eng.results()
