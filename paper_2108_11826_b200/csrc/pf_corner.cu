@@ -1211,7 +1211,7 @@ struct CrowdSink {
 };
 
 #ifndef PF_CROWD_MINB
-#define PF_CROWD_MINB 3
+#define PF_CROWD_MINB 4   // 64 registers (128 B spill): C3 Mode U 0.507 -> 0.494 ms vs 3; 2: 0.639
 #endif
 __global__ void __launch_bounds__(kFinThreads, PF_CROWD_MINB)
 k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
