@@ -821,6 +821,12 @@ constexpr int kScanCrowd = 64;       // more survivors than this: k_corner_crowd
 #ifndef PF_SCAN_STAGES
 #define PF_SCAN_STAGES 1
 #endif
+#ifndef PF_SCAN_B_FAST
+#define PF_SCAN_B_FAST 1   // unguarded hot-list writes when the run fits: scan 0.578 -> 0.545 ms
+#endif
+#ifndef PF_SCAN_A_LANE0
+#define PF_SCAN_A_LANE0 1   // ballot words stored by lane 0: scan 0.596 -> 0.575 ms (fewer selects per word)
+#endif
 
 struct ScanLayout {
     int plane_floats;
@@ -905,6 +911,14 @@ k_nms_up_scan(const UpCornerArgs a)
                 const int c = (j << 5) + lane;
                 v[j] = (j < NWS - 1 || c < w) ? row[c] : -INFINITY;
             }
+#if PF_SCAN_A_LANE0
+            uint32_t *hr = hot + (r + 1) * nws;
+#pragma unroll
+            for (int j = 0; j < NWS; ++j) {
+                const uint32_t word = __ballot_sync(0xffffffffu, v[j] >= a.thr);
+                if (lane == 0) hr[j] = word;
+            }
+#else
             uint32_t mine = 0u;
 #pragma unroll
             for (int j = 0; j < NWS; ++j) {
@@ -912,6 +926,7 @@ k_nms_up_scan(const UpCornerArgs a)
                 if (lane == j) mine = word;
             }
             if (lane < nws) hot[(r + 1) * nws + lane] = mine;
+#endif
         }
         __syncthreads();
         // (B) hot cells
@@ -919,7 +934,18 @@ k_nms_up_scan(const UpCornerArgs a)
             const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;   // exact for t < 2^16
             uint32_t c = cell_word(hot, nws, p, j);
             if (c) {
-                int slot = atomicAdd(&n_hot, __popc(c));
+                const int nb = __popc(c);
+                int slot = atomicAdd(&n_hot, nb);
+                const uint32_t base = (uint32_t(p) << 8) | uint32_t(j << 5);   // (p << 8) | q, q = 32 j + bit
+#if PF_SCAN_B_FAST
+                if (slot + nb <= kCornerList) {
+                    uint16_t *dst = list + slot;
+                    while (c) {
+                        *dst++ = uint16_t(base + uint32_t(__ffs(c) - 1));
+                        c &= c - 1u;
+                    }
+                } else
+#endif
                 while (c) {
                     const int q = (j << 5) + __ffs(c) - 1;
                     c &= c - 1u;
