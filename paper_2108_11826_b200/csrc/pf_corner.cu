@@ -515,9 +515,9 @@ __device__ __forceinline__ void fill_band(const AxisTab &tab, const double *dt, 
 // (row-aligned words; guard rows -1 and h are zero) the cell word is
 // M | M << 1 plus bit 31 of the previous word.  Source bits stop at column
 // w-1, so cell bits stop at q = w (band count w + 1) by themselves.
-__device__ __forceinline__ uint32_t cell_word(const uint32_t *R, int nws, int p, int j)
+__device__ __forceinline__ uint32_t cell_word(const uint32_t *R, int nws, int p, int j, int stride)
 {
-    const uint32_t *r0 = R + p * nws, *r1 = r0 + nws;    // rows p-1, p (guard-offset by one row)
+    const uint32_t *r0 = R + p * stride, *r1 = r0 + stride;   // rows p-1, p (guard-offset by one row)
     const uint32_t m = j < nws ? (r0[j] | r1[j]) : 0u;
     const uint32_t cin = j > 0 ? (r0[j - 1] | r1[j - 1]) >> 31 : 0u;
     return m | (m << 1) | cin;
@@ -533,7 +533,7 @@ __device__ __noinline__ void redo_plane(const UpCornerArgs &a, const Bands &bd, 
     const int nws = (a.w + 31) >> 5, nwc = (a.w + 32) >> 5;
     for (int t = threadIdx.x; t < a.nbr * nwc; t += kCornerThreads) {
         const int p = t / nwc, j = t - p * nwc;
-        uint32_t c = cell_word(R, nws, p, j);
+        uint32_t c = cell_word(R, nws, p, j, nws);
         while (c) {
             const int q = (j << 5) + __ffs(c) - 1;
             c &= c - 1u;
@@ -658,7 +658,7 @@ k_nms_up_corner(const __grid_constant__ UpCornerArgs a)
         // ---- (B) hot cells, one (band row, 32 cells) word per task
         for (int t = threadIdx.x; t < nbr * nwc; t += kCornerThreads) {
             const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;   // exact for t < 2^16
-            uint32_t c = cell_word(hot, nws, p, j);
+            uint32_t c = cell_word(hot, nws, p, j, nws);
             if (c) {
                 int slot = atomicAdd(&n_hot, __popc(c));
                 while (c) {
@@ -683,7 +683,7 @@ k_nms_up_corner(const __grid_constant__ UpCornerArgs a)
             // walks the hot cells of its (band row, 32 cells) words itself
             for (int t = threadIdx.x; t < nbr * nwc; t += kCornerThreads) {
                 const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;
-                uint32_t c = cell_word(hot, nws, p, j);
+                uint32_t c = cell_word(hot, nws, p, j, nws);
                 while (c) {
                     const int q = (j << 5) + __ffs(c) - 1;
                     c &= c - 1u;
@@ -824,9 +824,6 @@ constexpr int kScanCrowd = 64;       // more survivors than this: k_corner_crowd
 #ifndef PF_SCAN_B_FAST
 #define PF_SCAN_B_FAST 1   // unguarded hot-list writes when the run fits: scan 0.578 -> 0.545 ms
 #endif
-#ifndef PF_SCAN_A_LANE0
-#define PF_SCAN_A_LANE0 1   // ballot words stored by lane 0: scan 0.596 -> 0.575 ms (fewer selects per word)
-#endif
 
 struct ScanLayout {
     int plane_floats;
@@ -841,7 +838,7 @@ __host__ __device__ inline ScanLayout scan_layout(int h, int w, int nst)
     L.planes = o; o += (size_t)nst * L.plane_floats * sizeof(float);
     L.bars = o;   o += (size_t)nst * 8;
     o = (o + 15) & ~(size_t)15;
-    L.hot = o;    o += (size_t)(h + 2) * ((w + 31) >> 5) * sizeof(uint32_t);
+    L.hot = o;    o += (size_t)(h + 2) * ((((w + 31) >> 5) + 3) & ~3) * sizeof(uint32_t);   // rows padded to 16 B
     L.list = o;   o += (size_t)kCornerList * sizeof(uint16_t);
     L.total = (o + 15) & ~(size_t)15;
     return L;
@@ -865,12 +862,13 @@ k_nms_up_scan(const UpCornerArgs a)
     const int P = a.B * a.K;
     const uint32_t plane_bytes = (uint32_t)hw * 4u;
     constexpr int nws = NWS;
+    constexpr int hs = (NWS + 3) & ~3;                   // hot-row stride: one 16-byte store per row
     const int nwc = (w + 32) >> 5;
     const float inv_nwc = 1.0f / (float)nwc;
 
-    for (int e = threadIdx.x; e < nws; e += kScanThreads) {
+    for (int e = threadIdx.x; e < hs; e += kScanThreads) {
         hot[e] = 0u;
-        hot[(h + 1) * nws + e] = 0u;
+        hot[(h + 1) * hs + e] = 0u;
     }
     if (threadIdx.x == 0) {
         n_hot = 0;
@@ -911,28 +909,20 @@ k_nms_up_scan(const UpCornerArgs a)
                 const int c = (j << 5) + lane;
                 v[j] = (j < NWS - 1 || c < w) ? row[c] : -INFINITY;
             }
-#if PF_SCAN_A_LANE0
-            uint32_t *hr = hot + (r + 1) * nws;
+            uint32_t wd[hs];
 #pragma unroll
-            for (int j = 0; j < NWS; ++j) {
-                const uint32_t word = __ballot_sync(0xffffffffu, v[j] >= a.thr);
-                if (lane == 0) hr[j] = word;
-            }
-#else
-            uint32_t mine = 0u;
+            for (int j = 0; j < hs; ++j) wd[j] = j < NWS ? __ballot_sync(0xffffffffu, v[j < NWS ? j : 0] >= a.thr) : 0u;
+            if (lane == 0) {                              // the row's words in one or two 16-byte stores
+                uint4 *hr = reinterpret_cast<uint4 *>(hot + (r + 1) * hs);
 #pragma unroll
-            for (int j = 0; j < NWS; ++j) {
-                const uint32_t word = __ballot_sync(0xffffffffu, v[j] >= a.thr);
-                if (lane == j) mine = word;
+                for (int q = 0; q < hs / 4; ++q) hr[q] = make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
             }
-            if (lane < nws) hot[(r + 1) * nws + lane] = mine;
-#endif
         }
         __syncthreads();
         // (B) hot cells
         for (int t = threadIdx.x; t < nbr * nwc; t += kScanThreads) {
             const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;   // exact for t < 2^16
-            uint32_t c = cell_word(hot, nws, p, j);
+            uint32_t c = cell_word(hot, nws, p, j, hs);
             if (c) {
                 const int nb = __popc(c);
                 int slot = atomicAdd(&n_hot, nb);
@@ -982,7 +972,7 @@ k_nms_up_scan(const UpCornerArgs a)
             // hot cells of its (band row, 32 cells) words itself
             for (int t = threadIdx.x; t < nbr * nwc; t += kScanThreads) {
                 const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;
-                uint32_t c = cell_word(hot, nws, p, j);
+                uint32_t c = cell_word(hot, nws, p, j, hs);
                 while (c) {
                     const int q = (j << 5) + __ffs(c) - 1;
                     c &= c - 1u;
@@ -1296,7 +1286,7 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
         __syncthreads();
         for (int t = threadIdx.x; t < nbr * nwc; t += kFinThreads) {
             const int p = t / nwc, j = t - p * nwc;
-            uint32_t c = cell_word(hot, nws, p, j);
+            uint32_t c = cell_word(hot, nws, p, j, nws);
             if (c) {
                 int slot = atomicAdd(&n_hot, __popc(c));
                 while (c) {
@@ -1343,7 +1333,7 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
         } else {
             for (int t = threadIdx.x; t < nbr * nwc; t += kFinThreads) {
                 const int p = t / nwc, j = t - p * nwc;
-                uint32_t c = cell_word(hot, nws, p, j);
+                uint32_t c = cell_word(hot, nws, p, j, nws);
                 while (c) {
                     const int q = (j << 5) + __ffs(c) - 1;
                     c &= c - 1u;
