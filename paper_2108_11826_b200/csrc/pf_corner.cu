@@ -900,22 +900,24 @@ k_nms_up_scan(const UpCornerArgs a)
             for (int e = threadIdx.x; e < hw; e += kScanThreads) S[e] = __ldg(src + e);
             __syncthreads();
         }
-        // (A) row-aligned hot words
-        for (int r = warp; r < h; r += kScanThreads / kWarp) {
-            const float *row = S + r * w;
-            float v[NWS];
+        // (A) row-aligned hot words (row and hot-row pointers stepped, not
+        // recomputed: this loop is a third of the kernel's instructions)
+        {
+            constexpr int kRowStep = kScanThreads / kWarp;
+            const float *row = S + warp * w + lane;
+            uint4 *hr = reinterpret_cast<uint4 *>(hot + (warp + 1) * hs);
+            const bool tail = (((NWS - 1) << 5) + lane) < w;      // the last word's column exists
+            for (int r = warp; r < h; r += kRowStep, row += kRowStep * w, hr += kRowStep * hs / 4) {
+                float v[NWS];
 #pragma unroll
-            for (int j = 0; j < NWS; ++j) {
-                const int c = (j << 5) + lane;
-                v[j] = (j < NWS - 1 || c < w) ? row[c] : -INFINITY;
-            }
-            uint32_t wd[hs];
+                for (int j = 0; j < NWS; ++j) v[j] = (j < NWS - 1 || tail) ? row[j << 5] : -INFINITY;
+                uint32_t wd[hs];
 #pragma unroll
-            for (int j = 0; j < hs; ++j) wd[j] = j < NWS ? __ballot_sync(0xffffffffu, v[j < NWS ? j : 0] >= a.thr) : 0u;
-            if (lane == 0) {                              // the row's words in one or two 16-byte stores
-                uint4 *hr = reinterpret_cast<uint4 *>(hot + (r + 1) * hs);
+                for (int j = 0; j < hs; ++j) wd[j] = j < NWS ? __ballot_sync(0xffffffffu, v[j < NWS ? j : 0] >= a.thr) : 0u;
+                if (lane == 0) {                          // the row's words in one or two 16-byte stores
 #pragma unroll
-                for (int q = 0; q < hs / 4; ++q) hr[q] = make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
+                    for (int q = 0; q < hs / 4; ++q) hr[q] = make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
+                }
             }
         }
         __syncthreads();
