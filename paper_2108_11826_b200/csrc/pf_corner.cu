@@ -1121,7 +1121,11 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
     uint32_t *wc = candw + grp * kFinCands;
     const CandList cl{wc, &n_cand[grp], kFinCands, nullptr, 0};
     const int P = a.B * a.K;
-    for (int plane = blockIdx.x * kFinGroups + grp; plane < P; plane += gridDim.x * kFinGroups) {
+    // (frame, part) of the plane stepped alongside it: no division per plane
+    const int p0 = blockIdx.x * kFinGroups + grp, pstep = gridDim.x * kFinGroups;
+    const int fstep = pstep / a.K, kstep = pstep - fstep * a.K;
+    int fb = p0 / a.K, k = p0 - fb * a.K;
+    for (int plane = p0; plane < P; plane += pstep, fb += fstep, k += kstep, fb += k >= a.K, k -= k >= a.K ? a.K : 0) {
         const int ns = __ldcg(a.surv_n + plane);
         if (ns < 0) continue;   // -1: k_nms_up_corner finished it; -2: crowded (k_corner_crowded); group-uniform
 #ifdef PF_FIN_PROF
@@ -1129,7 +1133,6 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
 #endif
         if (gl == 0) { n_cand[grp] = 0; n_pk[grp] = 0; }
         __syncwarp(gmask);
-        const int fb = plane / a.K, k = plane - fb * a.K;
         const float *S = a.conf + ((size_t)fb * a.C + k) * (size_t)a.h * a.w;
         const uint32_t *sv = a.surv_out + (size_t)plane * kCornerSurv;
         for (int i = gl; i < ns; i += kFinGroup) {
