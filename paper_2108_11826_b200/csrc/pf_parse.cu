@@ -936,6 +936,9 @@ k_pair_scan(const ParseArgs a, int B)
     if (threadIdx.x == 0) *a.pair_total = carry;
 }
 
+#ifndef PF_SCORE_BSEARCH
+#define PF_SCORE_BSEARCH 1
+#endif
 #ifndef PF_SCORE_MINB
 #define PF_SCORE_MINB 4   // 64 registers: 0.27 ms; 79 (1): 0.315, 48 (5): 0.318, 40 (6): 0.386
 #endif
@@ -973,8 +976,18 @@ k_score_pairs(const ParseArgs a, int B)
         while (b + 1 < B && __ldg(a.pair_base + b + 1) <= g) ++b;
         const int local0 = (int)(g - __ldg(a.pair_base + b));
         const int *pp = a.pair_pp + (size_t)b * (L + 1);
+        // the pair's limb: the last l with pp[l] <= local0 (binary search over
+        // the L + 1 prefix entries instead of a linear walk of dependent loads)
         int l = 0;
+#if PF_SCORE_BSEARCH
+        for (int hi = L; hi - l > 1;) {
+            const int mid = (l + hi) >> 1;
+            if (__ldg(pp + mid) <= local0) l = mid;
+            else hi = mid;
+        }
+#else
         while (local0 >= __ldg(pp + l + 1)) ++l;
+#endif
         const int *base = a.pk_base + (size_t)b * (K + 1);
         const int pa_part = a.topo.la[l], pb_part = a.topo.lb[l];
         const int nb = __ldg(base + pb_part + 1) - __ldg(base + pb_part);
