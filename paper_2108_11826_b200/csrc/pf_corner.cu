@@ -1260,6 +1260,7 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
     }
     const Bands bd{RB, CB, RT, CT};
     const int nws = (w + 31) >> 5, nwc = (w + 32) >> 5;
+    const float inv_nwc = 1.0f / (float)nwc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < nws; e += kFinThreads) {
         hot[e] = 0u;                                     // guard rows -1 and h
@@ -1290,7 +1291,7 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
         }
         __syncthreads();
         for (int t = threadIdx.x; t < nbr * nwc; t += kFinThreads) {
-            const int p = t / nwc, j = t - p * nwc;
+            const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;   // exact for t < 2^16
             uint32_t c = cell_word(hot, nws, p, j, nws);
             if (c) {
                 int slot = atomicAdd(&n_hot, __popc(c));
@@ -1337,7 +1338,7 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
             }
         } else {
             for (int t = threadIdx.x; t < nbr * nwc; t += kFinThreads) {
-                const int p = t / nwc, j = t - p * nwc;
+                const int p = (int)(((float)t + 0.5f) * inv_nwc), j = t - p * nwc;
                 uint32_t c = cell_word(hot, nws, p, j, nws);
                 while (c) {
                     const int q = (j << 5) + __ffs(c) - 1;
@@ -1362,14 +1363,16 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
             const int4 rb = bd.rb[int(pq >> 16)], cb = bd.cb[int(pq & 0xffffu)];
             const int y0 = rb.x - 1, x0 = cb.x - 1;
             const int bh = rb.y - rb.x + 3, bw = cb.y - cb.x + 3;
+            // row of e by a float reciprocal, exact for e < 2^16 (no integer division per pixel)
+            const float inv_bw = 1.0f / (float)bw, inv_cw = 1.0f / (float)(bw - 2);
             for (int e = lane; e < bh * bw; e += kWarp) {
-                const int yy = e / bw, xx = e - yy * bw;
+                const int yy = (int)(((float)e + 0.5f) * inv_bw), xx = e - yy * bw;
                 vb[e] = exact_value(a, S, y0 + yy, x0 + xx);          // -inf off the grid
             }
             __syncwarp();
             const int ch = bh - 2, cw = bw - 2;
             for (int e = lane; e < ch * cw; e += kWarp) {
-                const int yy = e / cw + 1, xx = e - (yy - 1) * cw + 1;
+                const int yy = (int)(((float)e + 0.5f) * inv_cw) + 1, xx = e - (yy - 1) * cw + 1;
                 const float *c = vb + yy * bw + xx;
                 const float v = c[0];
                 // paf.py:95-99: earlier neighbours strictly, later ones non-strictly

@@ -811,61 +811,74 @@ k_parse_crowd(const ParseArgs a)
 //                    (score_pair), gated candidates appended to the frame's
 //                    list in HBM (order irrelevant: the finish step sorts);
 //   k_parse_frames<true> — steps 4-7 per frame.
-constexpr int kPeakFrames = 4;       // frames (warps) per k_parse_peaks CTA
+constexpr int kPeakWarps = 4;        // warps per k_parse_peaks CTA
 constexpr int kScoreThreads = 256;
 
-__global__ void __launch_bounds__(kPeakFrames * kWarp)
+// WPF warps per frame, kPeakWarps / WPF frames per CTA.  Large batches keep a
+// warp per frame (WPF = 1); batches of at most a few frames per SM (C3's 256
+// crowded frames: ≈720 peaks per frame, 22 rank loops of ≈40 peaks per
+// lane at WPF = 1) spread each frame's rank sort over the CTA (WPF = 4).
+template <int WPF>
+__global__ void __launch_bounds__(kPeakWarps * kWarp)
 k_parse_peaks(const ParseArgs a, int B)
 {
+    constexpr int kFrames = kPeakWarps / WPF;
     const int K = a.topo.K, L = a.topo.L;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.x * kPeakFrames + warp;
-    __shared__ int s_base[kPeakFrames][PF_MAX_KEYPOINTS + 1];
+    const int fw = warp / WPF, sub = warp - fw * WPF;    // frame slot in the CTA, warp within the frame
+    const int b = blockIdx.x * kFrames + fw;
+    __shared__ int s_base[kFrames][PF_MAX_KEYPOINTS + 1];
+    __shared__ int s_err[kFrames];
     pdl_trigger();
     pdl_wait();                                          // the NMS slabs
-    if (b >= B) return;
+    const bool live = b < B;                             // no early return: the CTA meets at one barrier
     const int gframe = a.frame_base + b;
-    int c = 0;
-    if (lane < K) {
-        c = a.counts[(size_t)b * K + lane];
-        a.counts[(size_t)b * K + lane] = 0;               // ready for the next launch
-    }
-    int incl = c;
-#pragma unroll
-    for (int d = 1; d < kWarp; d <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += v;
-    }
-    const int P = __shfl_sync(0xffffffffu, incl, K - 1);
-    const uint32_t over = __ballot_sync(0xffffffffu, lane < K && c > a.cap_part);
-    int err = 0, val = 0;
-    if (over) { err = kCapPart; val = __shfl_sync(0xffffffffu, c, __ffs(over) - 1); }
-    else if (P > a.cap_frame) { err = kCapFrame; val = P; }
-    {   // exclusive prefix: s_base[k] = incl of lane k - 1 (every lane takes part in the shuffle)
-        const int prev = __shfl_sync(0xffffffffu, incl, min(max(lane - 1, 0), 31));
-        if (lane <= K) s_base[warp][lane] = lane == 0 ? 0 : prev;
-        if (lane == 0 && K == kWarp) s_base[warp][K] = P;   // K = 32: the total has no lane of its own
-    }
-    __syncwarp();
-    if (lane == 0) {
-        a.ferr[b] = make_int2(err, val);
-        a.cand_n[b] = 0;
-    }
-    if (err) {
-        if (lane == 0) {
-            a.n_pairs[b] = 0;
-            if (a.debug) { a.dbg_npeaks[gframe] = 0; a.dbg_nconns[gframe] = 0; }
+    if (live && sub == 0) {
+        int c = 0;
+        if (lane < K) {
+            c = a.counts[(size_t)b * K + lane];
+            a.counts[(size_t)b * K + lane] = 0;           // ready for the next launch
         }
-        return;
+        int incl = c;
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const int P = __shfl_sync(0xffffffffu, incl, K - 1);
+        const uint32_t over = __ballot_sync(0xffffffffu, lane < K && c > a.cap_part);
+        int err = 0, val = 0;
+        if (over) { err = kCapPart; val = __shfl_sync(0xffffffffu, c, __ffs(over) - 1); }
+        else if (P > a.cap_frame) { err = kCapFrame; val = P; }
+        {   // exclusive prefix: s_base[k] = incl of lane k - 1 (every lane takes part in the shuffle)
+            const int prev = __shfl_sync(0xffffffffu, incl, min(max(lane - 1, 0), 31));
+            if (lane <= K) s_base[fw][lane] = lane == 0 ? 0 : prev;
+            if (lane == 0 && K == kWarp) s_base[fw][K] = P;   // K = 32: the total has no lane of its own
+        }
+        if (lane == 0) {
+            s_err[fw] = err;
+            a.ferr[b] = make_int2(err, val);
+            a.cand_n[b] = 0;
+            if (err) {
+                a.n_pairs[b] = 0;
+                if (a.debug) { a.dbg_npeaks[gframe] = 0; a.dbg_nconns[gframe] = 0; }
+            }
+        }
     }
-    for (int k = lane; k <= K; k += kWarp) a.pk_base[(size_t)b * (K + 1) + k] = s_base[warp][k];
+    if (WPF > 1) __syncthreads();
+    else __syncwarp();
+    if (!live || s_err[fw]) return;
+    const int *sb = s_base[fw];
+    const int P = sb[K];
+    if (sub == 0)
+        for (int k = lane; k <= K; k += kWarp) a.pk_base[(size_t)b * (K + 1) + k] = sb[k];
     // rank sort of each part's peaks by (score desc, cell asc) straight from the slab
-    for (int e = lane; e < P; e += kWarp) {
+    for (int e = sub * kWarp + lane; e < P; e += WPF * kWarp) {
         int part = 0;
-        while (e >= s_base[warp][part + 1]) ++part;
+        while (e >= sb[part + 1]) ++part;
         const uint2 *slab = a.peaks + ((size_t)b * K + part) * a.cap_part;
-        const int np = s_base[warp][part + 1] - s_base[warp][part];
-        const uint2 v = __ldg(slab + (e - s_base[warp][part]));
+        const int np = sb[part + 1] - sb[part];
+        const uint2 v = __ldg(slab + (e - sb[part]));
         const float vs = __uint_as_float(v.x);
         int rank = 0;
         for (int q = 0; q < np; ++q) {
@@ -873,21 +886,21 @@ k_parse_peaks(const ParseArgs a, int B)
             const float us = __uint_as_float(u.x);
             rank += (us > vs) || (us == vs && u.y < v.y);
         }
-        const size_t o = (size_t)b * a.cap_frame + s_base[warp][part] + rank;
+        const size_t o = (size_t)b * a.cap_frame + sb[part] + rank;
         a.pk_cell[o] = v.y;
         a.pk_score[o] = vs;
         if (a.debug)
-            a.dbg_peaks[(size_t)gframe * a.cap_frame + s_base[warp][part] + rank] =
+            a.dbg_peaks[(size_t)gframe * a.cap_frame + sb[part] + rank] =
                 make_int4(part, int(v.y >> 16), int(v.y & 0xffff), __float_as_int(vs));
     }
-    if (lane == 0) {
+    if (sub == 0 && lane == 0) {
         if (a.debug) a.dbg_npeaks[gframe] = P;
         int acc = 0;
         int *pp = a.pair_pp + (size_t)b * (L + 1);
         for (int l = 0; l < L; ++l) {
             pp[l] = acc;
-            const int na = s_base[warp][a.topo.la[l] + 1] - s_base[warp][a.topo.la[l]];
-            const int nb = s_base[warp][a.topo.lb[l] + 1] - s_base[warp][a.topo.lb[l]];
+            const int na = sb[a.topo.la[l] + 1] - sb[a.topo.la[l]];
+            const int nb = sb[a.topo.lb[l] + 1] - sb[a.topo.lb[l]];
             acc += na * nb;
         }
         pp[L] = acc;
@@ -1060,11 +1073,24 @@ cudaError_t launch_parse_frames(const ParseArgs &a, int B, int threads, size_t s
     return cudaGetLastError();
 }
 
+#ifndef PF_PEAK_WPF_FRAMES_PER_SM
+#define PF_PEAK_WPF_FRAMES_PER_SM 4
+#endif
+constexpr int kPeakWpfMaxFramesPerSm = PF_PEAK_WPF_FRAMES_PER_SM;
+
 cudaError_t launch_parse_peaks(const ParseArgs &a, int B, cudaStream_t s)
 {
     if (B == 0) return cudaSuccess;
-    cudaError_t e = launch_pdl(kPdlParsePeaks, k_parse_peaks, dim3((B + kPeakFrames - 1) / kPeakFrames), dim3(kPeakFrames * kWarp), 0,
-                               s, a, B);
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    // a CTA per frame while the batch leaves SMs short of warps (kPeakWpfMaxFramesPerSm)
+    if (B <= kPeakWpfMaxFramesPerSm * sms)
+        e = launch_pdl(kPdlParsePeaks, k_parse_peaks<kPeakWarps>, dim3(B), dim3(kPeakWarps * kWarp), 0, s, a, B);
+    else
+        e = launch_pdl(kPdlParsePeaks, k_parse_peaks<1>, dim3((B + kPeakWarps - 1) / kPeakWarps), dim3(kPeakWarps * kWarp), 0,
+                       s, a, B);
     if (e != cudaSuccess) return e;
     return launch_pdl(kPdlPairScan, k_pair_scan, dim3(1), dim3(1024), 0, s, a, B);
 }
