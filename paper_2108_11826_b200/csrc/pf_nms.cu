@@ -23,6 +23,10 @@
 
 namespace pf {
 
+#ifndef PF_NMS_STAGE
+#define PF_NMS_STAGE 1
+#endif
+
 __device__ __forceinline__ bool plane_is_peak(const float *__restrict__ p, int H, int W,
                                               int i, int j, float v, int half)
 {
@@ -119,6 +123,64 @@ k_nms_plane(const float *__restrict__ conf, int C, int K, int H, int W, float th
             const int i = e / W, j = e - i * W;
             if (plane_is_peak(p, H, W, i, j, v, half)) emit_peak_s(npk, peaks, plane, cap, v, i, j);
         }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) counts[plane] = s_npk;
+}
+
+// Small planes (Mode R feature grids, <= kNmsStageBytes): the plane is
+// staged in shared memory with 16-byte loads, then every cell >= thr reads
+// its neighbours from there — no L1 round trip per neighbour and no integer
+// division per hot cell (crowded Mode R planes are mostly hot).  Same
+// predicate (nms_beats, -inf outside the plane) as k_nms_plane.
+constexpr int kNmsStageBytes = 24 * 1024;
+
+__global__ void __launch_bounds__(256)
+k_nms_plane_s(const float *__restrict__ conf, int C, int K, int H, int W, float thr, int half,
+              int cap, int *__restrict__ counts, uint2 *__restrict__ peaks)
+{
+    extern __shared__ __align__(16) float sp[];
+    __shared__ int s_npk;
+    if (threadIdx.x == 0) s_npk = 0;
+    const int plane = blockIdx.x;
+    const int b = plane / K, k = plane - b * K;
+    const float *p = conf + ((size_t)b * C + k) * (size_t)H * W;
+    const int HW = H * W;
+    if ((HW & 3) == 0 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        const float4 *p4 = reinterpret_cast<const float4 *>(p);
+        float4 *s4 = reinterpret_cast<float4 *>(sp);
+        for (int e4 = threadIdx.x; e4 < (HW >> 2); e4 += blockDim.x) s4[e4] = __ldg(p4 + e4);
+    } else {
+        for (int e = threadIdx.x; e < HW; e += blockDim.x) sp[e] = __ldg(p + e);
+    }
+    __syncthreads();
+    const float inv_w = 1.0f / (float)W;
+    for (int e = threadIdx.x; e < HW; e += blockDim.x) {
+        const float v = sp[e];
+        if (!(v >= thr)) continue;
+        const int i = (int)(((float)e + 0.5f) * inv_w), j = e - i * W;   // exact: HW < 2^16
+        bool peak = true;
+        if (half == 1) {
+            // 3x3 unrolled (nms_beats: the row above and the left neighbour
+            // strictly, the right neighbour and the row below non-strictly)
+            const float *c = sp + e;
+            const bool lf = j > 0, rt = j < W - 1;
+            peak = (!lf || v > c[-1]) && (!rt || v >= c[1]);
+            if (peak && i > 0) peak = (!lf || v > c[-W - 1]) && v > c[-W] && (!rt || v > c[-W + 1]);
+            if (peak && i < H - 1) peak = (!lf || v >= c[W - 1]) && v >= c[W] && (!rt || v >= c[W + 1]);
+            if (peak) emit_peak_s(&s_npk, peaks, plane, cap, v, i, j);
+            continue;
+        }
+        for (int di = -half; di <= half && peak; ++di) {
+            const int ni = i + di;
+            if (ni < 0 || ni >= H) continue;
+            for (int dj = -half; dj <= half; ++dj) {
+                const int nj = j + dj;
+                if ((di | dj) == 0 || nj < 0 || nj >= W) continue;
+                if (!nms_beats(v, sp[ni * W + nj], di, dj)) { peak = false; break; }
+            }
+        }
+        if (peak) emit_peak_s(&s_npk, peaks, plane, cap, v, i, j);
     }
     __syncthreads();
     if (threadIdx.x == 0) counts[plane] = s_npk;
@@ -229,6 +291,13 @@ cudaError_t launch_nms_plane(const float *conf, int B, int C, int K, int H, int 
                              int half, int cap, int *counts, uint2 *peaks, cudaStream_t s)
 {
     if (B * K == 0) return cudaSuccess;
+#if PF_NMS_STAGE
+    const size_t bytes = (size_t)H * W * sizeof(float);
+    if (bytes <= (size_t)kNmsStageBytes) {
+        k_nms_plane_s<<<B * K, 256, bytes, s>>>(conf, C, K, H, W, thr, half, cap, counts, peaks);
+        return cudaGetLastError();
+    }
+#endif
     k_nms_plane<<<B * K, 256, 0, s>>>(conf, C, K, H, W, thr, half, cap, counts, peaks);
     return cudaGetLastError();
 }

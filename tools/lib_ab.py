@@ -19,13 +19,14 @@ from support import synth
 topo = pf.load_topology("coco18")
 sp = synth.SynthParams()
 out = {}
-for name in ("c5", "c3u"):
+import os
+for name in os.environ.get("PF_AB_CFGS", "c5,c3u").split(","):
     if name == "c5":
         scenes = [synth.procedural_scene(5, s, 656, 368, sp) for s in range(8192)]
     else:
         scenes = [synth.crowd_scene(42, s) for s in range(256)]
     conf, paf = synth.render_batch_gpu(scenes, topo, sp)
-    params = pf.ParserParams(upsample=8)
+    params = pf.ParserParams(upsample=1 if name == "c3r" else 8)
     eng = pf.PafParser(topo)
     for _ in range(3):
         eng.parse_tensors(conf, paf, 8, params)
