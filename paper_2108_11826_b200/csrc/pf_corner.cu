@@ -1364,7 +1364,7 @@ k_corner_crowded(const __grid_constant__ UpCornerArgs a, const CrowdLayout L)
             const int y0 = rb.x - 1, x0 = cb.x - 1;
             const int bh = rb.y - rb.x + 3, bw = cb.y - cb.x + 3;
             // row of e by a float reciprocal, exact for e < 2^16 (no integer division per pixel)
-            const float inv_bw = 1.0f / (float)bw, inv_cw = 1.0f / (float)(bw - 2);
+            const float inv_bw = __frcp_rn((float)bw), inv_cw = __frcp_rn((float)(bw - 2));   // = 1.0f / n
             for (int e = lane; e < bh * bw; e += kWarp) {
                 const int yy = (int)(((float)e + 0.5f) * inv_bw), xx = e - yy * bw;
                 vb[e] = exact_value(a, S, y0 + yy, x0 + xx);          // -inf off the grid
