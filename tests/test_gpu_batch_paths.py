@@ -51,3 +51,30 @@ def test_batch_size_paths_match_oracle_and_split(pool, n, up):
     c = conf[:n].cpu().numpy()
     p = paf[:n].cpu().numpy()
     assert [got[f] for f in idx] == oracle_records(c, p, topo, params, idx=idx)
+
+
+def test_peak_ranking_forms_agree_on_crowded_frames():
+    """k_parse_peaks ranks a frame's peaks with a warp per frame above 4
+    frames per SM and with a 4-warp CTA per frame at or below: one batch
+    just above the boundary (crowded frames every third) equals the same
+    frames parsed in small batches, and its crowded frames equal the oracle."""
+    topo = pf.load_topology("coco18")
+    n = 4 * torch.cuda.get_device_properties(0).multi_processor_count + 8
+    scenes = [synth.crowd_scene(57, s) if s % 3 == 0 else synth.procedural_scene(57, s, 656, 368, SP)
+              for s in range(n)]
+    conf, paf = synth.render_batch_gpu(scenes, topo, SP)
+    params = pf.ParserParams(upsample=8)
+    eng = pf.PafParser(topo)
+    eng.parse_tensors(conf, paf, 8, params)
+    got = _records(eng.results(), topo, n)
+    chunks = []
+    for s in range(0, n, 100):
+        eng.parse_tensors(conf[s:s + 100], paf[s:s + 100], 8, params)
+        r = eng.results()
+        chunks += [pf.pose_record(s + f, r.poses(f), topo) for f in range(min(100, n - s))]
+    eng.close()
+    assert chunks == got
+    idx = [0, 3, n // 2 - (n // 2) % 3, n - 1 - (n - 1) % 3]
+    c = conf.cpu().numpy()
+    p = paf.cpu().numpy()
+    assert [got[f] for f in idx] == oracle_records(c, p, topo, params, idx=idx)
