@@ -49,6 +49,10 @@ int g_pdl_mask = PF_PDL_DEFAULT;
 #define PF_CORNER_SPLIT_MIN_FRAMES 256   // measured: one-kernel corner faster up to 128 frames (C2 64: 113 -> 98 us), equal at 256
 #endif
 constexpr int kCornerSplitMinFrames = PF_CORNER_SPLIT_MIN_FRAMES;   // the same for the Mode U scan + finish split
+#ifndef PF_EXACT_SPLIT
+#define PF_EXACT_SPLIT 1
+#endif
+constexpr bool kExactSplit = PF_EXACT_SPLIT;   // the finish hands its exact tests to k_corner_exact
 
 namespace {
 
@@ -179,6 +183,7 @@ struct pf_ctx {
     uint32_t *d_corner_spill = nullptr;   // k_nms_up_corner candidate overflow (per resident CTA)
     uint32_t *d_surv = nullptr;           // split corner path: survivors per plane
     int *d_surv_n = nullptr;
+    uint2 *d_exact = nullptr;             // split corner path: candidates for k_corner_exact
     int *d_crowd = nullptr;                 // crowded plane list + its counter (last slot)
     size_t surv_planes = 0;
     int corner_split = PF_CORNER_SPLIT_DEFAULT;
@@ -677,18 +682,23 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
                 cudaFree(ctx->d_surv);
                 cudaFree(ctx->d_surv_n);
                 cudaFree(ctx->d_crowd);
-                ctx->d_surv = nullptr; ctx->d_surv_n = nullptr; ctx->d_crowd = nullptr;
+                cudaFree(ctx->d_exact);
+                ctx->d_surv = nullptr; ctx->d_surv_n = nullptr; ctx->d_crowd = nullptr; ctx->d_exact = nullptr;
                 ctx->surv_planes = 0;
                 CU(dev_alloc(&ctx->d_surv, planes * corner_surv_entries_per_plane()));
                 CU(dev_alloc(&ctx->d_surv_n, planes));
-                CU(dev_alloc(&ctx->d_crowd, planes + 2));   // + count + hand-out counter
+                CU(dev_alloc(&ctx->d_crowd, planes + 3));   // + count + hand-out counter + exact count
+                if (kExactSplit) CU(dev_alloc(&ctx->d_exact, planes * corner_exact_entries_per_plane()));
                 ctx->surv_planes = planes;
             }
             a.surv_out = ctx->d_surv;
             a.surv_n = ctx->d_surv_n;
             a.crowd_list = ctx->d_crowd;
             a.crowd_n = ctx->d_crowd + ctx->surv_planes;
-            CU(cudaMemsetAsync(a.crowd_n, 0, 2 * sizeof(int), s));
+            a.exact_list = ctx->d_exact;
+            a.exact_n = ctx->d_crowd + ctx->surv_planes + 2;
+            a.exact_cap = (int)std::min<size_t>(ctx->surv_planes * corner_exact_entries_per_plane(), 0x7fffffff);
+            CU(cudaMemsetAsync(a.crowd_n, 0, 3 * sizeof(int), s));
         }
         if (csplit) {
             KernelTimer kt(ctx, kNmsUpScan, 1, s);                          // streaming half
@@ -699,8 +709,12 @@ int run_chunk(pf_ctx *ctx, const float *conf, const float *paf, int n, int frame
         }
         if (csplit) {
             {
-                KernelTimer kt(ctx, kCornerFinish, 1, s);
+                KernelTimer kt(ctx, kCornerFinish, 1, s);   // classification + the exact tests handed over
                 CU(launch_corner_finish(a, s));
+                if (a.exact_list) {
+                    CU(launch_corner_exact(a, s));
+                    ctx->launches += 1;
+                }
             }
             KernelTimer kt(ctx, kCornerCrowded, 1, s);
             CU(launch_corner_crowded(a, s));
@@ -1153,7 +1167,7 @@ void pf_destroy(pf_ctx *ctx)
                    ctx->d_hscore, ctx->d_hnparts, ctx->d_kpx, ctx->d_kpy, ctx->d_kps, ctx->d_kpp,
                    ctx->d_status, ctx->d_full, ctx->d_tmp,
                    ctx->d_dbg_np, ctx->d_dbg_nc, ctx->d_dbg_ci, ctx->d_dbg_peaks, ctx->d_dbg_cd,
-                   ctx->d_corner_spill, ctx->d_paf_touch, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_pk_cell, ctx->d_pk_score,
+                   ctx->d_corner_spill, ctx->d_paf_touch, ctx->d_surv, ctx->d_surv_n, ctx->d_crowd, ctx->d_exact, ctx->d_pk_cell, ctx->d_pk_score,
                    ctx->d_pk_base, ctx->d_pair_pp, ctx->d_npairs, ctx->d_pair_base, ctx->d_ferr, ctx->d_cand_n, ctx->d_crowd_frames,
                    ctx->d_owner};
     for (void *p : dev) cudaFree(p);

@@ -1096,6 +1096,23 @@ __device__ __noinline__ void classify_inline(const UpCornerArgs &a, const Bands 
 #ifndef PF_FIN_MINB
 #define PF_FIN_MINB 4
 #endif
+#ifndef PF_EXACT_MINB
+#define PF_EXACT_MINB 4
+#endif
+
+// The exact tests of one plane's candidate list in the finish itself (the
+// k_corner_exact list was full), out of line so they do not set the finish's
+// register count.
+__device__ __noinline__ void exact_tests_here(const UpCornerArgs &a, const float *S, const uint32_t *wc, int ncd,
+                                              int gl, int plane, int *npk)
+{
+    for (int ci = gl; ci < ncd; ci += kFinGroup) {
+        const uint32_t yx = wc[ci];
+        const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
+        float v;
+        if (exact_peak_all(a, PlaneSrc{S, a.w}, y, x, v)) emit_peak_c(npk, a.peaks, plane, a.cap, v, y, x);
+    }
+}
 __global__ void __launch_bounds__(kFinThreads, PF_FIN_MINB)
 k_corner_finish(const __grid_constant__ UpCornerArgs a)
 {
@@ -1141,12 +1158,30 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
         }
         __syncwarp(gmask);
         const int ncd = n_cand[grp];
-        if (ncd <= kFinCands) {
-            for (int ci = gl; ci < ncd; ci += kFinGroup) {
-                const uint32_t yx = wc[ci];
-                const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
-                float v;
-                if (exact_peak_all(a, PlaneSrc{S, a.w}, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
+        bool handed = false;
+        if (ncd > 0 && ncd <= kFinCands && a.exact_list) {
+            // the exact tests run in k_corner_exact, a thread per candidate of
+            // the whole batch (here ≈15 candidates would fill half the lanes);
+            // a plane's candidates stay contiguous, so its sources stay in L1
+            int base = 0;
+            if (gl == 0) base = atomicAdd(a.exact_n, ncd);
+            base = __shfl_sync(gmask, base, 0);
+            handed = base + ncd <= a.exact_cap;
+            for (int ci = gl; ci < ncd; ci += kFinGroup)
+                if (base + ci < a.exact_cap) a.exact_list[base + ci] = make_uint2(handed ? uint32_t(plane) : 0xffffffffu, wc[ci]);
+        }
+        if (handed) {
+            // counts[plane] stays 0 here; k_corner_exact adds the peaks
+        } else if (ncd <= kFinCands) {
+            if (a.exact_list) {
+                exact_tests_here(a, S, wc, ncd, gl, plane, &n_pk[grp]);   // the list was full (rare)
+            } else {
+                for (int ci = gl; ci < ncd; ci += kFinGroup) {
+                    const uint32_t yx = wc[ci];
+                    const int y = (int)(yx >> 16), x = (int)(yx & 0xffffu);
+                    float v;
+                    if (exact_peak_all(a, PlaneSrc{S, a.w}, y, x, v)) emit_peak_c(&n_pk[grp], a.peaks, plane, a.cap, v, y, x);
+                }
             }
         } else {
             // candidate overflow: classify again and test each candidate on
@@ -1160,6 +1195,41 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
         if (gl == 0) a.counts[plane] = n_pk[grp];
         __syncwarp(gmask);
     }
+}
+
+// Exact 3x3 tests of the candidates k_corner_finish handed over (thread per
+// candidate, grid-stride over the batch's list); peaks are appended to the
+// plane's slab with a global counter (k_parse_peaks sorts them).  Entries
+// marked 0xffffffff belong to a plane whose range overflowed the list (that
+// plane was tested in k_corner_finish).
+constexpr int kExactPerPlane = 32;
+size_t corner_exact_entries_per_plane() { return kExactPerPlane; }
+
+__global__ void __launch_bounds__(kFinThreads, PF_EXACT_MINB)
+k_corner_exact(const __grid_constant__ UpCornerArgs a)
+{
+    const int n = min(*a.exact_n, a.exact_cap);
+    const size_t hw = (size_t)a.h * a.w;
+    for (int i = blockIdx.x * kFinThreads + threadIdx.x; i < n; i += gridDim.x * kFinThreads) {
+        const uint2 e = a.exact_list[i];
+        if (e.x == 0xffffffffu) continue;
+        const int plane = (int)e.x, fb = plane / a.K, k = plane - fb * a.K;
+        const float *S = a.conf + ((size_t)fb * a.C + k) * hw;
+        const int y = (int)(e.y >> 16), x = (int)(e.y & 0xffffu);
+        float v;
+        if (exact_peak_all(a, PlaneSrc{S, a.w}, y, x, v)) emit_peak_c(a.counts + plane, a.peaks, plane, a.cap, v, y, x);
+    }
+}
+
+cudaError_t launch_corner_exact(const UpCornerArgs &a, cudaStream_t s)
+{
+    if (!a.exact_list || (long long)a.B * a.K == 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    k_corner_exact<<<sms * PF_EXACT_MINB, kFinThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 // Crowded planes of the split path (more than kScanCrowd survivors): the

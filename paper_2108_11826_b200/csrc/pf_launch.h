@@ -111,7 +111,12 @@ struct UpCornerArgs {
     int *surv_n;                         // split mode: [B*K] survivor counts, -1 = plane finished,
                                          //   sign bit = crowded (low bits: survivors)
     int *crowd_list, *crowd_n;           // split mode: crowded planes (compact) and their count
+    uint2 *exact_list;                   // split mode: (plane, y << 16 | x) candidates for k_corner_exact (or null)
+    int *exact_n;                        //   their count (zeroed before the scan)
+    int exact_cap;
 };
+cudaError_t launch_corner_exact(const UpCornerArgs &a, cudaStream_t s);
+size_t corner_exact_entries_per_plane();
 cudaError_t launch_corner_finish(const UpCornerArgs &a, cudaStream_t s);
 cudaError_t launch_corner_crowded(const UpCornerArgs &a, cudaStream_t s);
 cudaError_t launch_nms_up_scan(const UpCornerArgs &a, cudaStream_t s);

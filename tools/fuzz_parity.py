@@ -22,7 +22,7 @@ t0 = time.time()
 cases = frames_checked = 0
 fails = []
 while time.time() - t0 < budget:
-    n = int(rng.choice([1, 3, 17, 31, 64, 148, 149, 200, 256, 300]))
+    n = int(rng.choice([1, 3, 17, 31, 64, 148, 149, 200, 256, 300, 620]))
     seed = int(rng.integers(1 << 30))
     scenes = []
     for s in range(n):
