@@ -233,6 +233,9 @@ int pf_set_debug(pf_ctx *ctx, int enable);
                                     stream beside the parse of chunk c on a second stream (the in-place
                                     PAF parse waits on PCIe read requests, the NMS stage on the SMs);
                                     0: one compute stream */
+#define PF_OPT_EXACT_LIST 17      /* split Mode U 3x3: the finish hands its candidates to k_corner_exact
+                                   * (0 = default: batches of >= 4096 planes; -1 = off: the finish tests them itself;
+                                   * N > 0 = at most N list entries, the rest tested in the finish) */
 int pf_set_option(pf_ctx *ctx, int option, int value);
 
 /* With PF_OPT_COUNT_PAF on: distinct 32-byte PAF sectors the last parse call

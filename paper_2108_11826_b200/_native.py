@@ -32,6 +32,7 @@ PF_OPT_PDL = 12
 PF_OPT_COUNT_PAF = 13
 PF_OPT_LARGE = 15
 PF_OPT_HOST_OVERLAP = 16
+PF_OPT_EXACT_LIST = 17
 PF_N_KERNELS = 17
 
 # every symbol include/pf_b200.h declares (checked by tests/test_capi_symbols.py)

@@ -78,3 +78,26 @@ def test_peak_ranking_forms_agree_on_crowded_frames():
     c = conf.cpu().numpy()
     p = paf.cpu().numpy()
     assert [got[f] for f in idx] == oracle_records(c, p, topo, params, idx=idx)
+
+
+def test_exact_list_handover_and_fallbacks(pool):
+    """Split Mode U: k_corner_finish hands each plane's candidates to
+    k_corner_exact (default); with the hand-over off, and with a list so short
+    that most planes overflow it (their candidates are tested in the finish,
+    the slots they had reserved are skipped), the poses are the same, and a
+    sample equals the oracle."""
+    topo, conf, paf = pool
+    n = 288
+    params = pf.ParserParams(upsample=8)
+    eng = pf.PafParser(topo)
+    out = []
+    for opt in (0, -1, 700, 1):
+        eng.ctx.set_option(_native.PF_OPT_EXACT_LIST, opt)
+        eng.parse_tensors(conf[:n], paf[:n], 8, params)
+        out.append(_records(eng.results(), topo, n))
+    eng.close()
+    assert out[1] == out[0] and out[2] == out[0] and out[3] == out[0]
+    idx = [0, 24, 100, 287]
+    c = conf[:n].cpu().numpy()
+    p = paf[:n].cpu().numpy()
+    assert [out[0][f] for f in idx] == oracle_records(c, p, topo, params, idx=idx)
