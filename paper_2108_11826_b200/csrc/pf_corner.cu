@@ -1096,6 +1096,9 @@ __device__ __noinline__ void classify_inline(const UpCornerArgs &a, const Bands 
 #ifndef PF_FIN_MINB
 #define PF_FIN_MINB 4
 #endif
+#ifndef PF_FIN_REVERSE
+#define PF_FIN_REVERSE 1
+#endif
 #ifndef PF_EXACT_MINB
 #define PF_EXACT_MINB 4
 #endif
@@ -1141,8 +1144,15 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
     // (frame, part) of the plane stepped alongside it: no division per plane
     const int p0 = blockIdx.x * kFinGroups + grp, pstep = gridDim.x * kFinGroups;
     const int fstep = pstep / a.K, kstep = pstep - fstep * a.K;
+#if PF_FIN_REVERSE
+    // planes from the end: the scan streamed them last, so the first ones
+    // still have their sources in L2
+    int fb = (P - 1 - p0) / a.K, k = (P - 1 - p0) - fb * a.K;
+    for (int plane = P - 1 - p0; plane >= 0; plane -= pstep, fb -= fstep, k -= kstep, fb -= k < 0, k += k < 0 ? a.K : 0) {
+#else
     int fb = p0 / a.K, k = p0 - fb * a.K;
     for (int plane = p0; plane < P; plane += pstep, fb += fstep, k += kstep, fb += k >= a.K, k -= k >= a.K ? a.K : 0) {
+#endif
         const int ns = __ldcg(a.surv_n + plane);
         if (ns < 0) continue;   // -1: k_nms_up_corner finished it; -2: crowded (k_corner_crowded); group-uniform
 #ifdef PF_FIN_PROF
@@ -1211,7 +1221,9 @@ k_corner_exact(const __grid_constant__ UpCornerArgs a)
     const int n = min(*a.exact_n, a.exact_cap);
     const size_t hw = (size_t)a.h * a.w;
     for (int i = blockIdx.x * kFinThreads + threadIdx.x; i < n; i += gridDim.x * kFinThreads) {
-        const uint2 e = a.exact_list[i];
+        // newest entries first: the planes the finish classified last are the
+        // likeliest to still have their sources in L2 (0.260 -> 0.255 ms)
+        const uint2 e = a.exact_list[n - 1 - i];
         if (e.x == 0xffffffffu) continue;
         const int plane = (int)e.x, fb = plane / a.K, k = plane - fb * a.K;
         const float *S = a.conf + ((size_t)fb * a.C + k) * hw;
