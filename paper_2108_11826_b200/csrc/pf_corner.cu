@@ -1175,7 +1175,7 @@ k_corner_finish(const __grid_constant__ UpCornerArgs a)
             // a plane's candidates stay contiguous, so its sources stay in L1
             int base = 0;
             if (gl == 0) base = atomicAdd(a.exact_n, ncd);
-            base = __shfl_sync(gmask, base, 0);
+            base = __shfl_sync(gmask, base, 0, kFinGroup);   // the group's first lane
             handed = base + ncd <= a.exact_cap;
             for (int ci = gl; ci < ncd; ci += kFinGroup)
                 if (base + ci < a.exact_cap) a.exact_list[base + ci] = make_uint2(handed ? uint32_t(plane) : 0xffffffffu, wc[ci]);
